@@ -1,0 +1,999 @@
+// host.cu -- C++ host driver and C ABI of the B200 SMC sampler.
+//
+// Mirrors the reference's host-side semantics (paths relative to the
+// reference root):
+//   validate_smc_config        proj/src/smc.cpp:23-32
+//   validate_model / _prior    proj/src/model.cpp:97-113, proj/src/priors.cpp:9-20
+//   validate_spectrum          proj/src/spectrum.cpp:12-23
+//   smc_run (level loop)       proj/src/smc.cpp:186-211, report fields :218-249
+// The level loop runs every group (one SMC run = one (spectrum, K, seed)) of
+// a batch in lock-step: per round one k_temper (1 CTA per group), one k_chain
+// move launch covering every chain of every active group (longest d first),
+// and one k_stats.  The host reads back 48 bytes of state per group per round
+// to retire groups that reached beta = 1.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/specmc_b200.h"
+#include "launch.h"
+
+namespace smc {
+namespace {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error(SPECMC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------ instrumentation
+std::mutex g_stats_mu;
+specmc_stats g_stats{0, 0.0, 0, 0.0};
+
+void count_launch(int64_t n = 1) {
+  std::lock_guard<std::mutex> lk(g_stats_mu);
+  g_stats.kernel_launches += n;
+}
+
+// ------------------------------------------------------------------ validation
+void validate_config(const specmc_smc_config& c) {  // smc.cpp:23-32
+  if (c.T < 2) throw Error(SPECMC_EINVAL, "smc: T must be >= 2");
+  if (c.n < 1) throw Error(SPECMC_EINVAL, "smc: n must be >= 1");
+  if (c.T % c.n != 0) throw Error(SPECMC_EINVAL, "smc: T must be divisible by n");
+  if (c.T / c.n < 2) throw Error(SPECMC_EINVAL, "smc: S = T/n must be >= 2");
+  if (!(c.ess_target > 0.0 && c.ess_target < 1.0)) throw Error(SPECMC_EINVAL, "smc: ess_target must lie in (0, 1)");
+  if (c.max_levels < 1) throw Error(SPECMC_EINVAL, "smc: max_levels must be >= 1");
+  if (c.workers < 0) throw Error(SPECMC_EINVAL, "smc: workers must be >= 0");
+  if (c.T > (int64_t)1 << 30) throw Error(SPECMC_EINVAL, "smc: T above 2^30 is not supported by the device path");
+}
+
+int model_dim(const specmc_model_desc& m) {  // model.cpp:86-93
+  switch (m.family) {
+    case SPECMC_FAMILY_GM: return 3 * m.K;
+    case SPECMC_FAMILY_XPS: return 4 * m.K + 2;
+    case SPECMC_FAMILY_XRD: return 9 * m.K + 4;
+    case SPECMC_FAMILY_OFFSET: return 1;
+  }
+  return -1;
+}
+
+void validate_model(const specmc_model_desc& m) {
+  if (m.family == SPECMC_FAMILY_XRD)
+    throw Error(SPECMC_EINVAL, "xrd family is not implemented on the device path yet");
+  if (m.family != SPECMC_FAMILY_GM && m.family != SPECMC_FAMILY_XPS && m.family != SPECMC_FAMILY_OFFSET)
+    throw Error(SPECMC_EINVAL, "unknown model family");
+  if (m.K < 1) throw Error(SPECMC_EINVAL, "model needs K >= 1");
+  if (m.d != model_dim(m)) throw Error(SPECMC_EINVAL, "model layout length mismatch");
+  if (!m.prior_kind || !m.prior_a || !m.prior_b) throw Error(SPECMC_EINVAL, "model priors missing");
+  for (int i = 0; i < m.d; ++i) {  // priors.cpp:9-20
+    const double a = m.prior_a[i], b = m.prior_b[i];
+    switch (m.prior_kind[i]) {
+      case SPECMC_PRIOR_NORMAL:
+        if (!(b > 0.0) || !std::isfinite(b) || !std::isfinite(a))
+          throw Error(SPECMC_EINVAL, "normal prior needs finite mean and var > 0");
+        break;
+      case SPECMC_PRIOR_GAMMA:
+        if (!(a > 0.0) || !(b > 0.0)) throw Error(SPECMC_EINVAL, "gamma prior needs shape > 0 and rate > 0");
+        break;
+      case SPECMC_PRIOR_UNIFORM:
+        if (!(a < b)) throw Error(SPECMC_EINVAL, "uniform prior needs lo < hi");
+        break;
+      default: throw Error(SPECMC_EINVAL, "unknown prior kind");
+    }
+  }
+  switch (m.noise) {  // model.cpp:14-21
+    case SPECMC_NOISE_GAUSSIAN:
+      if (!(m.noise_sigma > 0.0)) throw Error(SPECMC_EINVAL, "gaussian noise needs sigma > 0");
+      break;
+    case SPECMC_NOISE_XPS_HETERO:
+      if (m.s0 < 0.0 || m.s1 < 0.0 || m.s2 < 0.0 || (m.s0 == 0.0 && m.s1 == 0.0 && m.s2 == 0.0))
+        throw Error(SPECMC_EINVAL, "hetero noise needs sigma0,1,2 >= 0, not all zero");
+      break;
+    case SPECMC_NOISE_POISSON:
+    case SPECMC_NOISE_GAUSS_APPROX: break;
+    default: throw Error(SPECMC_EINVAL, "unknown noise kind");
+  }
+}
+
+void validate_spectrum(const double* xs, const double* ys, int64_t n, bool nonneg) {  // spectrum.cpp:12-23
+  if (!xs || !ys) throw Error(SPECMC_EINVAL, "spectrum: null data");
+  if (n < 2) throw Error(SPECMC_EINVAL, "spectrum: needs at least 2 points");
+  for (int64_t i = 0; i < n; ++i) {
+    if (!std::isfinite(xs[i]) || !std::isfinite(ys[i]))
+      throw Error(SPECMC_EINVAL, "spectrum: non-finite value at row " + std::to_string(i));
+    if (i > 0 && !(xs[i] > xs[i - 1]))
+      throw Error(SPECMC_EINVAL, "spectrum: xs not strictly increasing at row " + std::to_string(i));
+    if (nonneg && ys[i] < 0.0) throw Error(SPECMC_EINVAL, "spectrum: negative intensity at row " + std::to_string(i));
+  }
+}
+
+// location parameters (peak centres mu_k) are shifted by x_shift on the device
+bool is_location(int family, int K, int i) {
+  if (family == SPECMC_FAMILY_GM) return i % 3 == 1;
+  if (family == SPECMC_FAMILY_XPS) return i < 4 * K && i % 4 == 1;
+  return false;
+}
+
+uint64_t mix64(uint64_t z) {  // rng.hpp:11-14
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// ----------------------------------------------------------- device memory
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t b) : bytes(b) {
+    if (b) cuda_check(cudaMalloc(&p, b), "cudaMalloc");
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(bytes, o.bytes);
+    return *this;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// bump allocator over one cudaMalloc (256-byte aligned slices)
+struct Arena {
+  DevBuf buf;
+  size_t off = 0;
+  static size_t al(size_t b) { return (b + 255) & ~(size_t)255; }
+  void reserve(size_t b) { buf = DevBuf(b); }
+  template <typename T>
+  T* take(size_t count) {
+    const size_t b = al(sizeof(T) * std::max<size_t>(count, 1));
+    if (off + b > buf.bytes) throw Error(SPECMC_ECUDA, "arena overflow");
+    T* p = reinterpret_cast<T*>(static_cast<char*>(buf.p) + off);
+    off += b;
+    return p;
+  }
+};
+
+// --------------------------------------------------------- host-side prep
+struct PreparedSpectrum {
+  std::vector<float> x;
+  std::vector<float> c;  // pairs
+  std::vector<float> y;  // pairs
+  double x_shift = 0.0;
+  float x0s = 0.f, inv_range = 0.f, range = 0.f;
+  double e_a0 = 0.0, e_a1 = 0.0;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, q = 0.5f;
+  int nz = NZ_GAUSS;
+};
+
+// Lane-transposed spectrum arrays for one launch shape (see device.cuh) and the
+// noise constants of E = e_a0 + e_a1 * sum_k l_k (kernels.cu noise_term).
+PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, const double* ys, int64_t N,
+                                  const Shape& s, double x_shift) {
+  PreparedSpectrum ps;
+  const int L = 32 * s.W;
+  const size_t npt = (size_t)s.PPL * L;
+  ps.x.assign(npt, 0.f);
+  ps.c.assign(2 * npt, 0.f);
+  ps.y.assign(2 * npt, 0.f);
+  ps.x_shift = x_shift;
+  const double range = xs[N - 1] - xs[0];
+  ps.range = (float)range;
+  ps.inv_range = (float)(1.0 / range);
+  ps.x0s = (float)(xs[0] - x_shift);
+  // noise
+  std::vector<double> inv_s(N, 1.0);
+  double a0 = 0.0;
+  switch (m.noise) {
+    case SPECMC_NOISE_GAUSSIAN: {
+      const double s2 = m.noise_sigma * m.noise_sigma;
+      ps.nz = NZ_GAUSS;
+      ps.e_a0 = 0.5 * std::log(2.0 * M_PI * s2);
+      ps.e_a1 = 1.0 / (2.0 * s2 * (double)N);
+      break;
+    }
+    case SPECMC_NOISE_POISSON: {
+      ps.nz = NZ_POISSON;
+      for (int64_t i = 0; i < N; ++i)
+        if (ys[i] > 0.0) {
+          inv_s[i] = 1.0 / ys[i];
+          a0 += ys[i] - ys[i] * std::log(ys[i]);
+        }
+      ps.e_a0 = a0 / (double)N;
+      ps.e_a1 = 1.0 / (double)N;
+      break;
+    }
+    default: {
+      double h0 = 1.0, h1 = 0.0, h2 = 0.0, q = 0.5;
+      if (m.noise == SPECMC_NOISE_XPS_HETERO) {
+        h0 = m.s0 * m.s0;
+        h1 = m.s1 * m.s1;
+        h2 = m.s2 * m.s2;
+        q = m.paper_literal ? 1.0 : 0.5;
+      }
+      ps.nz = NZ_HETERO;
+      ps.a0 = (float)h0;
+      ps.a1 = (float)h1;
+      ps.a2 = (float)h2;
+      ps.q = (float)q;
+      for (int64_t i = 0; i < N; ++i) {
+        const double y = std::fabs(ys[i]);
+        double sc = h0 * y + h1 * y * y + h2;
+        if (!(sc > 0.0)) sc = 1.0;
+        inv_s[i] = 1.0 / sc;
+        a0 += 0.5 * std::log(2.0 * M_PI * sc);
+      }
+      ps.e_a0 = a0 / (double)N;
+      ps.e_a1 = 1.0 / (double)N;
+      break;
+    }
+  }
+  for (int64_t p = 0; p < N; ++p) {
+    const int lane = (int)(p / s.PPL), k = (int)(p % s.PPL);
+    const size_t idx = (size_t)k * L + lane;
+    const double hk = p > 0 ? 0.5 * (xs[p] - xs[p - 1]) : 0.0;
+    const double hk1 = p + 1 < N ? 0.5 * (xs[p + 1] - xs[p]) : 0.0;
+    ps.x[idx] = (float)(xs[p] - x_shift);
+    ps.c[2 * idx] = (float)(hk + hk1);
+    ps.c[2 * idx + 1] = (float)hk1;
+    ps.y[2 * idx] = (float)ys[p];
+    ps.y[2 * idx + 1] = (float)inv_s[p];
+  }
+  for (size_t p = N; p < npt; ++p) {  // padding lanes: masked, finite
+    const int lane = (int)(p / s.PPL), k = (int)(p % s.PPL);
+    const size_t idx = (size_t)k * L + lane;
+    ps.x[idx] = (float)(xs[N - 1] - x_shift);
+    ps.y[2 * idx] = 1.f;
+    ps.y[2 * idx + 1] = 1.f;
+  }
+  return ps;
+}
+
+double pick_shift(const specmc_model_desc& m, const double* xs, int64_t N) {
+  if (m.family != SPECMC_FAMILY_GM && m.family != SPECMC_FAMILY_XPS) return 0.0;
+  for (int i = 0; i < m.d; ++i)
+    if (is_location(m.family, m.K, i) && m.prior_kind[i] == SPECMC_PRIOR_GAMMA) return 0.0;  // not translation-safe
+  return 0.5 * (xs[0] + xs[N - 1]);
+}
+
+// ------------------------------------------------------------------ batch
+struct RunSpec {
+  specmc_model_desc m;
+  std::vector<int32_t> pk;
+  std::vector<double> pa, pb;  // shifted
+  int spectrum;
+  specmc_smc_config cfg;
+  double x_shift;
+  int64_t N;
+};
+
+struct Device {
+  int ordinal;
+  cudaStream_t stream = nullptr;
+  explicit Device(int o) : ordinal(o) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+      throw Error(SPECMC_ECUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+    if (o < 0 || o >= count) throw Error(SPECMC_ECUDA, "invalid CUDA device ordinal " + std::to_string(o));
+    cuda_check(cudaSetDevice(o), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  }
+  ~Device() {
+    if (stream) cudaStreamDestroy(stream);
+  }
+  void sync() { cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize"); }
+};
+
+template <typename T>
+void h2d(T* dst, const T* src, size_t n, cudaStream_t st) {
+  if (n) cuda_check(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, st), "H2D");
+}
+template <typename T>
+void d2h(T* dst, const T* src, size_t n, cudaStream_t st) {
+  if (n) cuda_check(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, st), "D2H");
+}
+
+struct Timer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  Timer() {
+    cuda_check(cudaEventCreate(&a), "event");
+    cuda_check(cudaEventCreate(&b), "event");
+  }
+  ~Timer() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+  float ms() {
+    float t = 0.f;
+    cuda_check(cudaEventElapsedTime(&t, a, b), "cudaEventElapsedTime");
+    return t;
+  }
+};
+
+// Runs one homogeneous class of problems (same family, same launch shape,
+// same device) to completion and fills the results.
+void run_class(Device& dev, const std::vector<RunSpec>& runs, const std::vector<specmc_spectrum>& spectra,
+               const std::vector<int>& idx, specmc_smc_result* out, double& device_seconds) {
+  const int G = (int)idx.size();
+  const specmc_model_desc& m0 = runs[idx[0]].m;
+  int64_t Nmax = 0;
+  int dmax = 1, Tmax = 0;
+  for (int r : idx) {
+    Nmax = std::max(Nmax, runs[r].N);
+    dmax = std::max(dmax, runs[r].m.d);
+    Tmax = std::max<int>(Tmax, (int)runs[r].cfg.T);
+  }
+  const Shape shape = pick_shape(Nmax);
+  if ((int64_t)32 * shape.W * shape.PPL < Nmax)
+    throw Error(SPECMC_EINVAL, "spectrum has more points than the device path supports (8192)");
+  const size_t smem = chain_smem_bytes(shape, dmax);
+  if (smem > 227 * 1024) throw Error(SPECMC_EINVAL, "model too large for the device path (shared memory)");
+
+  // spectra prepared once per (spectrum, shift) for this shape
+  std::map<std::pair<int, double>, PreparedSpectrum> prep;
+  for (int r : idx) {
+    const auto key = std::make_pair(runs[r].spectrum, runs[r].x_shift);
+    if (!prep.count(key)) {
+      const auto& sp = spectra[runs[r].spectrum];
+      prep.emplace(key, prepare_spectrum(runs[r].m, sp.xs, sp.ys, sp.n, shape, runs[r].x_shift));
+    }
+  }
+
+  // ---- sizes
+  const int L = 32 * shape.W;
+  const size_t npt = (size_t)shape.PPL * L;
+  size_t bytes = Arena::al(sizeof(GroupDesc) * G) + Arena::al(sizeof(GroupState) * G) + 4 * Arena::al(4 * (G + 1));
+  bytes += prep.size() * (Arena::al(npt * 4) + 2 * Arena::al(npt * 8));
+  for (int r : idx) {
+    const auto& R = runs[r];
+    const size_t T = R.cfg.T, d = R.m.d, S = T / R.cfg.n;
+    bytes += 3 * Arena::al(d * 8) + Arena::al(d * 4);                       // priors + ls0
+    bytes += 2 * Arena::al(d * T * 8) + 2 * Arena::al(T * 8);               // theta, E
+    bytes += Arena::al(S * 4) + Arena::al(d * S * 4) + Arena::al(d * S * 8);  // anc, chain stats
+    bytes += Arena::al(T * 8) + Arena::al(kHist * (1 + 2 * d) * 8);         // wbuf, hist
+    bytes += Arena::al((size_t)R.cfg.max_levels * 4 * 8);                  // diag
+  }
+  Arena ar;
+  ar.reserve(bytes);
+  GroupDesc* d_gds = ar.take<GroupDesc>(G);
+  GroupState* d_st = ar.take<GroupState>(G);
+  int* d_list = ar.take<int>(G + 1);
+  int* d_prefix = ar.take<int>(G + 1);
+  int* d_list_all = ar.take<int>(G + 1);
+  int* d_prefix_all = ar.take<int>(G + 1);
+  cudaStream_t st = dev.stream;
+
+  std::map<std::pair<int, double>, const PreparedSpectrum*> pmap;
+  std::map<std::pair<int, double>, std::tuple<float*, float2*, float2*>> dspec;
+  for (auto& kv : prep) {
+    float* x = ar.take<float>(npt);
+    float2* c = ar.take<float2>(npt);
+    float2* y = ar.take<float2>(npt);
+    h2d(x, kv.second.x.data(), npt, st);
+    h2d(reinterpret_cast<float*>(c), kv.second.c.data(), 2 * npt, st);
+    h2d(reinterpret_cast<float*>(y), kv.second.y.data(), 2 * npt, st);
+    dspec[kv.first] = std::make_tuple(x, c, y);
+  }
+
+  std::vector<GroupDesc> gds(G);
+  std::vector<GroupState> sts(G);
+  for (int gi = 0; gi < G; ++gi) {
+    const RunSpec& R = runs[idx[gi]];
+    const auto key = std::make_pair(R.spectrum, R.x_shift);
+    const PreparedSpectrum& ps = prep.at(key);
+    GroupDesc& g = gds[gi];
+    std::memset(&g, 0, sizeof(g));
+    g.family = R.m.family;
+    g.K = R.m.K;
+    g.d = R.m.d;
+    g.noise = ps.nz;
+    g.T = (int)R.cfg.T;
+    g.n = R.cfg.n;
+    g.S = (int)(R.cfg.T / R.cfg.n);
+    g.max_levels = R.cfg.max_levels;
+    g.ess_target = R.cfg.ess_target;
+    g.n_data = (double)R.N;
+    const uint64_t k = mix64(R.cfg.seed);
+    g.key0 = (uint32_t)k;
+    g.key1 = (uint32_t)(k >> 32);
+    g.chain_base = 0;
+    g.N = (int)R.N;
+    g.e_a0 = ps.e_a0;
+    g.e_a1 = ps.e_a1;
+    g.nz_a0 = ps.a0;
+    g.nz_a1 = ps.a1;
+    g.nz_a2 = ps.a2;
+    g.nz_q = ps.q;
+    g.x0s = ps.x0s;
+    g.inv_range = ps.inv_range;
+    g.range = ps.range;
+    g.x_shift_f = (float)R.x_shift;
+    auto t = dspec.at(key);
+    g.spec_x = std::get<0>(t);
+    g.spec_c = std::get<1>(t);
+    g.spec_y = std::get<2>(t);
+    const size_t T = R.cfg.T, d = R.m.d, S = g.S;
+    int* pk = ar.take<int>(d);
+    double* pa = ar.take<double>(d);
+    double* pb = ar.take<double>(d);
+    h2d(pk, R.pk.data(), d, st);
+    h2d(pa, R.pa.data(), d, st);
+    h2d(pb, R.pb.data(), d, st);
+    g.pkind = pk;
+    g.pa = pa;
+    g.pb = pb;
+    g.theta[0] = ar.take<double>(d * T);
+    g.theta[1] = ar.take<double>(d * T);
+    g.E[0] = ar.take<double>(T);
+    g.E[1] = ar.take<double>(T);
+    g.anc = ar.take<int>(S);
+    g.ls0 = ar.take<double>(d);
+    g.chain_acc = ar.take<int>(d * S);
+    g.chain_ls = ar.take<double>(d * S);
+    g.wbuf = ar.take<double>(T);
+    g.hist = ar.take<double>(kHist * (1 + 2 * d));
+    g.diag = ar.take<double>((size_t)R.cfg.max_levels * 4);
+    g.st = d_st + gi;
+    GroupState& s = sts[gi];
+    std::memset(&s, 0, sizeof(s));
+    s.active = 1;
+  }
+  h2d(d_gds, gds.data(), G, st);
+  h2d(d_st, sts.data(), G, st);
+
+  // longest chains first (d descending) so the move grid drains in LPT order
+  std::vector<int> order(G);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return gds[a].d > gds[b].d; });
+
+  auto build_list = [&](const std::vector<int>& groups, bool energy, std::vector<int>& list,
+                        std::vector<int>& prefix) -> int {
+    list.clear();
+    prefix.clear();
+    int total = 0;
+    for (int gi : groups) {
+      list.push_back(gi);
+      prefix.push_back(total);
+      const int units = energy ? gds[gi].T : gds[gi].S;
+      total += (units + shape.U - 1) / shape.U;
+    }
+    prefix.push_back(total);
+    return total;
+  };
+
+  Timer whole;
+  cuda_check(cudaEventRecord(whole.a, st), "event");
+
+  // ---- init_ensemble: prior draws + full energies
+  std::vector<int> list, prefix;
+  int total = build_list(order, true, list, prefix);
+  h2d(d_list_all, list.data(), list.size(), st);
+  h2d(d_prefix_all, prefix.data(), prefix.size(), st);
+  cuda_check(launch_init_draw(d_gds, d_list_all, G, Tmax, st), "k_init_draw");
+  cuda_check(launch_energy(m0.family, shape, dmax, d_gds, d_list_all, d_prefix_all, G, total, st), "k_chain<energy>");
+  count_launch(2);
+
+  // pinned staging for the per-round state read-back
+  GroupState* h_st = nullptr;
+  int* h_list = nullptr;
+  cuda_check(cudaMallocHost(&h_st, sizeof(GroupState) * G), "cudaMallocHost");
+  cuda_check(cudaMallocHost(&h_list, sizeof(int) * 2 * (G + 1)), "cudaMallocHost");
+  struct PinnedFree {
+    void* a;
+    void* b;
+    ~PinnedFree() {
+      cudaFreeHost(a);
+      cudaFreeHost(b);
+    }
+  } pf{h_st, h_list};
+
+  std::vector<int> active = order;
+  Timer mv;
+  double move_ms = 0.0;
+  int64_t move_launches = 0;
+  while (!active.empty()) {
+    total = build_list(active, false, list, prefix);
+    const int na = (int)list.size();
+    std::memcpy(h_list, list.data(), sizeof(int) * na);
+    std::memcpy(h_list + (G + 1), prefix.data(), sizeof(int) * (na + 1));
+    h2d(d_list, h_list, na, st);
+    h2d(d_prefix, h_list + (G + 1), na + 1, st);
+    cuda_check(launch_temper(d_gds, d_list, na, st), "k_temper");
+    cuda_check(cudaEventRecord(mv.a, st), "event");
+    cuda_check(launch_move(m0.family, shape, dmax, d_gds, d_list, d_prefix, na, total, st), "k_chain<move>");
+    cuda_check(cudaEventRecord(mv.b, st), "event");
+    cuda_check(launch_stats(d_gds, d_list, na, st), "k_stats");
+    count_launch(3);
+    d2h(h_st, d_st, G, st);
+    dev.sync();
+    move_ms += mv.ms();
+    ++move_launches;
+    std::vector<int> next;
+    for (int gi : active)
+      if (h_st[gi].active) next.push_back(gi);
+    active.swap(next);
+  }
+  cuda_check(cudaEventRecord(whole.b, st), "event");
+  dev.sync();
+  device_seconds = whole.ms() * 1e-3;
+  {
+    std::lock_guard<std::mutex> lk(g_stats_mu);
+    g_stats.move_kernel_ms += move_ms;
+    g_stats.move_launches += move_launches;
+    double pe = 0.0;
+    for (int gi = 0; gi < G; ++gi) pe += (double)h_st[gi].trials * (double)gds[gi].N;
+    g_stats.point_evals += pe;
+  }
+
+  // ---- results
+  for (int gi = 0; gi < G; ++gi) {
+    const RunSpec& R = runs[idx[gi]];
+    specmc_smc_result& o = out[idx[gi]];
+    const GroupState& s = h_st[gi];
+    const size_t T = R.cfg.T, d = R.m.d;
+    o.d = (int)d;
+    o.T = (int64_t)T;
+    o.levels = s.level;
+    o.trials = (int64_t)s.trials;
+    o.proposals = (int64_t)T * (int64_t)d * s.level;
+    if (s.error == GE_MAX_LEVELS) {
+      o.status = SPECMC_ERUNTIME;
+      continue;
+    }
+    if (s.error == GE_ZERO_WEIGHT) {
+      o.status = SPECMC_ERUNTIME;
+      continue;
+    }
+    o.status = SPECMC_OK;
+    o.F = s.neg_log_z;
+    o.diverged = !std::isfinite(o.F);
+    const int Lv = s.level;
+    std::vector<double> diag((size_t)Lv * 4);
+    d2h(diag.data(), gds[gi].diag, diag.size(), st);
+    std::vector<double> th(d * T);
+    d2h(th.data(), gds[gi].theta[s.cur], th.size(), st);
+    o.energies = static_cast<double*>(std::malloc(sizeof(double) * T));
+    d2h(o.energies, gds[gi].E[s.cur], T, st);
+    dev.sync();
+    o.ladder = static_cast<double*>(std::malloc(sizeof(double) * (Lv + 1)));
+    o.level_ess_ratio = static_cast<double*>(std::malloc(sizeof(double) * std::max(Lv, 1)));
+    o.level_log_mean_w = static_cast<double*>(std::malloc(sizeof(double) * std::max(Lv, 1)));
+    o.level_acc_rate = static_cast<double*>(std::malloc(sizeof(double) * std::max(Lv, 1)));
+    o.ladder[0] = 0.0;
+    for (int l = 0; l < Lv; ++l) {
+      o.ladder[l + 1] = diag[4 * l];
+      o.level_ess_ratio[l] = diag[4 * l + 1];
+      o.level_log_mean_w[l] = diag[4 * l + 2];
+      o.level_acc_rate[l] = diag[4 * l + 3];
+    }
+    o.posterior = static_cast<double*>(std::malloc(sizeof(double) * d * T));
+    for (size_t c = 0; c < T; ++c)
+      for (size_t i = 0; i < d; ++i) {
+        double v = th[i * T + c];
+        if (is_location(R.m.family, R.m.K, (int)i) && R.x_shift != 0.0) v += R.x_shift;
+        o.posterior[c * d + i] = v;
+      }
+  }
+}
+
+void copy_err(char* err, size_t errlen, const std::string& m) {
+  if (err && errlen) {
+    std::strncpy(err, m.c_str(), errlen - 1);
+    err[errlen - 1] = 0;
+  }
+}
+
+RunSpec make_runspec(const specmc_model_desc& m, int spectrum, const specmc_smc_config& cfg,
+                     const specmc_spectrum& sp) {
+  validate_config(cfg);
+  validate_model(m);
+  validate_spectrum(sp.xs, sp.ys, sp.n, m.noise == SPECMC_NOISE_POISSON);
+  RunSpec R;
+  R.m = m;
+  R.spectrum = spectrum;
+  R.cfg = cfg;
+  R.N = sp.n;
+  R.x_shift = pick_shift(m, sp.xs, sp.n);
+  R.pk.assign(m.prior_kind, m.prior_kind + m.d);
+  R.pa.assign(m.prior_a, m.prior_a + m.d);
+  R.pb.assign(m.prior_b, m.prior_b + m.d);
+  for (int i = 0; i < m.d; ++i)
+    if (is_location(m.family, m.K, i) && R.x_shift != 0.0) {
+      if (R.pk[i] == SPECMC_PRIOR_NORMAL) R.pa[i] -= R.x_shift;
+      if (R.pk[i] == SPECMC_PRIOR_UNIFORM) {
+        R.pa[i] -= R.x_shift;
+        R.pb[i] -= R.x_shift;
+      }
+    }
+  R.m.prior_kind = nullptr;  // owned copies live in R
+  R.m.prior_a = nullptr;
+  R.m.prior_b = nullptr;
+  return R;
+}
+
+int run_batch(int n_problems, const specmc_problem* problems, int n_spectra, const specmc_spectrum* spectra,
+              specmc_smc_result* out, char* err, size_t errlen) {
+  const auto t0 = std::chrono::steady_clock::now();
+  if (n_problems < 1 || !problems || !out) throw Error(SPECMC_EINVAL, "batch: no problems");
+  if (n_spectra < 1 || !spectra) throw Error(SPECMC_EINVAL, "batch: no spectra");
+  for (int i = 0; i < n_problems; ++i) std::memset(&out[i], 0, sizeof(specmc_smc_result));
+  std::vector<specmc_spectrum> sps(spectra, spectra + n_spectra);
+  std::vector<RunSpec> runs;
+  for (int i = 0; i < n_problems; ++i) {
+    const auto& p = problems[i];
+    if (p.spectrum < 0 || p.spectrum >= n_spectra) throw Error(SPECMC_EINVAL, "batch: spectrum index out of range");
+    runs.push_back(make_runspec(p.model, p.spectrum, p.cfg, sps[p.spectrum]));
+  }
+  const int device = runs[0].cfg.device;
+  for (auto& r : runs)
+    if (r.cfg.device != device) throw Error(SPECMC_EINVAL, "batch: all problems must target the same device");
+  Device dev(device);
+  // classes: same family and same launch shape
+  std::map<std::pair<int, int>, std::vector<int>> classes;
+  for (int i = 0; i < n_problems; ++i) {
+    const Shape s = pick_shape(runs[i].N);
+    classes[{runs[i].m.family, s.W * 100 + s.PPL}].push_back(i);
+  }
+  double dev_s = 0.0;
+  for (auto& kv : classes) {
+    double s = 0.0;
+    run_class(dev, runs, sps, kv.second, out, s);
+    dev_s += s;
+  }
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  int first = SPECMC_OK;
+  for (int i = 0; i < n_problems; ++i) {
+    out[i].wall_seconds = wall;
+    out[i].device_seconds = dev_s;
+    if (out[i].status != SPECMC_OK && first == SPECMC_OK) {
+      first = out[i].status;
+      copy_err(err, errlen, "smc: max_levels exceeded before reaching beta = 1 (or total weight is zero)");
+    }
+  }
+  return first;
+}
+
+template <typename F>
+int guarded(char* err, size_t errlen, F&& f) {
+  try {
+    return f();
+  } catch (const Error& e) {
+    copy_err(err, errlen, e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    copy_err(err, errlen, "host allocation failed");
+    return SPECMC_ERUNTIME;
+  } catch (const std::exception& e) {
+    copy_err(err, errlen, e.what());
+    return SPECMC_ERUNTIME;
+  }
+}
+
+// device scratch for the unit entry points
+struct Scratch {
+  std::vector<DevBuf> bufs;
+  template <typename T>
+  T* alloc(size_t n) {
+    bufs.emplace_back(sizeof(T) * std::max<size_t>(n, 1));
+    return bufs.back().as<T>();
+  }
+};
+
+}  // namespace
+}  // namespace smc
+
+using namespace smc;
+
+extern "C" {
+
+int specmc_smc_run(const specmc_model_desc* model, const double* xs, const double* ys, int64_t n_points,
+                   const specmc_smc_config* cfg, specmc_smc_result* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> int {
+    if (!model || !cfg || !out) throw Error(SPECMC_EINVAL, "null argument");
+    specmc_problem p;
+    p.model = *model;
+    p.spectrum = 0;
+    p.cfg = *cfg;
+    specmc_spectrum sp{xs, ys, n_points};
+    const int rc = run_batch(1, &p, 1, &sp, out, err, errlen);
+    return rc;
+  });
+}
+
+int specmc_smc_run_batch(int32_t n_problems, const specmc_problem* problems, int32_t n_spectra,
+                         const specmc_spectrum* spectra, specmc_smc_result* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> int { return run_batch(n_problems, problems, n_spectra, spectra, out, err, errlen); });
+}
+
+void specmc_result_free(specmc_smc_result* r) {
+  if (!r) return;
+  std::free(r->ladder);
+  std::free(r->level_ess_ratio);
+  std::free(r->level_log_mean_w);
+  std::free(r->level_acc_rate);
+  std::free(r->posterior);
+  std::free(r->energies);
+  r->ladder = r->level_ess_ratio = r->level_log_mean_w = r->level_acc_rate = r->posterior = r->energies = nullptr;
+}
+
+int specmc_validate_config(const specmc_smc_config* cfg, char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> int {
+    if (!cfg) throw Error(SPECMC_EINVAL, "null config");
+    validate_config(*cfg);
+    return SPECMC_OK;
+  });
+}
+
+int specmc_validate_problem(const specmc_model_desc* model, const double* xs, const double* ys, int64_t n_points,
+                            char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> int {
+    if (!model) throw Error(SPECMC_EINVAL, "null model");
+    validate_model(*model);
+    validate_spectrum(xs, ys, n_points, model->noise == SPECMC_NOISE_POISSON);
+    return SPECMC_OK;
+  });
+}
+
+int specmc_energy_batch(const specmc_model_desc* model, const double* xs, const double* ys, int64_t n_points,
+                        const double* thetas, int64_t n_thetas, int32_t device, double* energies_out, char* err,
+                        size_t errlen) {
+  return guarded(err, errlen, [&]() -> int {
+    if (!model || !thetas || !energies_out) throw Error(SPECMC_EINVAL, "null argument");
+    if (n_thetas < 1) throw Error(SPECMC_EINVAL, "energy_batch: no parameter vectors");
+    specmc_smc_config cfg{std::max<int64_t>(n_thetas, 2), 1, 0.5, 1, 0, 1, device};
+    specmc_spectrum sp{xs, ys, n_points};
+    RunSpec R = make_runspec(*model, 0, cfg, sp);
+    Device dev(device);
+    const Shape shape = pick_shape(n_points);
+    if ((int64_t)32 * shape.W * shape.PPL < n_points)
+      throw Error(SPECMC_EINVAL, "spectrum has more points than the device path supports (8192)");
+    const PreparedSpectrum ps = prepare_spectrum(*model, xs, ys, n_points, shape, R.x_shift);
+    const int d = model->d;
+    const int64_t T = n_thetas;
+    Scratch sc;
+    const size_t npt = ps.x.size();
+    float* dx = sc.alloc<float>(npt);
+    float2* dc = sc.alloc<float2>(npt);
+    float2* dy = sc.alloc<float2>(npt);
+    int* pk = sc.alloc<int>(d);
+    double* pa = sc.alloc<double>(d);
+    double* pb = sc.alloc<double>(d);
+    double* th = sc.alloc<double>((size_t)d * T);
+    double* E = sc.alloc<double>(T);
+    GroupState* gst = sc.alloc<GroupState>(1);
+    GroupDesc* gd = sc.alloc<GroupDesc>(1);
+    int* lst = sc.alloc<int>(2);
+    int* pre = sc.alloc<int>(2);
+    cudaStream_t st = dev.stream;
+    h2d(dx, ps.x.data(), npt, st);
+    h2d(reinterpret_cast<float*>(dc), ps.c.data(), 2 * npt, st);
+    h2d(reinterpret_cast<float*>(dy), ps.y.data(), 2 * npt, st);
+    h2d(pk, R.pk.data(), d, st);
+    h2d(pa, R.pa.data(), d, st);
+    h2d(pb, R.pb.data(), d, st);
+    std::vector<double> soa((size_t)d * T);
+    for (int64_t c = 0; c < T; ++c)
+      for (int i = 0; i < d; ++i) {
+        double v = thetas[c * d + i];
+        if (is_location(model->family, model->K, i)) v -= R.x_shift;
+        soa[(size_t)i * T + c] = v;
+      }
+    h2d(th, soa.data(), soa.size(), st);
+    GroupDesc g;
+    std::memset(&g, 0, sizeof(g));
+    g.family = model->family;
+    g.K = model->K;
+    g.d = d;
+    g.noise = ps.nz;
+    g.T = (int)T;
+    g.n = 1;
+    g.S = (int)T;
+    g.max_levels = 1;
+    g.n_data = (double)n_points;
+    g.N = (int)n_points;
+    g.e_a0 = ps.e_a0;
+    g.e_a1 = ps.e_a1;
+    g.nz_a0 = ps.a0;
+    g.nz_a1 = ps.a1;
+    g.nz_a2 = ps.a2;
+    g.nz_q = ps.q;
+    g.x0s = ps.x0s;
+    g.inv_range = ps.inv_range;
+    g.range = ps.range;
+    g.spec_x = dx;
+    g.spec_c = dc;
+    g.spec_y = dy;
+    g.pkind = pk;
+    g.pa = pa;
+    g.pb = pb;
+    g.theta[0] = g.theta[1] = th;
+    g.E[0] = g.E[1] = E;
+    g.st = gst;
+    GroupState s;
+    std::memset(&s, 0, sizeof(s));
+    h2d(gd, &g, 1, st);
+    h2d(gst, &s, 1, st);
+    const int total = (int)((T + shape.U - 1) / shape.U);
+    const int hl[2] = {0, 0}, hp[2] = {0, total};
+    h2d(lst, hl, 2, st);
+    h2d(pre, hp, 2, st);
+    cuda_check(launch_energy(model->family, shape, d, gd, lst, pre, 1, total, st), "k_chain<energy>");
+    count_launch();
+    d2h(energies_out, E, T, st);
+    dev.sync();
+    return SPECMC_OK;
+  });
+}
+
+int specmc_ess(const double* lw, int64_t n, int32_t device, double* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> int {
+    if (!lw || !out || n < 1) throw Error(SPECMC_EINVAL, "ess: empty input");
+    Device dev(device);
+    Scratch sc;
+    double* d_lw = sc.alloc<double>(n);
+    double* d_out = sc.alloc<double>(1);
+    int* d_err = sc.alloc<int>(1);
+    h2d(d_lw, lw, n, dev.stream);
+    cuda_check(launch_unit_ess(d_lw, n, d_out, d_err, dev.stream), "k_unit_ess");
+    count_launch();
+    int e = 0;
+    d2h(out, d_out, 1, dev.stream);
+    d2h(&e, d_err, 1, dev.stream);
+    dev.sync();
+    if (e) throw Error(SPECMC_ERUNTIME, "ess: total weight is zero");
+    return SPECMC_OK;
+  });
+}
+
+int specmc_log_mean_exp(const double* v, int64_t n, int32_t device, double* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> int {
+    if (!v || !out || n < 1) throw Error(SPECMC_EINVAL, "log_mean_exp: empty input");
+    Device dev(device);
+    Scratch sc;
+    double* d_v = sc.alloc<double>(n);
+    double* d_out = sc.alloc<double>(1);
+    h2d(d_v, v, n, dev.stream);
+    cuda_check(launch_unit_log_mean_exp(d_v, n, d_out, dev.stream), "k_unit_lme");
+    count_launch();
+    d2h(out, d_out, 1, dev.stream);
+    dev.sync();
+    return SPECMC_OK;
+  });
+}
+
+int specmc_next_beta(const double* E, int64_t n, double n_data, double beta_prev, double ess_target, int32_t device,
+                     double* beta_out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> int {
+    if (!E || !beta_out || n < 1) throw Error(SPECMC_EINVAL, "next_beta: empty input");
+    if (!(beta_prev < 1.0)) throw Error(SPECMC_EINVAL, "next_beta: beta_prev must be < 1");
+    Device dev(device);
+    Scratch sc;
+    double* d_E = sc.alloc<double>(n);
+    double* d_out = sc.alloc<double>(1);
+    int* d_err = sc.alloc<int>(1);
+    h2d(d_E, E, n, dev.stream);
+    cuda_check(launch_unit_next_beta(d_E, n, n_data, beta_prev, ess_target, d_out, d_err, dev.stream),
+               "k_unit_next_beta");
+    count_launch();
+    int e = 0;
+    d2h(beta_out, d_out, 1, dev.stream);
+    d2h(&e, d_err, 1, dev.stream);
+    dev.sync();
+    if (e) throw Error(SPECMC_ERUNTIME, "ess: total weight is zero");
+    return SPECMC_OK;
+  });
+}
+
+int specmc_systematic_resample(const double* lw, int64_t n, int64_t S, double u, int32_t device, int64_t* anc_out,
+                               char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> int {
+    if (!lw || !anc_out || n < 1 || S < 1) throw Error(SPECMC_EINVAL, "systematic_resample: empty input");
+    if (n > ((int64_t)1 << 31) - 1) throw Error(SPECMC_EINVAL, "systematic_resample: too many weights");
+    Device dev(device);
+    Scratch sc;
+    double* d_lw = sc.alloc<double>(n);
+    double* d_w = sc.alloc<double>(n);
+    int* d_anc = sc.alloc<int>(S);
+    int* d_err = sc.alloc<int>(1);
+    h2d(d_lw, lw, n, dev.stream);
+    cuda_check(launch_unit_resample(d_lw, n, S, u, d_w, d_anc, d_err, dev.stream), "k_unit_resample");
+    count_launch();
+    std::vector<int> a(S);
+    int e = 0;
+    d2h(a.data(), d_anc, S, dev.stream);
+    d2h(&e, d_err, 1, dev.stream);
+    dev.sync();
+    if (e) throw Error(SPECMC_ERUNTIME, "systematic_resample: total weight is zero");
+    for (int64_t j = 0; j < S; ++j) anc_out[j] = a[j];
+    return SPECMC_OK;
+  });
+}
+
+int specmc_predict_step_size(const double* hist_beta, const double* hist_acc, const double* hist_step, int32_t H,
+                             const specmc_model_desc* model, double beta_next, int32_t device, double* out, char* err,
+                             size_t errlen) {
+  return guarded(err, errlen, [&]() -> int {
+    if (!model || !out || H < 0) throw Error(SPECMC_EINVAL, "predict_step_size: bad arguments");
+    const int d = model->d;
+    // ring layout of the device: entry j at slot j % 5
+    std::vector<double> ring((size_t)kHist * (1 + 2 * d), 0.0);
+    for (int j = std::max(0, H - kHist); j < H; ++j) {
+      double* e = ring.data() + (size_t)(j % kHist) * (1 + 2 * d);
+      e[0] = hist_beta[j];
+      for (int i = 0; i < d; ++i) {
+        e[1 + i] = hist_acc[(size_t)j * d + i];
+        e[1 + d + i] = hist_step[(size_t)j * d + i];
+      }
+    }
+    Device dev(device);
+    Scratch sc;
+    double* d_ring = sc.alloc<double>(ring.size());
+    int* d_pk = sc.alloc<int>(d);
+    double* d_pa = sc.alloc<double>(d);
+    double* d_pb = sc.alloc<double>(d);
+    double* d_out = sc.alloc<double>(d);
+    h2d(d_ring, ring.data(), ring.size(), dev.stream);
+    h2d(d_pk, model->prior_kind, d, dev.stream);
+    h2d(d_pa, model->prior_a, d, dev.stream);
+    h2d(d_pb, model->prior_b, d, dev.stream);
+    cuda_check(launch_unit_predict(d_ring, H, d, beta_next, d_pk, d_pa, d_pb, d_out, dev.stream), "k_unit_predict");
+    count_launch();
+    d2h(out, d_out, d, dev.stream);
+    dev.sync();
+    return SPECMC_OK;
+  });
+}
+
+int specmc_stats_get(specmc_stats* out) {
+  if (!out) return SPECMC_EINVAL;
+  std::lock_guard<std::mutex> lk(g_stats_mu);
+  *out = g_stats;
+  return SPECMC_OK;
+}
+
+void specmc_stats_reset(void) {
+  std::lock_guard<std::mutex> lk(g_stats_mu);
+  g_stats = specmc_stats{0, 0.0, 0, 0.0};
+}
+
+int specmc_launch_shape(int64_t n_points, int32_t* W, int32_t* PPL, int32_t* U) {
+  if (n_points < 1) return SPECMC_EINVAL;
+  const Shape s = pick_shape(n_points);
+  if (W) *W = s.W;
+  if (PPL) *PPL = s.PPL;
+  if (U) *U = s.U;
+  return (int64_t)32 * s.W * s.PPL >= n_points ? SPECMC_OK : SPECMC_EINVAL;
+}
+
+int specmc_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+const char* specmc_version(void) { return "specmc_b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,46 @@
+// launch.h -- host-visible launchers for the sm_100a kernels (kernels.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+
+namespace smc {
+
+// Launch shape of the chain-parallel kernels for a spectrum of N points:
+// W warps cooperate on one chain (unit), each lane owns PPL consecutive
+// points in registers, U units share one CTA (and its staged spectrum).
+struct Shape {
+  int W;
+  int PPL;
+  int U;
+};
+
+Shape pick_shape(int64_t N);
+bool ppl_supported(int ppl);
+size_t chain_smem_bytes(const Shape& s, int dmax);
+
+// prior draws for every particle of every listed group (init_ensemble, smc.cpp:34-53)
+cudaError_t launch_init_draw(const GroupDesc* d_gds, const int* d_list, int n_list, int Tmax, cudaStream_t st);
+// full energies of theta[cur] (BlockEvaluator::full, energy.cpp:43-55), one chain unit per particle
+cudaError_t launch_energy(int family, const Shape& s, int dmax, const GroupDesc* d_gds, const int* d_list,
+                          const int* d_cta_prefix, int n_list, int total_ctas, cudaStream_t st);
+// fused waste-free chain move (wastefree_level chain loop x cw_mh_sweep, smc.cpp:142-156, mcmc.cpp:55-96)
+cudaError_t launch_move(int family, const Shape& s, int dmax, const GroupDesc* d_gds, const int* d_list,
+                        const int* d_cta_prefix, int n_list, int total_ctas, cudaStream_t st);
+// next_beta + weights + evidence + systematic resampling + predict_step_size (one CTA per group)
+cudaError_t launch_temper(const GroupDesc* d_gds, const int* d_list, int n_list, cudaStream_t st);
+// step-size statistics + history + buffer flip (one CTA per group)
+cudaError_t launch_stats(const GroupDesc* d_gds, const int* d_list, int n_list, cudaStream_t st);
+
+// ---- parity units (single-array versions of the temper building blocks)
+cudaError_t launch_unit_ess(const double* d_lw, int64_t n, double* d_out, int* d_err, cudaStream_t st);
+cudaError_t launch_unit_log_mean_exp(const double* d_v, int64_t n, double* d_out, cudaStream_t st);
+cudaError_t launch_unit_next_beta(const double* d_E, int64_t n, double n_data, double beta_prev, double target,
+                                  double* d_out, int* d_err, cudaStream_t st);
+cudaError_t launch_unit_resample(const double* d_lw, int64_t n, int64_t S, double u, double* d_wscratch,
+                                 int* d_anc, int* d_err, cudaStream_t st);
+cudaError_t launch_unit_predict(const double* d_hist, int H, int d, double beta_next, const int* d_pk,
+                                const double* d_pa, const double* d_pb, double* d_out, cudaStream_t st);
+
+}  // namespace smc

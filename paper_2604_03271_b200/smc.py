@@ -1,0 +1,298 @@
+"""SMC entry points mirroring the reference interface, over the C ABI.
+
+Reference (paths relative to the reference root):
+  SmcConfig / validate_smc_config   proj/include/specmc/smc.hpp:12-21, proj/src/smc.cpp:23-32
+  smc_run(spec, data, cfg)          proj/include/specmc/smc.hpp:78, proj/src/smc.cpp:218-249
+  RunReport                         proj/include/specmc/report.hpp:16-27
+  model_select                      proj/src/posterior.cpp:68-104
+  parity units                      smc.cpp:61-112 (ess, next_beta, systematic_resample),
+                                    math.hpp:28-30 (log_mean_exp), mcmc.cpp:20-53
+                                    (predict_step_size), energy.cpp:7-55 (energies)
+
+Errors map like the reference: invalid configuration -> ValueError (the
+std::invalid_argument analogue, CLI exit 2), numeric failure -> RuntimeError
+(std::runtime_error, CLI exit 3); CUDA failures raise CudaError.  Every
+compute call runs hand-written sm_100a kernels; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib
+from ._lib import lib
+from .model import ModelSpec, Spectrum
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _raise(rc: int, err: C.Array):
+    msg = err.value.decode(errors="replace")
+    if rc == _lib.SPECMC_EINVAL:
+        raise ValueError(msg)
+    if rc == _lib.SPECMC_ERUNTIME:
+        raise RuntimeError(msg)
+    if rc == _lib.SPECMC_ECUDA:
+        raise CudaError(msg)
+    raise RuntimeError(f"specmc error {rc}: {msg}")
+
+
+def _d(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _p(a):
+    return a.ctypes.data_as(_lib._dp)
+
+
+@dataclass
+class SmcConfig:
+    """proj/include/specmc/smc.hpp:12-19 (+ the CUDA device ordinal)."""
+    T: int = 10000
+    n: int = 10
+    ess_target: float = 0.5
+    max_levels: int = 2000
+    seed: int = 0
+    workers: int = 1
+    device: int = 0
+
+    def c(self):
+        return _lib.SmcConfigC(int(self.T), int(self.n), float(self.ess_target), int(self.max_levels),
+                               int(self.seed) & 0xFFFFFFFFFFFFFFFF, int(self.workers), int(self.device))
+
+
+def validate_smc_config(cfg: SmcConfig) -> None:
+    """smc.cpp:23-32 (host-side; needs no GPU)."""
+    err = C.create_string_buffer(512)
+    c = cfg.c()
+    rc = lib.specmc_validate_config(C.byref(c), err, 512)
+    if rc:
+        _raise(rc, err)
+
+
+@dataclass
+class RunReport:
+    """proj/include/specmc/report.hpp:16-27, filled as smc.cpp:218-249 does."""
+    sampler: str = "smc"
+    label: str = ""
+    F: float = math.nan
+    diverged: bool = False
+    wall_seconds: float = 0.0
+    param_names: List[str] = field(default_factory=list)
+    scalars: Dict[str, float] = field(default_factory=dict)
+    arrays: Dict[str, np.ndarray] = field(default_factory=dict)
+    posterior: Optional[np.ndarray] = None  # d x T
+    energies: Optional[np.ndarray] = None   # T
+    device_seconds: float = 0.0
+    proposals: int = 0
+    trials: int = 0
+
+
+def _report(spec: ModelSpec, cfg: SmcConfig, n_data: int, r: _lib.SmcResultC) -> RunReport:
+    L = r.levels
+    rep = RunReport(sampler="smc", F=r.F, diverged=bool(r.diverged), wall_seconds=r.wall_seconds,
+                    param_names=spec.param_names, device_seconds=r.device_seconds, proposals=r.proposals,
+                    trials=r.trials)
+    rep.scalars = {"T": float(cfg.T), "n": float(cfg.n), "ess_target": cfg.ess_target, "seed": float(cfg.seed),
+                   "workers": float(cfg.workers), "n_data": float(n_data), "levels": float(L)}
+    rep.arrays = {
+        "ladder": np.ctypeslib.as_array(r.ladder, (L + 1,)).copy(),
+        "level_ess_ratio": np.ctypeslib.as_array(r.level_ess_ratio, (max(L, 1),))[:L].copy(),
+        "level_log_mean_w": np.ctypeslib.as_array(r.level_log_mean_w, (max(L, 1),))[:L].copy(),
+        "level_acc_rate": np.ctypeslib.as_array(r.level_acc_rate, (max(L, 1),))[:L].copy(),
+    }
+    d, T = r.d, r.T
+    rep.posterior = np.ctypeslib.as_array(r.posterior, (T, d)).T.copy()
+    rep.energies = np.ctypeslib.as_array(r.energies, (T,)).copy()
+    return rep
+
+
+def smc_run(spec: ModelSpec, data: Spectrum, cfg: SmcConfig) -> RunReport:
+    """RunReport smc_run(const ModelSpec&, const Spectrum&, const SmcConfig&) -- smc.cpp:218."""
+    return smc_run_batch([(spec, 0, cfg)], [data])[0]
+
+
+def smc_run_batch(problems: Sequence[Tuple[ModelSpec, int, SmcConfig]], spectra: Sequence[Spectrum],
+                  raise_on_error: bool = True):
+    """Runs every (spec, spectrum index, cfg) concurrently on one GPU.
+
+    Returns a list of RunReport (or, with raise_on_error=False, the exception
+    instance for runs that failed, e.g. max_levels exceeded)."""
+    n = len(problems)
+    keep = []
+    probs = (_lib.ProblemC * n)()
+    for i, (spec, si, cfg) in enumerate(problems):
+        desc, k = spec.desc()
+        keep.append(k)
+        probs[i] = _lib.ProblemC(desc, int(si), cfg.c())
+    sps = (_lib.SpectrumC * len(spectra))()
+    for j, s in enumerate(spectra):
+        keep.append(s)
+        sps[j] = _lib.SpectrumC(_p(s.xs), _p(s.ys), len(s.xs))
+    res = (_lib.SmcResultC * n)()
+    err = C.create_string_buffer(1024)
+    rc = lib.specmc_smc_run_batch(n, probs, len(spectra), sps, res, err, 1024)
+    try:
+        if rc and rc != _lib.SPECMC_ERUNTIME:
+            _raise(rc, err)
+        out = []
+        for i, (spec, si, cfg) in enumerate(problems):
+            r = res[i]
+            if r.status != _lib.SPECMC_OK:
+                e = RuntimeError("smc: max_levels exceeded before reaching beta = 1 (or total weight is zero)")
+                if raise_on_error:
+                    raise e
+                out.append(e)
+            else:
+                out.append(_report(spec, cfg, len(spectra[si].xs), r))
+        return out
+    finally:
+        for i in range(n):
+            lib.specmc_result_free(C.byref(res[i]))
+
+
+# ---------------------------------------------------------------- parity units
+def energies(spec: ModelSpec, data: Spectrum, thetas, device: int = 0) -> np.ndarray:
+    """Batched BlockEvaluator::full + data_energy (energy.cpp:7-55) on the device (K2)."""
+    th = _d(np.atleast_2d(thetas))
+    if th.shape[1] != spec.d:
+        raise ValueError("theta length mismatch")
+    desc, keep = spec.desc()
+    out = np.empty(th.shape[0])
+    err = C.create_string_buffer(512)
+    rc = lib.specmc_energy_batch(C.byref(desc), _p(data.xs), _p(data.ys), len(data.xs), _p(th), th.shape[0],
+                                 device, _p(out), err, 512)
+    if rc:
+        _raise(rc, err)
+    return out
+
+
+def energy(spec: ModelSpec, theta, data: Spectrum, device: int = 0) -> float:
+    """double energy(spec, theta, data) -- energy.cpp:130-132"""
+    return float(energies(spec, data, np.atleast_2d(theta), device)[0])
+
+
+def ess(log_weights, device: int = 0) -> float:
+    lw = _d(log_weights)
+    out = C.c_double()
+    err = C.create_string_buffer(512)
+    rc = lib.specmc_ess(_p(lw), len(lw), device, C.byref(out), err, 512)
+    if rc:
+        _raise(rc, err)
+    return out.value
+
+
+def log_mean_exp(v, device: int = 0) -> float:
+    v = _d(v)
+    out = C.c_double()
+    err = C.create_string_buffer(512)
+    rc = lib.specmc_log_mean_exp(_p(v), len(v), device, C.byref(out), err, 512)
+    if rc:
+        _raise(rc, err)
+    return out.value
+
+
+def next_beta(energies_, n_data: float, beta_prev: float, ess_target: float, device: int = 0) -> float:
+    E = _d(energies_)
+    out = C.c_double()
+    err = C.create_string_buffer(512)
+    rc = lib.specmc_next_beta(_p(E), len(E), n_data, beta_prev, ess_target, device, C.byref(out), err, 512)
+    if rc:
+        _raise(rc, err)
+    return out.value
+
+
+def systematic_resample(log_weights, S: int, u: float, device: int = 0) -> np.ndarray:
+    lw = _d(log_weights)
+    out = np.empty(S, dtype=np.int64)
+    err = C.create_string_buffer(512)
+    rc = lib.specmc_systematic_resample(_p(lw), len(lw), S, u, device, out.ctypes.data_as(_lib._lp), err, 512)
+    if rc:
+        _raise(rc, err)
+    return out
+
+
+def predict_step_size(hist_beta, hist_acc, hist_step, beta_next: float, spec: ModelSpec,
+                      device: int = 0) -> np.ndarray:
+    hb, ha, hs = _d(hist_beta), _d(hist_acc), _d(hist_step)
+    desc, keep = spec.desc()
+    out = np.empty(spec.d)
+    err = C.create_string_buffer(512)
+    rc = lib.specmc_predict_step_size(_p(hb), _p(ha), _p(hs), len(hb), C.byref(desc), beta_next, device, _p(out),
+                                      err, 512)
+    if rc:
+        _raise(rc, err)
+    return out
+
+
+# ------------------------------------------------------------ model selection
+@dataclass
+class ModelChoiceRow:
+    K: int
+    F: float = math.nan
+    trial_std: float = math.nan
+    trials: int = 0
+    excluded: bool = False
+
+
+@dataclass
+class ModelChoice:
+    K_best: int = 0
+    table: List[ModelChoiceRow] = field(default_factory=list)
+
+
+def model_select(reports: Sequence[Tuple[int, RunReport]]) -> ModelChoice:
+    """posterior.cpp:68-104: argmin of mean F per K; non-finite/diverged K
+    excluded; ties keep the smaller K; RuntimeError if every K is excluded."""
+    if not reports:
+        raise ValueError("model_select: no reports")
+    by_k: Dict[int, List[float]] = {}
+    bad = set()
+    for k, rep in reports:
+        by_k.setdefault(k, []).append(rep.F)
+        if not math.isfinite(rep.F) or rep.diverged:
+            bad.add(k)
+    out = ModelChoice()
+    best = None
+    for k in sorted(by_k):
+        fs = by_k[k]
+        row = ModelChoiceRow(K=k, trials=len(fs), excluded=k in bad)
+        if not row.excluded:
+            mean = sum(fs) / len(fs)
+            row.F = mean
+            if len(fs) > 1:
+                row.trial_std = math.sqrt(sum((f - mean) ** 2 for f in fs) / (len(fs) - 1))
+            if best is None or mean < best:
+                best = mean
+                out.K_best = k
+        out.table.append(row)
+    if best is None:
+        raise RuntimeError("model_select: every candidate diverged")
+    return out
+
+
+def stats():
+    s = _lib.StatsC()
+    lib.specmc_stats_get(C.byref(s))
+    return {"kernel_launches": s.kernel_launches, "move_kernel_ms": s.move_kernel_ms,
+            "move_launches": s.move_launches, "point_evals": s.point_evals}
+
+
+def stats_reset():
+    lib.specmc_stats_reset()
+
+
+def launch_shape(n_points: int):
+    W, P, U = C.c_int32(), C.c_int32(), C.c_int32()
+    lib.specmc_launch_shape(n_points, C.byref(W), C.byref(P), C.byref(U))
+    return W.value, P.value, U.value
+
+
+def device_count() -> int:
+    return lib.specmc_device_count()

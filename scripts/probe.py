@@ -1,0 +1,31 @@
+"""Exploratory GPU probe: model selection runs on the BASELINE configs."""
+import sys, time, json
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np
+import paper_2604_03271_b200 as S
+from paper_2604_03271_b200 import synthetic as syn
+
+def run(name, T=None, kmax=None, seed=7):
+    w = syn.config(name, T)
+    ks = list(range(w.k_range[0], (kmax or w.k_range[1]) + 1))
+    probs = [(w.spec(k), 0, S.SmcConfig(T=w.T, n=w.n, seed=seed)) for k in ks]
+    S.stats_reset()
+    t = time.perf_counter()
+    reps = S.smc_run_batch(probs, [w.data])
+    wall = time.perf_counter() - t
+    st = S.stats()
+    props = sum(r.proposals for r in reps); trials = sum(r.trials for r in reps)
+    choice = S.model_select([(k, r) for k, r in zip(ks, reps)])
+    out = dict(cfg=name, T=w.T, wall=round(wall, 3), dev=round(reps[0].device_seconds, 3),
+               levels=[int(r.scalars["levels"]) for r in reps], F=[round(r.F, 3) for r in reps],
+               K_best=choice.K_best, proposals=props, trials=trials,
+               evals_per_s=props / reps[0].device_seconds, move_ms=round(st["move_kernel_ms"], 1),
+               pt_evals_per_s_move=st["point_evals"] / (st["move_kernel_ms"] * 1e-3),
+               launches=st["kernel_launches"])
+    print(json.dumps(out), flush=True)
+
+if __name__ == "__main__":
+    for arg in sys.argv[1:]:
+        name, T = arg.split(":")
+        run(name, int(T) if T != "full" else None)
