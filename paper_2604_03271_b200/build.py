@@ -16,8 +16,8 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 ROOT = PKG.parent
 LIB = PKG / "libspecmc_b200.so"
-SOURCES = [CSRC / "kernels.cu", CSRC / "host.cu"]
-HEADERS = [CSRC / "device.cuh", CSRC / "launch.h", ROOT / "include" / "specmc_b200.h"]
+SOURCES = sorted(CSRC.glob("*.cu"))
+HEADERS = [CSRC / "device.cuh", CSRC / "chain.cuh", CSRC / "launch.h", ROOT / "include" / "specmc_b200.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--use_fast_math",

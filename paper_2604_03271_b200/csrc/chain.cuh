@@ -1,0 +1,564 @@
+// chain.cuh -- the chain-parallel kernel of the B200 SMC sampler (K2 + K3).
+//
+//   k_chain<FAM, PPL, W, ENERGY=true>   batched full energies, one chain unit
+//                                       per particle (BlockEvaluator::full,
+//                                       energy.cpp:43-55 + data_energy :7-28)
+//   k_chain<FAM, PPL, W, ENERGY=false>  fused propose/evaluate/accept move of
+//                                       a waste-free level (smc.cpp:142-156
+//                                       x cw_mh_sweep, mcmc.cpp:55-96)
+// Reference paths are relative to the reference root (proj/...).
+//
+// A chain unit is W warps (L = 32 W lanes, compile-time).  Lane l owns the PPL
+// consecutive points [l*PPL, (l+1)*PPL) of the spectrum and keeps, in
+// registers,
+//   P[k]  committed peak signal  sum_b g_b(x)      (combine, model.cpp:287-288)
+//   G[k]  cached g_b(x) of the block being swept
+// A proposal changes one block: the trial signal is Pn = P + g_new - G, and an
+// amplitude proposal needs no transcendental at all (Pn = P + (A'/A - 1) G).
+// The Shirley background (lineshapes.hpp:65-83) needs the cumulative
+// trapezoid of Pn: C_k = sum_{j<=k} c_j Pn_j - h_{k+1} Pn_k with
+// c_j = h_j + h_{j+1}, h_j = (x_j - x_{j-1})/2, i.e. a lane-local scan and one
+// warp (and cross-warp) scan per proposal.  Energy terms are O(1)-centred,
+// summed per lane in fp32 and across lanes in fp64.  Padding points replicate
+// the last real point with weight 0, so no per-point masks are needed; a
+// forward/noise fault shows up as a non-finite sum (=> E = +inf, the
+// reference's rejection sentinel).
+#pragma once
+#include <cfloat>
+#include <cmath>
+
+#include "launch.h"
+
+namespace smc {
+
+__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
+
+constexpr float kHalfLn2 = 0.34657359027997264f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+struct BlockC {
+  float mu, c1, c2, c3;
+  bool ok;
+};
+
+template <int FAM>
+__device__ __forceinline__ constexpr int block_stride() {
+  return FAM == FAM_GM ? 3 : (FAM == FAM_XPS ? 4 : 1);
+}
+
+// gm:  g = A exp(-b/2 (x-mu)^2) = c1 2^(c2 d^2)                   (model.cpp:216-220)
+// xps: g = c1 2^(-u) + c2 / (1 + u), u = d^2 c3, c1 = A eta, c2 = A (1-eta), c3 = 1/sigma^2
+//      (= A [eta exp(-ln2 d^2/s^2) + (1-eta) s^2/(s^2+d^2)], model.cpp:269-280)
+// offset: g = theta_0                              (conjugate_oracle.hpp:22-26)
+template <int FAM>
+__device__ __forceinline__ BlockC block_consts(const double* p) {
+  BlockC c;
+  c.ok = true;
+  c.c3 = 0.f;
+  if (FAM == FAM_GM) {
+    c.c1 = (float)p[0];
+    c.mu = (float)p[1];
+    c.c2 = (float)p[2] * -0.72134752044448170f;  // -b/2 * log2(e)
+  } else if (FAM == FAM_XPS) {
+    const double A = p[0], sig = p[2], eta = p[3];
+    c.ok = sig > 0.0;
+    c.mu = (float)p[1];
+    c.c1 = (float)(A * eta);
+    c.c2 = (float)(A * (1.0 - eta));
+    const float s = (float)sig;
+    c.c3 = __frcp_rn(s * s);
+  } else {
+    c.c1 = (float)p[0];
+    c.mu = 0.f;
+    c.c2 = 0.f;
+  }
+  return c;
+}
+
+template <int FAM>
+__device__ __forceinline__ float shape(const BlockC& b, float x) {
+  if (FAM == FAM_GM) {
+    const float d = x - b.mu;
+    return b.c1 * ex2f(b.c2 * (d * d));
+  } else if (FAM == FAM_XPS) {
+    const float d = x - b.mu;
+    const float u = (d * d) * b.c3;
+    return fmaf(b.c1, ex2f(-u), b.c2 * rcpf(1.0f + u));
+  } else {
+    return b.c1;
+  }
+}
+
+struct Xch {  // per-unit cross-warp exchange, double-buffered by parity
+  float scan[2][16];
+  double en[2][16];
+};
+
+// Per-CTA shared memory (dynamic):
+//   [0,16)     mbarrier of the spectrum bulk copy
+//   sx  float  [PPL][L]   shifted abscissa
+//   sc  float2 [PPL][L]   (c_k, h_{k+1})
+//   sy  float4 [PPL][L]   (y_k, 1/s_k, weight, 0)
+//   per warp: th f64[dpad], ls f64[dpad], acc i32[dpad], z f32[dpad], u f32[dpad]
+//   per unit: Xch
+template <int PPL, int W>
+struct Smem {
+  static constexpr int L = 32 * W;
+  static constexpr int NPT = PPL * L;
+  static constexpr size_t off_x = 16;
+  static constexpr size_t off_c = off_x + (size_t)NPT * 4;
+  static constexpr size_t off_y = off_c + (size_t)NPT * 8;
+  static constexpr size_t off_w = off_y + (size_t)NPT * 16;
+  __host__ __device__ static size_t per_warp(int dpad) { return (size_t)dpad * (8 + 8 + 4 + 4 + 4); }
+  __host__ __device__ static size_t bytes(int U, int dpad) {
+    size_t b = off_w + (size_t)U * W * per_warp(dpad);
+    b = (b + 15) & ~(size_t)15;
+    return b + (size_t)U * sizeof(Xch);
+  }
+};
+
+template <int PPL, int W>
+struct Unit {
+  static constexpr int L = 32 * W;
+  const float* sx;
+  const float2* sc;
+  const float4* sy;
+  Xch* xc;
+  int lg, wiu, lane, bar_id;
+  int par;
+  __device__ __forceinline__ float x(int k) const { return sx[k * L + lg]; }
+  __device__ __forceinline__ float2 c(int k) const { return sc[k * L + lg]; }
+  __device__ __forceinline__ float4 y(int k) const { return sy[k * L + lg]; }
+  __device__ __forceinline__ void sync() const {
+    if (W > 1) named_bar(bar_id, L);
+  }
+};
+
+// P_k = sum_b g_b(x_k) in layout order, optionally with component ovr_i := ovr_v
+template <int FAM, int PPL, int W>
+__device__ __forceinline__ bool full_signal(const GroupDesc& g, const double* th, int ovr_i, double ovr_v,
+                                            const Unit<PPL, W>& u, float (&P)[PPL]) {
+  constexpr int stride = block_stride<FAM>();
+#pragma unroll
+  for (int k = 0; k < PPL; ++k) P[k] = 0.f;
+  const int nb = FAM == FAM_OFFSET ? 1 : g.K;
+  bool ok = true;
+  for (int b = 0; b < nb; ++b) {
+    double p[stride];
+#pragma unroll
+    for (int j = 0; j < stride; ++j) p[j] = (b * stride + j == ovr_i) ? ovr_v : th[b * stride + j];
+    const BlockC c = block_consts<FAM>(p);
+    ok = ok && c.ok;
+#pragma unroll
+    for (int k = 0; k < PPL; ++k) P[k] += shape<FAM>(c, u.x(k));
+  }
+  return ok;
+}
+
+// fp64 reduction of the lane partials over the unit (identical in every warp)
+template <int PPL, int W>
+__device__ __forceinline__ double unit_sum(Unit<PPL, W>& u, float acc) {
+  double s = warp_sum_d((double)acc);
+  if (W > 1) {
+    if (u.lane == 0) u.xc->en[u.par][u.wiu] = s;
+    u.sync();
+    s = 0.0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) s += u.xc->en[u.par][w];
+  }
+  u.par ^= 1;
+  return s;
+}
+
+// per-point centred NLL term, in units of 1/2 ln 2 for the hetero model:
+//   gauss:   r^2                                        E = a0 + a1 * sum
+//   hetero:  lg2(var/s) + q' r^2/var, q' = q / (ln2/2)  E = a0 + a1 (ln2/2) sum
+//   poisson: f - y - y ln(f/y)                          E = a0 + a1 * sum
+template <int NZ>
+__device__ __forceinline__ float noise_term(const GroupDesc& g, float f, float4 yq) {
+  const float r = yq.x - f;
+  if (NZ == NZ_GAUSS) {
+    return r * r;
+  } else if (NZ == NZ_HETERO) {
+    const float var = fmaf(fmaf(g.nz_a1, f, g.nz_a0), f, g.nz_a2);
+    return fmaf(g.nz_q, (r * r) * rcpf(var), lg2f(var * yq.y));
+  } else {
+    return (f - yq.x) - yq.x * (kLn2 * lg2f(f * yq.y));
+  }
+}
+
+template <int NZ>
+__device__ __forceinline__ double finish_energy(const GroupDesc& g, double s) {
+  if (!isfinite(s)) return dinf();  // var <= 0 / f <= 0 sentinel (energy.cpp:16, :20, :25)
+  return g.e_a0 + g.e_a1 * s;
+}
+
+template <int PPL, int W, int NZ>
+__device__ __forceinline__ double eval_plain_nz(const GroupDesc& g, Unit<PPL, W>& u, const float (&Pn)[PPL]) {
+  float acc = 0.f;
+#pragma unroll
+  for (int k = 0; k < PPL; ++k) {
+    const float4 yq = u.y(k);
+    acc = fmaf(yq.z, noise_term<NZ>(g, Pn[k], yq), acc);
+  }
+  return finish_energy<NZ>(g, unit_sum(u, acc));
+}
+
+// Shirley background + energy (lineshapes.hpp:65-83, model.cpp:289-292).
+// amp_bound >= max_k |P_k| (sum of |amplitudes|) decides the degenerate-signal
+// test without a max reduction unless it is inconclusive.
+template <int PPL, int W, int NZ>
+__device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, W>& u, const float (&Pn)[PPL],
+                                                  float bga, float bgb, float amp_bound) {
+  float Cn[PPL];
+  float run = 0.f;
+#pragma unroll
+  for (int k = 0; k < PPL; ++k) {
+    const float2 c = u.c(k);
+    run = fmaf(c.x, Pn[k], run);
+    Cn[k] = fmaf(-c.y, Pn[k], run);
+  }
+  const float incl = warp_incl_scan_f(run, u.lane);
+  float prefix = incl - run;
+  float total = __shfl_sync(0xffffffffu, incl, 31);
+  if (W > 1) {
+    if (u.lane == 0) u.xc->scan[u.par][u.wiu] = total;
+    u.sync();
+    float pre = 0.f, tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const float s = u.xc->scan[u.par][w];
+      if (w < u.wiu) pre += s;
+      tot += s;
+    }
+    prefix += pre;
+    total = tot;
+  }
+  const float ba = bgb - bga;
+  bool degen = !(total > 1e-12f * amp_bound * g.range);
+  if (degen) {  // inconclusive bound: exact max over the real points (rare)
+    float mx = -FLT_MAX;
+#pragma unroll
+    for (int k = 0; k < PPL; ++k)
+      if (u.y(k).z > 0.f) mx = fmaxf(mx, Pn[k]);
+    mx = warp_max_f(mx);
+    if (W > 1) {
+      u.sync();  // everyone has consumed scan[par] above
+      if (u.lane == 0) u.xc->scan[u.par][u.wiu] = mx;
+      u.sync();
+      for (int w = 0; w < W; ++w) mx = fmaxf(mx, u.xc->scan[u.par][w]);
+      u.sync();
+    }
+    degen = !(total > 1e-12f * mx * g.range);
+  }
+  float acc = 0.f;
+  if (!degen) {
+    const float scale = ba / total;
+#pragma unroll
+    for (int k = 0; k < PPL; ++k) {
+      const float B = fmaf(scale, prefix + Cn[k], bga);
+      const float4 yq = u.y(k);
+      acc = fmaf(yq.z, noise_term<NZ>(g, Pn[k] + B, yq), acc);
+    }
+  } else {  // linear ramp a -> b
+#pragma unroll
+    for (int k = 0; k < PPL; ++k) {
+      const float B = fmaf(ba, (u.x(k) - g.x0s) * g.inv_range, bga);
+      const float4 yq = u.y(k);
+      acc = fmaf(yq.z, noise_term<NZ>(g, Pn[k] + B, yq), acc);
+    }
+  }
+  return finish_energy<NZ>(g, unit_sum(u, acc));
+}
+
+template <int FAM, int PPL, int W>
+__device__ __forceinline__ double evaluate(const GroupDesc& g, Unit<PPL, W>& u, const float (&Pn)[PPL], float bga,
+                                           float bgb, float amp_bound) {
+  if (FAM == FAM_XPS) {
+    switch (g.noise) {
+      case NZ_GAUSS: return eval_shirley_nz<PPL, W, NZ_GAUSS>(g, u, Pn, bga, bgb, amp_bound);
+      case NZ_HETERO: return eval_shirley_nz<PPL, W, NZ_HETERO>(g, u, Pn, bga, bgb, amp_bound);
+      default: return eval_shirley_nz<PPL, W, NZ_POISSON>(g, u, Pn, bga, bgb, amp_bound);
+    }
+  } else {
+    switch (g.noise) {
+      case NZ_GAUSS: return eval_plain_nz<PPL, W, NZ_GAUSS>(g, u, Pn);
+      case NZ_HETERO: return eval_plain_nz<PPL, W, NZ_HETERO>(g, u, Pn);
+      default: return eval_plain_nz<PPL, W, NZ_POISSON>(g, u, Pn);
+    }
+  }
+}
+
+// lp_new - lp_old for one component (priors.cpp:22-35); false = -inf (reject)
+__device__ __forceinline__ bool prior_delta(int kind, double a, double b, double xo, double xn, double& dlp) {
+  if (kind == PR_UNIFORM) {
+    if (xn < a || xn > b) return false;
+    dlp = (xo < a || xo > b) ? dinf() : 0.0;
+    return true;
+  }
+  if (kind == PR_NORMAL) {
+    const double dn = xn - a, dd = xo - a;
+    dlp = (dd * dd - dn * dn) / (2.0 * b);
+    return true;
+  }
+  if (!(xn > 0.0)) return false;
+  if (!(xo > 0.0)) {
+    dlp = dinf();
+    return true;
+  }
+  dlp = (a - 1.0) * (double)__logf((float)(xn / xo)) - b * (xn - xo);
+  return true;
+}
+
+__device__ __forceinline__ int find_group(const int* prefix, int n, int x) {
+  int lo = 0, hi = n - 1;  // largest gi with prefix[gi] <= x
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (prefix[mid] <= x)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+template <int FAM>
+__device__ __forceinline__ float amp_bound(const GroupDesc& g, const double* th, int ovr_i, double ovr_v) {
+  if (FAM != FAM_XPS) return 0.f;
+  float s = 0.f;
+  for (int b = 0; b < g.K; ++b) s += fabsf((float)(4 * b == ovr_i ? ovr_v : th[4 * b]));
+  return s;
+}
+
+template <int FAM, int PPL, int W, bool ENERGY>
+__global__ void __launch_bounds__(W >= 8 ? 32 * W : 256, W >= 8 ? 1 : 2)
+    k_chain(const GroupDesc* __restrict__ gds, const int* __restrict__ list, const int* __restrict__ cta_prefix,
+            int n_list, int U, int dpad) {
+  using SM = Smem<PPL, W>;
+  constexpr int L = 32 * W;
+  constexpr int stride = block_stride<FAM>();
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int gi = find_group(cta_prefix, n_list, blockIdx.x);
+  const GroupDesc& g = gds[list[gi]];
+  const int cta_in_group = blockIdx.x - cta_prefix[gi];
+
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  float* sx = reinterpret_cast<float*>(smem + SM::off_x);
+  float2* sc = reinterpret_cast<float2*>(smem + SM::off_c);
+  float4* sy = reinterpret_cast<float4*>(smem + SM::off_y);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wb = smem + SM::off_w + (size_t)warp * SM::per_warp(dpad);
+  double* th = reinterpret_cast<double*>(wb);
+  double* lsv = th + dpad;
+  int* acc = reinterpret_cast<int*>(lsv + dpad);
+  float* zb = reinterpret_cast<float*>(acc + dpad);
+  float* ub = zb + dpad;
+  const size_t xoff = ((SM::off_w + (size_t)U * W * SM::per_warp(dpad)) + 15) & ~(size_t)15;
+  Xch* xcs = reinterpret_cast<Xch*>(smem + xoff);
+
+  // ---- stage the spectrum: cp.async.bulk (UBLKCP) completing on an mbarrier
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    constexpr uint32_t bx = SM::NPT * 4u, bc = SM::NPT * 8u, by = SM::NPT * 16u;
+    mbar_expect_tx(bar, bx + (FAM == FAM_XPS ? bc : 0u) + by);
+    bulk_g2s(sx, g.spec_x, bx, bar);
+    if (FAM == FAM_XPS) bulk_g2s(sc, g.spec_c, bc, bar);
+    bulk_g2s(sy, g.spec_y, by, bar);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+
+  const int unit = warp / W, wiu = warp - unit * W;
+  const int c = cta_in_group * U + unit;
+  const int units = ENERGY ? g.T : g.S;
+  if (c >= units) return;  // the whole unit leaves; no CTA-wide barrier follows
+
+  Unit<PPL, W> u;
+  u.sx = sx;
+  u.sc = sc;
+  u.sy = sy;
+  u.xc = xcs + unit;
+  u.lg = wiu * 32 + lane;
+  u.wiu = wiu;
+  u.lane = lane;
+  u.bar_id = 1 + unit;
+  u.par = 0;
+
+  const GroupState* st = g.st;
+  const int cur = st->cur;
+  const int d = g.d, T = g.T;
+  const double* thc = g.theta[cur];
+  const int src = ENERGY ? c : g.anc[c];
+  for (int i = lane; i < d; i += 32) {
+    th[i] = thc[(size_t)i * T + src];
+    if (!ENERGY) {
+      lsv[i] = g.ls0[i];
+      acc[i] = 0;
+    }
+  }
+  __syncwarp();
+
+  const int ibg = 4 * g.K;  // xps Shirley endpoints (a, b) at ibg, ibg + 1
+  float P[PPL];
+  bool pvalid = full_signal<FAM, PPL, W>(g, th, -1, 0.0, u, P);
+  double e = pvalid ? evaluate<FAM, PPL, W>(g, u, P, FAM == FAM_XPS ? (float)th[ibg] : 0.f,
+                                            FAM == FAM_XPS ? (float)th[ibg + 1] : 0.f,
+                                            amp_bound<FAM>(g, th, -1, 0.0))
+                    : dinf();
+  if (ENERGY) {
+    if (wiu == 0 && lane == 0) g.E[cur][c] = e;
+    return;
+  }
+
+  // ---- waste-free chain: n sweeps at beta_next, every post-sweep state kept
+  const int n = g.n, S = g.S;
+  const int level = st->level;
+  const double beta = st->beta;
+  const double nd = g.n_data;
+  const int adapt_sweeps = (n + 1) / 2;  // smc.cpp:136
+  const uint32_t cg = g.chain_base + (uint32_t)c;
+  double* thn = g.theta[cur ^ 1];
+  double* En = g.E[cur ^ 1];
+  const int npeak = FAM == FAM_OFFSET ? 0 : stride * g.K;
+  unsigned long long trials = 0;
+  float G[PPL];
+  float Pn[PPL];
+  bool gvalid = false;
+
+  for (int t = 1; t <= n; ++t) {
+    // Philox draws of this sweep: lane i handles components i, i+32, ...
+    for (int i = lane; i < d; i += 32) {
+      const u32x4 o = philox(u32x4{cg, (uint32_t)level, (uint32_t)((t - 1) * d + i), ROLE_CHAIN}, g.key0, g.key1);
+      zb[i] = normal_f32(o.x, o.y);
+      ub[i] = __logf(u01_open_lo(o.z));
+    }
+    __syncwarp();
+    const float gam = (t <= adapt_sweeps) ? exp2f(-0.6f * log2f((float)t)) : 0.f;  // t^-0.6 (mcmc.cpp:15)
+    for (int i = 0; i < d; ++i) {
+      const int b = i / stride, j = i - b * stride;
+      const bool peak = i < npeak;
+      if (peak && j == 0) {  // entering block b: cache g_b(x)
+        const BlockC cb = block_consts<FAM>(th + b * stride);
+        gvalid = cb.ok && pvalid;
+        if (gvalid) {
+#pragma unroll
+          for (int k = 0; k < PPL; ++k) G[k] = shape<FAM>(cb, u.x(k));
+        }
+      }
+      const double old_i = th[i];
+      const double new_i = old_i + (double)__expf((float)lsv[i]) * (double)zb[i];
+      double dlp = 0.0;
+      const bool in_support = prior_delta(g.pkind[i], g.pa[i], g.pb[i], old_i, new_i, dlp);
+      bool accept = false;
+      if (in_support) {
+        ++trials;
+        bool nvalid = true;
+        if (FAM == FAM_OFFSET || !pvalid || (peak && !gvalid)) {
+          nvalid = full_signal<FAM, PPL, W>(g, th, i, new_i, u, Pn);
+        } else if (!peak) {  // Shirley endpoint: enters combine() only (block -1)
+#pragma unroll
+          for (int k = 0; k < PPL; ++k) Pn[k] = P[k];
+        } else if (j == 0 && old_i != 0.0) {  // amplitude: g' = (A'/A) g
+          const float r = (float)(new_i / old_i - 1.0);
+#pragma unroll
+          for (int k = 0; k < PPL; ++k) Pn[k] = fmaf(r, G[k], P[k]);
+        } else {
+          double pn[stride];
+#pragma unroll
+          for (int q = 0; q < stride; ++q) pn[q] = (q == j) ? new_i : th[b * stride + q];
+          const BlockC cn = block_consts<FAM>(pn);
+          nvalid = cn.ok;
+          if (nvalid) {
+#pragma unroll
+            for (int k = 0; k < PPL; ++k) Pn[k] = P[k] + (shape<FAM>(cn, u.x(k)) - G[k]);
+          }
+        }
+        float bga = 0.f, bgb = 0.f, ab = 0.f;
+        if (FAM == FAM_XPS) {
+          bga = (float)(i == ibg ? new_i : th[ibg]);
+          bgb = (float)(i == ibg + 1 ? new_i : th[ibg + 1]);
+          ab = amp_bound<FAM>(g, th, i, new_i);
+        }
+        const double e_new = nvalid ? evaluate<FAM, PPL, W>(g, u, Pn, bga, bgb, ab) : dinf();
+        // mcmc.cpp:72-80
+        double lr;
+        const bool inf_new = e_new == dinf(), inf_old = e == dinf();
+        if (beta == 0.0 || (inf_new && inf_old))
+          lr = dlp;
+        else if (inf_new)
+          lr = -dinf();
+        else if (inf_old)
+          lr = dinf();
+        else
+          lr = -beta * nd * (e_new - e) + dlp;
+        accept = lr >= 0.0 || (double)ub[i] < lr;
+        if (accept) {
+          if (peak && gvalid && nvalid) {
+#pragma unroll
+            for (int k = 0; k < PPL; ++k) G[k] += Pn[k] - P[k];
+          } else if (peak) {
+            gvalid = false;
+          }
+#pragma unroll
+          for (int k = 0; k < PPL; ++k) P[k] = Pn[k];
+          if (pvalid != nvalid) gvalid = false;
+          pvalid = nvalid;
+          e = e_new;
+          if (lane == 0) {
+            th[i] = new_i;
+            acc[i] += 1;
+          }
+        }
+      }
+      if (t <= adapt_sweeps && lane == 0) {  // robbins_monro_update in log space (mcmc.cpp:14-18)
+        const double ls = lsv[i] + (double)gam * ((accept ? 1.0 : 0.0) - 0.5);
+        lsv[i] = fmin(fmax(ls, kLogStepMin), kLogStepMax);
+      }
+      __syncwarp();
+    }
+    const size_t slot = (size_t)c * n + (t - 1);  // smc.cpp:151
+    if (wiu == 0) {
+      for (int i = lane; i < d; i += 32) thn[(size_t)i * T + slot] = th[i];
+      if (lane == 0) En[slot] = e;
+    }
+  }
+  if (wiu == 0) {
+    for (int i = lane; i < d; i += 32) {
+      g.chain_acc[(size_t)i * S + c] = acc[i];
+      g.chain_ls[(size_t)i * S + c] = lsv[i];
+    }
+    if (lane == 0) atomicAdd(&g.st->trials, trials);
+  }
+}
+
+// ------------------------------------------------------------------ launch
+template <int FAM, int PPL, int W, bool ENERGY>
+cudaError_t launch_chain_t(int U, int dmax, const GroupDesc* gds, const int* list, const int* prefix, int n_list,
+                           int total_ctas, cudaStream_t st) {
+  const int dpad = (dmax + 1) & ~1;
+  const size_t smem = Smem<PPL, W>::bytes(U, dpad);
+  auto kern = k_chain<FAM, PPL, W, ENERGY>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  kern<<<total_ctas, 32 * W * U, smem, st>>>(gds, list, prefix, n_list, U, dpad);
+  return cudaGetLastError();
+}
+
+// (W, PPL) pairs compiled (see pick_shape in kernels.cu)
+#define SMC_FOR_EACH_SHAPE(X) \
+  X(1, 2) X(1, 4) X(1, 6) X(1, 8) X(1, 10) X(1, 12) X(1, 14) X(1, 16) \
+  X(2, 12) X(2, 14) X(2, 16) X(4, 12) X(4, 14) X(4, 16) X(8, 12) X(8, 14) X(8, 16) X(16, 12) X(16, 14) X(16, 16)
+
+template <int FAM, bool ENERGY>
+cudaError_t launch_chain_fam(const Shape& s, int dmax, const GroupDesc* gds, const int* list, const int* prefix,
+                             int n_list, int total_ctas, cudaStream_t st) {
+#define SMC_CASE(WW, PP) \
+  if (s.W == WW && s.PPL == PP) return launch_chain_t<FAM, PP, WW, ENERGY>(s.U, dmax, gds, list, prefix, n_list, total_ctas, st);
+  SMC_FOR_EACH_SHAPE(SMC_CASE)
+#undef SMC_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace smc

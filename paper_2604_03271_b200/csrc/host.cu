@@ -180,8 +180,8 @@ struct Arena {
 // --------------------------------------------------------- host-side prep
 struct PreparedSpectrum {
   std::vector<float> x;
-  std::vector<float> c;  // pairs
-  std::vector<float> y;  // pairs
+  std::vector<float> c;  // (c_k, h_{k+1}) pairs
+  std::vector<float> y;  // (y_k, 1/s_k, weight, 0) quads
   double x_shift = 0.0;
   float x0s = 0.f, inv_range = 0.f, range = 0.f;
   double e_a0 = 0.0, e_a1 = 0.0;
@@ -198,7 +198,7 @@ PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, 
   const size_t npt = (size_t)s.PPL * L;
   ps.x.assign(npt, 0.f);
   ps.c.assign(2 * npt, 0.f);
-  ps.y.assign(2 * npt, 0.f);
+  ps.y.assign(4 * npt, 0.f);
   ps.x_shift = x_shift;
   const double range = xs[N - 1] - xs[0];
   ps.range = (float)range;
@@ -234,11 +234,12 @@ PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, 
         h2 = m.s2 * m.s2;
         q = m.paper_literal ? 1.0 : 0.5;
       }
+      // device terms are lg2(var/s) + q' r^2/var with q' = q / (ln2/2)
       ps.nz = NZ_HETERO;
       ps.a0 = (float)h0;
       ps.a1 = (float)h1;
       ps.a2 = (float)h2;
-      ps.q = (float)q;
+      ps.q = (float)(q / (0.5 * M_LN2));
       for (int64_t i = 0; i < N; ++i) {
         const double y = std::fabs(ys[i]);
         double sc = h0 * y + h1 * y * y + h2;
@@ -247,27 +248,25 @@ PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, 
         a0 += 0.5 * std::log(2.0 * M_PI * sc);
       }
       ps.e_a0 = a0 / (double)N;
-      ps.e_a1 = 1.0 / (double)N;
+      ps.e_a1 = 0.5 * M_LN2 / (double)N;
       break;
     }
   }
-  for (int64_t p = 0; p < N; ++p) {
+  // padding points replicate the last real point with weight 0 (no masks in the kernel)
+  for (size_t p = 0; p < npt; ++p) {
+    const int64_t q = p < (size_t)N ? (int64_t)p : N - 1;
+    const bool real = p < (size_t)N;
     const int lane = (int)(p / s.PPL), k = (int)(p % s.PPL);
     const size_t idx = (size_t)k * L + lane;
-    const double hk = p > 0 ? 0.5 * (xs[p] - xs[p - 1]) : 0.0;
-    const double hk1 = p + 1 < N ? 0.5 * (xs[p + 1] - xs[p]) : 0.0;
-    ps.x[idx] = (float)(xs[p] - x_shift);
-    ps.c[2 * idx] = (float)(hk + hk1);
-    ps.c[2 * idx + 1] = (float)hk1;
-    ps.y[2 * idx] = (float)ys[p];
-    ps.y[2 * idx + 1] = (float)inv_s[p];
-  }
-  for (size_t p = N; p < npt; ++p) {  // padding lanes: masked, finite
-    const int lane = (int)(p / s.PPL), k = (int)(p % s.PPL);
-    const size_t idx = (size_t)k * L + lane;
-    ps.x[idx] = (float)(xs[N - 1] - x_shift);
-    ps.y[2 * idx] = 1.f;
-    ps.y[2 * idx + 1] = 1.f;
+    const double hk = q > 0 ? 0.5 * (xs[q] - xs[q - 1]) : 0.0;
+    const double hk1 = q + 1 < N ? 0.5 * (xs[q + 1] - xs[q]) : 0.0;
+    ps.x[idx] = (float)(xs[q] - x_shift);
+    ps.c[2 * idx] = real ? (float)(hk + hk1) : 0.f;
+    ps.c[2 * idx + 1] = real ? (float)hk1 : 0.f;
+    ps.y[4 * idx] = (float)ys[q];
+    ps.y[4 * idx + 1] = (float)inv_s[q];
+    ps.y[4 * idx + 2] = real ? 1.f : 0.f;
+    ps.y[4 * idx + 3] = 0.f;
   }
   return ps;
 }
@@ -366,7 +365,7 @@ void run_class(Device& dev, const std::vector<RunSpec>& runs, const std::vector<
   const int L = 32 * shape.W;
   const size_t npt = (size_t)shape.PPL * L;
   size_t bytes = Arena::al(sizeof(GroupDesc) * G) + Arena::al(sizeof(GroupState) * G) + 4 * Arena::al(4 * (G + 1));
-  bytes += prep.size() * (Arena::al(npt * 4) + 2 * Arena::al(npt * 8));
+  bytes += prep.size() * (Arena::al(npt * 4) + Arena::al(npt * 8) + Arena::al(npt * 16));
   for (int r : idx) {
     const auto& R = runs[r];
     const size_t T = R.cfg.T, d = R.m.d, S = T / R.cfg.n;
@@ -387,14 +386,14 @@ void run_class(Device& dev, const std::vector<RunSpec>& runs, const std::vector<
   cudaStream_t st = dev.stream;
 
   std::map<std::pair<int, double>, const PreparedSpectrum*> pmap;
-  std::map<std::pair<int, double>, std::tuple<float*, float2*, float2*>> dspec;
+  std::map<std::pair<int, double>, std::tuple<float*, float2*, float4*>> dspec;
   for (auto& kv : prep) {
     float* x = ar.take<float>(npt);
     float2* c = ar.take<float2>(npt);
-    float2* y = ar.take<float2>(npt);
+    float4* y = ar.take<float4>(npt);
     h2d(x, kv.second.x.data(), npt, st);
     h2d(reinterpret_cast<float*>(c), kv.second.c.data(), 2 * npt, st);
-    h2d(reinterpret_cast<float*>(y), kv.second.y.data(), 2 * npt, st);
+    h2d(reinterpret_cast<float*>(y), kv.second.y.data(), 4 * npt, st);
     dspec[kv.first] = std::make_tuple(x, c, y);
   }
 
@@ -777,7 +776,7 @@ int specmc_energy_batch(const specmc_model_desc* model, const double* xs, const 
     const size_t npt = ps.x.size();
     float* dx = sc.alloc<float>(npt);
     float2* dc = sc.alloc<float2>(npt);
-    float2* dy = sc.alloc<float2>(npt);
+    float4* dy = sc.alloc<float4>(npt);
     int* pk = sc.alloc<int>(d);
     double* pa = sc.alloc<double>(d);
     double* pb = sc.alloc<double>(d);
@@ -790,7 +789,7 @@ int specmc_energy_batch(const specmc_model_desc* model, const double* xs, const 
     cudaStream_t st = dev.stream;
     h2d(dx, ps.x.data(), npt, st);
     h2d(reinterpret_cast<float*>(dc), ps.c.data(), 2 * npt, st);
-    h2d(reinterpret_cast<float*>(dy), ps.y.data(), 2 * npt, st);
+    h2d(reinterpret_cast<float*>(dy), ps.y.data(), 4 * npt, st);
     h2d(pk, R.pk.data(), d, st);
     h2d(pa, R.pa.data(), d, st);
     h2d(pb, R.pb.data(), d, st);

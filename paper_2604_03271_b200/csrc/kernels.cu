@@ -1,493 +1,19 @@
-// kernels.cu -- sm_100a kernels of the B200 waste-free SMC sampler.
+// kernels.cu -- level-wide sm_100a kernels of the B200 waste-free SMC sampler.
 //
 //   k_init_draw   prior draws, one thread per particle        (smc.cpp:34-53, priors.cpp:105-110)
-//   k_chain<E=1>  batched full energies, one chain unit each  (energy.cpp:43-55 + :7-28)   [K2]
-//   k_chain<E=0>  fused propose/evaluate/accept move          (smc.cpp:142-156, mcmc.cpp:55-96) [K3]
 //   k_temper      ESS bisection, weights, evidence, systematic resampling, step prediction
-//                                                             (smc.cpp:55-112, :128-135, mcmc.cpp:20-53)
+//                 (one CTA per SMC run)                       (smc.cpp:55-112, :128-135, mcmc.cpp:20-53)
 //   k_stats       step-size statistics and history            (smc.cpp:162-183)
-//
+//   k_unit_*      single-array parity units of the same device functions
+// The chain-parallel kernel (energies K2, fused move K3) lives in chain.cuh and
+// is instantiated per family in chain_<family>_<mode>.cu.
 // Reference paths are relative to the reference root (proj/...).
-//
-// A "chain unit" is W warps (32*W lanes).  Lane l owns the PPL consecutive
-// spectrum points [l*PPL, (l+1)*PPL) and keeps the committed peak signal P and
-// the trial signal Pn for them in registers.  The observed spectrum is staged
-// once per CTA into shared memory with cp.async.bulk and read lane-transposed.
-// A proposal changes one block (peak), so the trial signal is
-// Pn = P + g_new - g_old (2 shape evaluations per point instead of the
-// reference's K-block recombination, model.cpp:285-294).  The xps Shirley
-// background (lineshapes.hpp:65-83) needs the cumulative trapezoid integral
-// of Pn: it is written as C_k = sum_{j<=k} c_j Pn_j - h_{k+1} Pn_k, i.e. one
-// lane-local inclusive scan plus one warp (and cross-warp) scan per proposal.
-// Energies are summed per lane in fp32 from O(1) centred terms and reduced
-// across lanes in fp64; the energy of the committed state is carried in fp64.
 #include <cfloat>
 #include <cmath>
 
-#include "launch.h"
+#include "chain.cuh"
 
 namespace smc {
-
-__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
-
-constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kHalfLn2 = 0.34657359027997264f;
-constexpr float kLn2 = 0.6931471805599453f;
-
-// ------------------------------------------------------------ block shapes
-// Per-block fp32 constants of one peak; location parameters are in shifted
-// coordinates (x' = x - x_shift, mu' = mu - x_shift) on the device.
-struct BlockC {
-  float mu, c1, c2, c3;
-  bool ok;
-};
-
-template <int FAM>
-__device__ __forceinline__ int block_stride() {
-  return FAM == FAM_GM ? 3 : (FAM == FAM_XPS ? 4 : 1);
-}
-
-// gm:  g = A exp(-1/2 b (x-mu)^2)                          (model.cpp:216-220)
-// xps: g = A [eta 2^(-u) + (1-eta) / (1 + u)], u = (x-mu)^2 / sigma^2
-//      (= A [eta exp(-ln2 d^2/s^2) + (1-eta) s^2/(s^2+d^2)], model.cpp:269-280)
-// offset: g = theta_0                                      (conjugate_oracle.hpp:22-26)
-template <int FAM>
-__device__ __forceinline__ BlockC block_consts(const double* p) {
-  BlockC c;
-  c.ok = true;
-  c.c3 = 0.f;
-  if (FAM == FAM_GM) {
-    c.c1 = (float)p[0];
-    c.mu = (float)p[1];
-    c.c2 = (float)(-0.5 * p[2] * 1.4426950408889634);
-  } else if (FAM == FAM_XPS) {
-    const double A = p[0], sig = p[2], eta = p[3];
-    c.ok = sig > 0.0;
-    c.mu = (float)p[1];
-    c.c1 = (float)(A * eta);
-    c.c2 = (float)(A * (1.0 - eta));
-    c.c3 = (float)(1.0 / (sig * sig));
-  } else {
-    c.c1 = (float)p[0];
-    c.mu = 0.f;
-    c.c2 = 0.f;
-  }
-  return c;
-}
-
-template <int FAM>
-__device__ __forceinline__ float shape(const BlockC& b, float x) {
-  if (FAM == FAM_GM) {
-    const float d = x - b.mu;
-    return b.c1 * ex2f(b.c2 * (d * d));
-  } else if (FAM == FAM_XPS) {
-    const float d = x - b.mu;
-    const float u = (d * d) * b.c3;
-    return fmaf(b.c1, ex2f(-u), b.c2 * rcpf(1.0f + u));
-  } else {
-    return b.c1;
-  }
-}
-
-// ------------------------------------------------------------- chain unit
-struct Xch {  // per-unit cross-warp exchange, double-buffered by parity
-  float2 scan[2][16];
-  double en[2][16];
-  int flt[2][16];
-};
-
-struct UnitCtx {
-  const float* sx;
-  const float2* sc;
-  const float2* sy;
-  Xch* xc;
-  int lg, L, W, wiu, lane, bar_id, p0;
-  int par;
-};
-
-__device__ __forceinline__ void unit_sync(const UnitCtx& u) {
-  if (u.W > 1) named_bar(u.bar_id, 32 * u.W);
-}
-
-// signal without background: P_k = sum_b g_b(x_k), blocks in layout order
-// (combine, model.cpp:287-288).  Optional override of one parameter.
-template <int FAM, int PPL>
-__device__ __forceinline__ bool full_signal(const GroupDesc& g, const double* th, int ovr_i, double ovr_v,
-                                            const UnitCtx& u, float (&P)[PPL]) {
-#pragma unroll
-  for (int k = 0; k < PPL; ++k) P[k] = 0.f;
-  const int stride = block_stride<FAM>();
-  const int nb = FAM == FAM_OFFSET ? 1 : g.K;
-  bool ok = true;
-  for (int b = 0; b < nb; ++b) {
-    double p[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (j < stride) p[j] = (b * stride + j == ovr_i) ? ovr_v : th[b * stride + j];
-    const BlockC c = block_consts<FAM>(p);
-    ok = ok && c.ok;
-#pragma unroll
-    for (int k = 0; k < PPL; ++k) P[k] += shape<FAM>(c, u.sx[k * u.L + u.lg]);
-  }
-  return ok;
-}
-
-// trial signal for component i set to v.  Returns false on a shape fault.
-template <int FAM, int PPL>
-__device__ __forceinline__ bool trial_signal(const GroupDesc& g, const double* th, int i, double v, const UnitCtx& u,
-                                             const float (&P)[PPL], bool pvalid, float (&Pn)[PPL]) {
-  const int stride = block_stride<FAM>();
-  if (FAM == FAM_OFFSET) return full_signal<FAM, PPL>(g, th, i, v, u, Pn);
-  if (FAM == FAM_XPS && i >= 4 * g.K) {  // Shirley endpoint: enters combine() only (block -1)
-    if (pvalid) {
-#pragma unroll
-      for (int k = 0; k < PPL; ++k) Pn[k] = P[k];
-      return true;
-    }
-    return full_signal<FAM, PPL>(g, th, i, v, u, Pn);
-  }
-  if (!pvalid) return full_signal<FAM, PPL>(g, th, i, v, u, Pn);
-  const int b = i / stride, j = i - b * stride;
-  double po[4], pn[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (q < stride) {
-      po[q] = th[b * stride + q];
-      pn[q] = (q == j) ? v : po[q];
-    }
-  const BlockC cn = block_consts<FAM>(pn);
-  if (!cn.ok) return false;
-  const BlockC co = block_consts<FAM>(po);
-#pragma unroll
-  for (int k = 0; k < PPL; ++k) {
-    const float x = u.sx[k * u.L + u.lg];
-    Pn[k] = P[k] + (shape<FAM>(cn, x) - shape<FAM>(co, x));
-  }
-  return true;
-}
-
-// per-point centred negative log-likelihood term (data_energy, energy.cpp:7-28)
-//   gauss:  r^2                                         E = a0 + a1 * sum
-//   hetero: 1/2 ln(var/s_k) + q r^2/var, var = a1 f^2 + a0 f + a2  (GaussApprox = (1,0,0))
-//   poisson: f - y - y ln(f/y)  (deviance form)
-template <int NZ>
-__device__ __forceinline__ float noise_term(const GroupDesc& g, float f, float2 yq, bool& flt) {
-  const float r = yq.x - f;
-  if (NZ == NZ_GAUSS) {
-    return r * r;
-  } else if (NZ == NZ_HETERO) {
-    const float var = fmaf(fmaf(g.nz_a1, f, g.nz_a0), f, g.nz_a2);
-    flt = flt || !(var > 0.f);
-    return fmaf(kHalfLn2, lg2f(var * yq.y), g.nz_q * (r * r) * rcpf(var));
-  } else {
-    flt = flt || !(f > 0.f);
-    return (f - yq.x) - yq.x * (kLn2 * lg2f(f * yq.y));
-  }
-}
-
-// fp64 reduction of the lane partials over the unit; identical in every warp
-__device__ __forceinline__ double unit_energy(const GroupDesc& g, UnitCtx& u, float acc, bool flt) {
-  double s = warp_sum_d((double)acc);
-  bool wf = __any_sync(0xffffffffu, flt);
-  if (u.W > 1) {
-    if (u.lane == 0) {
-      u.xc->en[u.par][u.wiu] = s;
-      u.xc->flt[u.par][u.wiu] = wf ? 1 : 0;
-    }
-    unit_sync(u);
-    s = 0.0;
-    wf = false;
-    for (int w = 0; w < u.W; ++w) {
-      s += u.xc->en[u.par][w];
-      wf = wf || u.xc->flt[u.par][w];
-    }
-  }
-  u.par ^= 1;
-  return wf ? dinf() : g.e_a0 + g.e_a1 * s;
-}
-
-template <int PPL, int NZ>
-__device__ __forceinline__ double eval_plain_nz(const GroupDesc& g, UnitCtx& u, const float (&Pn)[PPL]) {
-  float acc = 0.f;
-  bool flt = false;
-#pragma unroll
-  for (int k = 0; k < PPL; ++k) {
-    const float2 yq = u.sy[k * u.L + u.lg];
-    bool f1 = false;
-    const float l = noise_term<NZ>(g, Pn[k], yq, f1);
-    if (u.p0 + k < g.N) {
-      acc += l;
-      flt = flt || f1;
-    }
-  }
-  return unit_energy(g, u, acc, flt);
-}
-
-// Shirley background + energy (lineshapes.hpp:65-83, model.cpp:289-292)
-template <int PPL, int NZ>
-__device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, UnitCtx& u, const float (&Pn)[PPL], float bga,
-                                                  float bgb) {
-  float Cn[PPL];
-  float run = 0.f, mx = -FLT_MAX;
-#pragma unroll
-  for (int k = 0; k < PPL; ++k) {
-    const float2 c = u.sc[k * u.L + u.lg];
-    run = fmaf(c.x, Pn[k], run);
-    Cn[k] = fmaf(-c.y, Pn[k], run);
-    if (u.p0 + k < g.N) mx = fmaxf(mx, Pn[k]);
-  }
-  const float incl = warp_incl_scan_f(run, u.lane);
-  float prefix = incl - run;
-  float total = __shfl_sync(0xffffffffu, incl, 31);
-  float gmax = warp_max_f(mx);
-  if (u.W > 1) {
-    if (u.lane == 0) u.xc->scan[u.par][u.wiu] = make_float2(total, gmax);
-    unit_sync(u);
-    float pre = 0.f, tot = 0.f, gm = -FLT_MAX;
-    for (int w = 0; w < u.W; ++w) {
-      const float2 s = u.xc->scan[u.par][w];
-      if (w < u.wiu) pre += s.x;
-      tot += s.x;
-      gm = fmaxf(gm, s.y);
-    }
-    prefix += pre;
-    total = tot;
-    gmax = gm;
-  }
-  const float ba = bgb - bga;
-  const bool degen = !(total > 1e-12f * gmax * g.range);
-  const float scale = degen ? 0.f : ba / total;
-  float acc = 0.f;
-  bool flt = false;
-#pragma unroll
-  for (int k = 0; k < PPL; ++k) {
-    const int p = u.p0 + k;
-    float B = degen ? fmaf(ba, (u.sx[k * u.L + u.lg] - g.x0s) * g.inv_range, bga) : fmaf(scale, prefix + Cn[k], bga);
-    if (p == 0) B = bga;
-    if (p == g.N - 1) B = bgb;
-    const float2 yq = u.sy[k * u.L + u.lg];
-    bool f1 = false;
-    const float l = noise_term<NZ>(g, Pn[k] + B, yq, f1);
-    if (p < g.N) {
-      acc += l;
-      flt = flt || f1;
-    }
-  }
-  return unit_energy(g, u, acc, flt);
-}
-
-template <int FAM, int PPL>
-__device__ __forceinline__ double evaluate(const GroupDesc& g, UnitCtx& u, const float (&Pn)[PPL], float bga,
-                                           float bgb) {
-  if (FAM == FAM_XPS) {
-    switch (g.noise) {
-      case NZ_GAUSS: return eval_shirley_nz<PPL, NZ_GAUSS>(g, u, Pn, bga, bgb);
-      case NZ_HETERO: return eval_shirley_nz<PPL, NZ_HETERO>(g, u, Pn, bga, bgb);
-      default: return eval_shirley_nz<PPL, NZ_POISSON>(g, u, Pn, bga, bgb);
-    }
-  } else {
-    switch (g.noise) {
-      case NZ_GAUSS: return eval_plain_nz<PPL, NZ_GAUSS>(g, u, Pn);
-      case NZ_HETERO: return eval_plain_nz<PPL, NZ_HETERO>(g, u, Pn);
-      default: return eval_plain_nz<PPL, NZ_POISSON>(g, u, Pn);
-    }
-  }
-}
-
-// ------------------------------------------------------------------ priors
-// lp_new - lp_old for one component (priors.cpp:22-35); false = -inf (reject)
-__device__ __forceinline__ bool prior_delta(int kind, double a, double b, double xo, double xn, double& dlp) {
-  if (kind == PR_UNIFORM) {
-    if (xn < a || xn > b) return false;
-    dlp = (xo < a || xo > b) ? dinf() : 0.0;
-    return true;
-  }
-  if (kind == PR_NORMAL) {
-    const double dn = xn - a, dd = xo - a;
-    dlp = (dd * dd - dn * dn) / (2.0 * b);
-    return true;
-  }
-  if (!(xn > 0.0)) return false;
-  if (!(xo > 0.0)) {
-    dlp = dinf();
-    return true;
-  }
-  dlp = (a - 1.0) * (double)__logf((float)(xn / xo)) - b * (xn - xo);
-  return true;
-}
-
-// ------------------------------------------------------------- CTA -> group
-__device__ __forceinline__ int find_group(const int* prefix, int n, int x) {
-  int lo = 0, hi = n - 1;  // largest gi with prefix[gi] <= x
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (prefix[mid] <= x)
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  return lo;
-}
-
-// ------------------------------------------------------------ chain kernel
-// ENERGY = true : unit c evaluates the full energy of particle c of theta[cur]
-// ENERGY = false: unit c runs waste-free chain c of the current level
-template <int FAM, int PPL, bool ENERGY>
-__global__ void __launch_bounds__(256) k_chain(const GroupDesc* __restrict__ gds, const int* __restrict__ list,
-                                               const int* __restrict__ cta_prefix, int n_list, int W, int U,
-                                               int dpad) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int gi = find_group(cta_prefix, n_list, blockIdx.x);
-  const GroupDesc& g = gds[list[gi]];
-  const int cta_in_group = blockIdx.x - cta_prefix[gi];
-  const int L = 32 * W;
-  const int npt = PPL * L;
-
-  // ---- carve shared memory
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  float* sx = reinterpret_cast<float*>(smem + 16);
-  float2* sc = reinterpret_cast<float2*>(sx + npt);
-  float2* sy = sc + npt;
-  unsigned char* wbase = reinterpret_cast<unsigned char*>(sy + npt);
-  const int nwarps = blockDim.x >> 5;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* th = reinterpret_cast<double*>(wbase) + (size_t)warp * dpad;
-  double* lsv = reinterpret_cast<double*>(wbase) + (size_t)(nwarps + warp) * dpad;
-  int* acc = reinterpret_cast<int*>(reinterpret_cast<double*>(wbase) + (size_t)2 * nwarps * dpad) + (size_t)warp * dpad;
-  Xch* xcs = reinterpret_cast<Xch*>(reinterpret_cast<int*>(reinterpret_cast<double*>(wbase) + (size_t)2 * nwarps * dpad) +
-                                    (size_t)nwarps * dpad);
-
-  // ---- stage the spectrum (cp.async.bulk -> mbarrier)
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    const uint32_t bx = npt * 4u, bc = npt * 8u;
-    mbar_expect_tx(bar, bx + 2u * bc);
-    bulk_g2s(sx, g.spec_x, bx, bar);
-    bulk_g2s(sc, g.spec_c, bc, bar);
-    bulk_g2s(sy, g.spec_y, bc, bar);
-  }
-  __syncthreads();
-  mbar_wait(bar, 0);
-
-  const int unit = warp / W, wiu = warp - unit * W;
-  const int c = cta_in_group * U + unit;
-  const int units = ENERGY ? g.T : g.S;
-  if (c >= units) return;  // whole unit leaves together; no CTA-wide barrier follows
-
-  UnitCtx u;
-  u.sx = sx;
-  u.sc = sc;
-  u.sy = sy;
-  u.xc = xcs + unit;
-  u.lg = wiu * 32 + lane;
-  u.L = L;
-  u.W = W;
-  u.wiu = wiu;
-  u.lane = lane;
-  u.bar_id = 1 + unit;
-  u.p0 = u.lg * PPL;
-  u.par = 0;
-
-  const GroupState* st = g.st;
-  const int cur = st->cur;
-  const int d = g.d, T = g.T;
-  const double* thc = g.theta[cur];
-  const int src = ENERGY ? c : g.anc[c];
-  for (int i = lane; i < d; i += 32) {
-    th[i] = thc[(size_t)i * T + src];
-    if (!ENERGY) {
-      lsv[i] = g.ls0[i];
-      acc[i] = 0;
-    }
-  }
-  __syncwarp();
-
-  float P[PPL];
-  bool pvalid = full_signal<FAM, PPL>(g, th, -1, 0.0, u, P);
-  const int ibg = 4 * g.K;
-  double e = pvalid ? evaluate<FAM, PPL>(g, u, P, FAM == FAM_XPS ? (float)th[ibg] : 0.f,
-                                         FAM == FAM_XPS ? (float)th[ibg + 1] : 0.f)
-                    : dinf();
-  if (ENERGY) {
-    if (wiu == 0 && lane == 0) g.E[cur][c] = e;
-    return;
-  }
-
-  // ---- waste-free chain: n sweeps at beta_next, keep every post-sweep state
-  const int n = g.n, S = g.S;
-  const int level = st->level;
-  const double beta = st->beta;
-  const double nd = g.n_data;
-  const int adapt_sweeps = (n + 1) / 2;  // smc.cpp:136
-  const uint32_t cg = g.chain_base + (uint32_t)c;
-  double* thn = g.theta[cur ^ 1];
-  double* En = g.E[cur ^ 1];
-  unsigned long long trials = 0;
-  float Pn[PPL];
-
-  for (int t = 1; t <= n; ++t) {
-    const float gam = (t <= adapt_sweeps) ? exp2f(-0.6f * log2f((float)t)) : 0.f;  // t^-0.6 (mcmc.cpp:15)
-    for (int i = 0; i < d; ++i) {
-      const u32x4 o = philox(u32x4{cg, (uint32_t)level, (uint32_t)((t - 1) * d + i), ROLE_CHAIN}, g.key0, g.key1);
-      const float z = normal_f32(o.x, o.y);
-      const double old_i = th[i];
-      const double s = (double)__expf((float)lsv[i]);
-      const double new_i = old_i + s * (double)z;
-      double dlp = 0.0;
-      const bool in_support = prior_delta(g.pkind[i], g.pa[i], g.pb[i], old_i, new_i, dlp);
-      bool accept = false;
-      if (in_support) {
-        ++trials;
-        const bool nvalid = trial_signal<FAM, PPL>(g, th, i, new_i, u, P, pvalid, Pn);
-        float bga = 0.f, bgb = 0.f;
-        if (FAM == FAM_XPS) {
-          bga = (float)(i == ibg ? new_i : th[ibg]);
-          bgb = (float)(i == ibg + 1 ? new_i : th[ibg + 1]);
-        }
-        const double e_new = nvalid ? evaluate<FAM, PPL>(g, u, Pn, bga, bgb) : dinf();
-        // mcmc.cpp:72-80
-        double lr;
-        const bool inf_new = e_new == dinf(), inf_old = e == dinf();
-        if (beta == 0.0 || (inf_new && inf_old))
-          lr = dlp;
-        else if (inf_new)
-          lr = -dinf();
-        else if (inf_old)
-          lr = dinf();
-        else
-          lr = -beta * nd * (e_new - e) + dlp;
-        accept = lr >= 0.0 || (double)__logf(u01_open_lo(o.z)) < lr;
-        if (accept) {
-#pragma unroll
-          for (int k = 0; k < PPL; ++k) P[k] = Pn[k];
-          pvalid = nvalid;
-          e = e_new;
-          if (lane == 0) {
-            th[i] = new_i;
-            acc[i] += 1;
-          }
-        }
-      }
-      if (t <= adapt_sweeps && lane == 0) {  // robbins_monro_update in log space (mcmc.cpp:14-18)
-        double ls = lsv[i] + (double)gam * ((accept ? 1.0 : 0.0) - 0.5);
-        lsv[i] = fmin(fmax(ls, kLogStepMin), kLogStepMax);
-      }
-      __syncwarp();
-    }
-    const size_t slot = (size_t)c * n + (t - 1);  // smc.cpp:151
-    if (wiu == 0) {
-      for (int i = lane; i < d; i += 32) thn[(size_t)i * T + slot] = th[i];
-      if (lane == 0) En[slot] = e;
-    }
-  }
-  if (wiu == 0) {
-    for (int i = lane; i < d; i += 32) {
-      g.chain_acc[(size_t)i * S + c] = acc[i];
-      g.chain_ls[(size_t)i * S + c] = lsv[i];
-    }
-    if (lane == 0) atomicAdd(&g.st->trials, trials);
-  }
-}
 
 // ------------------------------------------------------------- init draws
 // rng.hpp:77-92 (Marsaglia-Tsang) in fp64 on a Philox stream
@@ -939,88 +465,58 @@ __global__ void k_unit_predict(const double* hist, int H, int d, double beta_nex
 }
 
 // ============================================================== launchers
-static const int kPPL[] = {2, 4, 6, 8, 10, 12, 14, 16};
+bool ppl_supported(int ppl) { return ppl >= 2 && ppl <= 16 && ppl % 2 == 0; }
 
-bool ppl_supported(int ppl) {
-  for (int p : kPPL)
-    if (p == ppl) return true;
-  return false;
-}
-
+// W warps per chain, PPL points per lane; must match SMC_FOR_EACH_SHAPE (chain.cuh)
 Shape pick_shape(int64_t N) {
-  int W = 1;
-  while (W < 16 && (int64_t)32 * W * 16 < N) W *= 2;
-  int ppl = 16;
-  for (int p : kPPL)
-    if ((int64_t)32 * W * p >= N) {
-      ppl = p;
-      break;
-    }
   Shape s;
-  s.W = W;
-  s.PPL = ppl;
-  s.U = W >= 8 ? 1 : 8 / W;
+  if (N <= 32 * 16) {
+    s.W = 1;
+    s.PPL = 16;
+    for (int p = 2; p <= 16; p += 2)
+      if (32 * p >= N) {
+        s.PPL = p;
+        break;
+      }
+  } else {
+    s.W = 2;
+    while (s.W < 16 && (int64_t)32 * s.W * 16 < N) s.W *= 2;
+    s.PPL = 16;
+    for (int p = 12; p <= 16; p += 2)
+      if ((int64_t)32 * s.W * p >= N) {
+        s.PPL = p;
+        break;
+      }
+  }
+  s.U = s.W >= 8 ? 1 : 8 / s.W;
   return s;
 }
 
 size_t chain_smem_bytes(const Shape& s, int dmax) {
   const int dpad = (dmax + 1) & ~1;
-  const int L = 32 * s.W;
-  const int nwarps = s.W * s.U;
-  size_t b = 16;                         // mbarrier
-  b += (size_t)s.PPL * L * (4 + 8 + 8);  // sx, sc, sy
-  b += (size_t)nwarps * dpad * (8 + 8 + 4);
+  const size_t npt = (size_t)s.PPL * 32 * s.W;
+  size_t b = 16 + npt * (4 + 8 + 16) + (size_t)s.U * s.W * dpad * (8 + 8 + 4 + 4 + 4);
   b = (b + 15) & ~(size_t)15;
-  b += (size_t)s.U * sizeof(Xch);
-  return b;
-}
-
-template <int FAM, int PPL, bool ENERGY>
-static cudaError_t launch_chain_t(const Shape& s, int dmax, const GroupDesc* gds, const int* list, const int* prefix,
-                                  int n_list, int total_ctas, cudaStream_t st) {
-  const size_t smem = chain_smem_bytes(s, dmax);
-  auto kern = k_chain<FAM, PPL, ENERGY>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const int dpad = (dmax + 1) & ~1;
-  kern<<<total_ctas, 32 * s.W * s.U, smem, st>>>(gds, list, prefix, n_list, s.W, s.U, dpad);
-  return cudaGetLastError();
-}
-
-template <bool ENERGY>
-static cudaError_t launch_chain(int family, const Shape& s, int dmax, const GroupDesc* gds, const int* list,
-                                const int* prefix, int n_list, int total_ctas, cudaStream_t st) {
-#define SMC_PPL_CASE(FAM, P) \
-  case P: return launch_chain_t<FAM, P, ENERGY>(s, dmax, gds, list, prefix, n_list, total_ctas, st);
-#define SMC_FAM_CASE(FAM)                                                                                      \
-  switch (s.PPL) {                                                                                             \
-    SMC_PPL_CASE(FAM, 2)                                                                                       \
-    SMC_PPL_CASE(FAM, 4)                                                                                       \
-    SMC_PPL_CASE(FAM, 6)                                                                                       \
-    SMC_PPL_CASE(FAM, 8)                                                                                       \
-    SMC_PPL_CASE(FAM, 10)                                                                                      \
-    SMC_PPL_CASE(FAM, 12)                                                                                      \
-    SMC_PPL_CASE(FAM, 14)                                                                                      \
-    SMC_PPL_CASE(FAM, 16)                                                                                      \
-    default: return cudaErrorInvalidValue;                                                                     \
-  }
-  switch (family) {
-    case FAM_GM: SMC_FAM_CASE(FAM_GM)
-    case FAM_XPS: SMC_FAM_CASE(FAM_XPS)
-    case FAM_OFFSET: SMC_FAM_CASE(FAM_OFFSET)
-    default: return cudaErrorInvalidValue;
-  }
-#undef SMC_FAM_CASE
-#undef SMC_PPL_CASE
+  return b + (size_t)s.U * sizeof(Xch);
 }
 
 cudaError_t launch_energy(int family, const Shape& s, int dmax, const GroupDesc* gds, const int* list,
                           const int* prefix, int n_list, int total_ctas, cudaStream_t st) {
-  return launch_chain<true>(family, s, dmax, gds, list, prefix, n_list, total_ctas, st);
+  switch (family) {
+    case FAM_GM: return launch_chain_gm_energy(s, dmax, gds, list, prefix, n_list, total_ctas, st);
+    case FAM_XPS: return launch_chain_xps_energy(s, dmax, gds, list, prefix, n_list, total_ctas, st);
+    case FAM_OFFSET: return launch_chain_offset_energy(s, dmax, gds, list, prefix, n_list, total_ctas, st);
+  }
+  return cudaErrorInvalidValue;
 }
 cudaError_t launch_move(int family, const Shape& s, int dmax, const GroupDesc* gds, const int* list,
                         const int* prefix, int n_list, int total_ctas, cudaStream_t st) {
-  return launch_chain<false>(family, s, dmax, gds, list, prefix, n_list, total_ctas, st);
+  switch (family) {
+    case FAM_GM: return launch_chain_gm_move(s, dmax, gds, list, prefix, n_list, total_ctas, st);
+    case FAM_XPS: return launch_chain_xps_move(s, dmax, gds, list, prefix, n_list, total_ctas, st);
+    case FAM_OFFSET: return launch_chain_offset_move(s, dmax, gds, list, prefix, n_list, total_ctas, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_init_draw(const GroupDesc* gds, const int* list, int n_list, int Tmax, cudaStream_t st) {

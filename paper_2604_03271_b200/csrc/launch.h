@@ -25,6 +25,17 @@ cudaError_t launch_init_draw(const GroupDesc* d_gds, const int* d_list, int n_li
 // full energies of theta[cur] (BlockEvaluator::full, energy.cpp:43-55), one chain unit per particle
 cudaError_t launch_energy(int family, const Shape& s, int dmax, const GroupDesc* d_gds, const int* d_list,
                           const int* d_cta_prefix, int n_list, int total_ctas, cudaStream_t st);
+// per-(family, mode) instantiation units (chain_<fam>_<mode>.cu)
+#define SMC_DECL_CHAIN(NAME)                                                                                    \
+  cudaError_t NAME(const Shape& s, int dmax, const GroupDesc* d_gds, const int* d_list, const int* d_cta_prefix, \
+                   int n_list, int total_ctas, cudaStream_t st);
+SMC_DECL_CHAIN(launch_chain_gm_energy)
+SMC_DECL_CHAIN(launch_chain_gm_move)
+SMC_DECL_CHAIN(launch_chain_xps_energy)
+SMC_DECL_CHAIN(launch_chain_xps_move)
+SMC_DECL_CHAIN(launch_chain_offset_energy)
+SMC_DECL_CHAIN(launch_chain_offset_move)
+#undef SMC_DECL_CHAIN
 // fused waste-free chain move (wastefree_level chain loop x cw_mh_sweep, smc.cpp:142-156, mcmc.cpp:55-96)
 cudaError_t launch_move(int family, const Shape& s, int dmax, const GroupDesc* d_gds, const int* d_list,
                         const int* d_cta_prefix, int n_list, int total_ctas, cudaStream_t st);
