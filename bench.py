@@ -1,0 +1,329 @@
+"""bench.py -- headline benchmark of the B200 SMC sampler (driver contract).
+
+Workload (BASELINE.json configs[1], "C2"): synthetic XRD-like spectrum,
+N = 2000 points, 6 pseudo-Voigt peaks + Shirley background, heteroscedastic
+(GaussApprox-Poisson) noise; full model selection K = 1..10 with the xps
+family (d = 4K+2), T = 65536 particles, n = 8 sweeps per chain, ess 0.5.
+One "step" = one complete model-selection trial (all ten SMC runs to
+beta = 1, log-evidence per K + posterior samples).
+
+Metric: particle-likelihood evals/s, one eval = one MH proposal (the
+SURVEY.md 8d unit, counted as sum over levels of T*d = smc.cpp:182 on both the
+GPU and the CPU side), plus the time to log-evidence for K = 1..Kmax.
+
+  value   device-resident throughput (specmc_session_run: spectra, priors and
+          particles already in HBM), CUDA-event timed per step, L2 flushed
+          between steps (256 MiB write), max over ranks.
+  e2e     the same metric through the C ABI call specmc_smc_run_batch with host
+          buffers: H2D of the spectrum/priors and D2H of every posterior (d x T
+          fp64), energies and diagnostics inside the timed region.
+  roofline  move kernel (k_chain<xps, 16, 4, move>): point-evals/s from CUDA
+          events around every move launch x algorithmic MUFU ops per point
+          (pV + Shirley + hetero = 4) against the measured MUFU
+          ex2 throughput of this GPU (specmc_probe_mufu).
+  cpu_baseline  the reference itself (oracle/_ref, the unchanged reference
+          sources), smc_run with workers = 0 (all host threads) on a bounded
+          sample of the same workload (same spectrum, K = 1..10, T = 256).
+
+Multi-GPU (torchrun): each rank runs its own trial (seed trial_seed(4242, rank),
+weak scaling, no data-path collective); F per K is all-gathered for model
+selection.  --impl reference: rank 0 times the reference CPU path alone.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+MUFU_PER_POINT = {"xps": 4.0, "gm": 1.0, "offset": 0.0}  # SURVEY.md 8d algorithmic counts
+CPU_SAMPLE_T = 256
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--T", type=int, default=None, help="override particle count (debug only)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.f.flush()
+        rows = []
+        for line in Path(self.f.name).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        loaded = [v for v in sm if v > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": smax, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference_sample(workload, seed, T):
+    """Reference smc_run (oracle/_ref, unchanged reference sources) for K = 1..Kmax
+    at T particles, workers = 0.  Returns (evals, seconds, cores, kind)."""
+    from oracle.oracle import OracleModel, Port, Ref, ref_available
+    ks = list(range(workload.k_range[0], workload.k_range[1] + 1))
+    kind = "reference" if ref_available() else "port"
+    lib = Ref() if kind == "reference" else Port()
+    evals, secs = 0, 0.0
+    for K in ks:
+        spec = workload.spec(K)
+        pk, pa, pb = spec.arrays()
+        nz = spec.noise
+        kw = dict(noise="xps_hetero", s0=nz.s0, s1=nz.s1, s2=nz.s2) if workload.family == "xps" else dict(
+            noise="gaussian", sigma=nz.sigma)
+        om = OracleModel(workload.family, K, pk, pa, pb, workload.data.xs, workload.data.ys, **kw)
+        t0 = time.perf_counter()
+        if kind == "reference":
+            r = lib.smc_run(om, T, workload.n, 0.5, 2000, seed, workers=0, keep=False)
+            secs += r.wall_seconds
+        else:
+            r = lib.smc_run(om, T, workload.n, 0.5, 2000, seed, keep=False)
+            secs += time.perf_counter() - t0
+        evals += T * spec.d * r.levels
+    cores = os.cpu_count() if kind == "reference" else 1
+    return evals, secs, cores, kind
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    from paper_2604_03271_b200 import synthetic as syn
+    w = syn.config(args.config)
+    T = CPU_SAMPLE_T
+    seed = syn.trial_seed(4242, 0)
+    for _ in range(args.warmup):
+        cpu_reference_sample(w, seed, T)
+    ev, secs = 0, 0.0
+    for _ in range(args.steps):
+        e, s, cores, kind = cpu_reference_sample(w, seed, T)
+        ev += e
+        secs += s
+    v = ev / secs
+    line = {
+        "metric": f"particle-likelihood evals/s (K=1..{w.k_range[1]} model selection, {args.config})",
+        "value": v, "unit": "evals/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{args.config} bounded sample: N={len(w.data.xs)}, K={w.k_range[0]}..{w.k_range[1]},"
+                               f" T={T}, n={w.n} (reference CPU path)", "N": len(w.data.xs), "T": T, "n": w.n,
+                   "K_range": list(w.k_range)},
+        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": kind,
+                         "sample": f"smc_run K={w.k_range[0]}..{w.k_range[1]} at T={T}, workers=0, per step"},
+        "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+    import paper_2604_03271_b200 as S
+    from paper_2604_03271_b200 import synthetic as syn
+
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = syn.config(args.config, args.T)
+    ks = list(range(w.k_range[0], w.k_range[1] + 1))
+    seed = syn.trial_seed(4242, rank)
+    problems = [(w.spec(K), 0, S.SmcConfig(T=w.T, n=w.n, ess_target=0.5, seed=seed, device=local)) for K in ks]
+    N = len(w.data.xs)
+    peak_mufu = S.probe_mufu(local)
+
+    sess = S.Session(problems, [w.data])
+    for _ in range(args.warmup):
+        sess.run()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    clocks = Clocks(local)
+    S.stats_reset()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    elapsed = 0.0
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # L2 flush between timed steps (outside the timed window)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        sess.run()
+        b.record()
+        torch.cuda.synchronize()
+        elapsed += a.elapsed_time(b) * 1e-3
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    st = S.stats()
+    reps = sess.fetch(raise_on_error=False)
+    sess.close()
+    ok = [r for r in reps if not isinstance(r, Exception)]
+    evals_step = sum(r.proposals for r in ok)
+    trials_step = sum(r.trials for r in ok)
+
+    # ---- e2e: the C ABI call with host buffers (H2D spectrum/priors, D2H posteriors)
+    e2e = None
+    if not args.no_e2e:
+        S.smc_run_batch(problems, [w.data])  # warm-up of the allocation path
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_evals = 0
+        for _ in range(args.steps):
+            rr = S.smc_run_batch(problems, [w.data], raise_on_error=False)
+            e2e_evals += sum(r.proposals for r in rr if not isinstance(r, Exception))
+        torch.cuda.synchronize()
+        e2e_t = time.perf_counter() - t0
+        h2d = 2 * N * 8 + sum(p[0].d * (4 + 8 + 8) for p in problems)
+        d2h = sum(p[0].d * w.T * 8 + w.T * 8 for p in problems) + sum(
+            int(r.scalars["levels"]) * 4 * 8 for r in rr if not isinstance(r, Exception))
+        e2e = {"value": e2e_evals, "t": e2e_t, "h2d": h2d, "d2h": d2h}
+
+    # ---- model selection over all trials (ranks); max-over-ranks timing
+    Fs = [r.F if not isinstance(r, Exception) else float("nan") for r in reps]
+    if dist:
+        t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+        tot = torch.tensor([evals_step * args.steps], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tot)
+        total_evals = float(tot.item())
+        gathered = [None] * ws
+        dist.all_gather_object(gathered, Fs)
+        if e2e:
+            te = torch.tensor([e2e["t"]], device="cuda", dtype=torch.float64)
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            ee = torch.tensor([float(e2e["value"])], device="cuda", dtype=torch.float64)
+            dist.all_reduce(ee)
+            e2e["t"], e2e["value"] = float(te.item()), float(ee.item())
+    else:
+        total_evals = evals_step * args.steps
+        gathered = [Fs]
+    rows = []
+    for Ftr in gathered:
+        for K, F in zip(ks, Ftr):
+            rows.append((K, S.RunReport(F=F)))
+    try:
+        k_sel = S.model_select(rows).K_best
+    except RuntimeError:
+        k_sel = None
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    value = total_evals / elapsed
+    move_s = st["move_kernel_ms"] * 1e-3
+    pe_rate = st["point_evals"] / move_s if move_s > 0 else 0.0
+    mufu_pt = MUFU_PER_POINT[w.family]
+    achieved = pe_rate * mufu_pt
+    traffic = None
+    prof = ROOT / "profiles" / "move_kernel_ncu.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": f"particle-likelihood evals/s (K=1..{ks[-1]} model selection, {args.config})",
+        "value": value, "unit": "evals/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": elapsed / args.steps * 1e3, "time_to_evidence_s": elapsed / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 point terms / f64 accumulation", "data": "synthetic",
+        "config": {"workload": f"{args.config}: synthetic XRD-like spectrum N={N}, 6 pseudo-Voigt peaks + Shirley,"
+                               f" xps family K={ks[0]}..{ks[-1]}, T={w.T}, n={w.n}, ess 0.5; 1 trial per GPU",
+                   "N": N, "K_range": [ks[0], ks[-1]], "T": w.T, "n": w.n, "trials_per_gpu": 1,
+                   "l2": "flushed between steps (256 MiB write)", "parallelism": f"trials x{ws} (weak)"},
+        "K_selected": k_sel, "trials_per_step": trials_step, "point_evals_per_s_move": pe_rate,
+        "gpu_launches": st["kernel_launches"],
+        "roofline": {"bound": "sfu", "achieved": achieved / 1e9, "peak": peak_mufu / 1e9,
+                     "unit": "Gop/s (MUFU)", "frac": achieved / peak_mufu if peak_mufu else None,
+                     "traffic": traffic,
+                     "note": f"move kernel; {mufu_pt:g} algorithmic MUFU ops per point-eval (SURVEY 8d) x "
+                             "point-evals/s from CUDA events on the launch stream; peak = measured ex2 "
+                             "throughput of this GPU (specmc_probe_mufu)"},
+        "clocks": clk,
+    }
+    if e2e:
+        line["e2e"] = {"value": e2e["value"] / e2e["t"], "unit": "evals/s", "h2d_bytes_per_step": e2e["h2d"],
+                       "d2h_bytes_per_step": e2e["d2h"]}
+    if ws == 1 and not args.no_cpu_baseline:
+        ev, secs, cores, kind = cpu_reference_sample(w, seed, CPU_SAMPLE_T)
+        line["cpu_baseline"] = {"value": ev / secs, "unit": "evals/s", "cores": cores, "kind": kind,
+                                "sample": f"smc_run K={ks[0]}..{ks[-1]} on the same spectrum at T={CPU_SAMPLE_T} "
+                                          f"(n={w.n}, workers=0), {secs:.1f} s"}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_init()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -127,6 +127,18 @@ int specmc_smc_run_batch(int32_t n_problems, const specmc_problem* problems, int
 
 void specmc_result_free(specmc_smc_result* r);
 
+/* ---- device-resident sessions -----------------------------------------
+ * specmc_smc_run_batch == create + run + fetch + destroy.  A session keeps the
+ * spectra, priors and particle buffers resident in HBM; run() re-runs every
+ * problem from init_ensemble (same seeds => same results) without any
+ * host<->device traffic besides 48 bytes of state per run and level. */
+typedef struct specmc_session specmc_session;
+int specmc_session_create(int32_t n_problems, const specmc_problem* problems, int32_t n_spectra,
+                          const specmc_spectrum* spectra, specmc_session** out, char* err, size_t errlen);
+int specmc_session_run(specmc_session* s, double* device_seconds, char* err, size_t errlen);
+int specmc_session_fetch(specmc_session* s, specmc_smc_result* out, char* err, size_t errlen);
+void specmc_session_destroy(specmc_session* s);
+
 /* ---- parity units (each runs the same device code as the sampler) ------ */
 
 /* Batched full energies E(theta) for fixed parameters: the K2 kernel.
@@ -182,6 +194,10 @@ void specmc_stats_reset(void);
  * warps per chain, points per lane, chains per CTA. */
 int specmc_launch_shape(int64_t n_points, int32_t* warps_per_chain, int32_t* points_per_lane,
                         int32_t* chains_per_cta);
+
+/* Measured MUFU (ex2) throughput of the device in operations per second:
+ * the SFU roofline denominator of the move kernel (bench.py). */
+int specmc_probe_mufu(int32_t device, double* ops_per_second, char* err, size_t errlen);
 
 int specmc_device_count(void);
 const char* specmc_version(void);

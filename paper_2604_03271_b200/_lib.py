@@ -57,7 +57,8 @@ EXPORTS = [
     "specmc_smc_run", "specmc_smc_run_batch", "specmc_result_free", "specmc_energy_batch", "specmc_ess",
     "specmc_log_mean_exp", "specmc_next_beta", "specmc_systematic_resample", "specmc_predict_step_size",
     "specmc_validate_config", "specmc_validate_problem", "specmc_stats_get", "specmc_stats_reset",
-    "specmc_launch_shape", "specmc_device_count", "specmc_version",
+    "specmc_launch_shape", "specmc_device_count", "specmc_version", "specmc_session_create", "specmc_session_run",
+    "specmc_session_fetch", "specmc_session_destroy", "specmc_probe_mufu",
 ]
 
 
@@ -73,6 +74,13 @@ def _load():
                                    C.POINTER(SmcResultC), E, Z]
     lib.specmc_smc_run_batch.argtypes = [C.c_int32, C.POINTER(ProblemC), C.c_int32, C.POINTER(SpectrumC),
                                          C.POINTER(SmcResultC), E, Z]
+    lib.specmc_session_create.argtypes = [C.c_int32, C.POINTER(ProblemC), C.c_int32, C.POINTER(SpectrumC),
+                                          C.POINTER(C.c_void_p), E, Z]
+    lib.specmc_session_run.argtypes = [C.c_void_p, _dp, E, Z]
+    lib.specmc_session_fetch.argtypes = [C.c_void_p, C.POINTER(SmcResultC), E, Z]
+    lib.specmc_session_destroy.argtypes = [C.c_void_p]
+    lib.specmc_session_destroy.restype = None
+    lib.specmc_probe_mufu.argtypes = [C.c_int32, _dp, E, Z]
     lib.specmc_result_free.argtypes = [C.POINTER(SmcResultC)]
     lib.specmc_result_free.restype = None
     lib.specmc_energy_batch.argtypes = [C.POINTER(ModelDesc), _dp, _dp, C.c_int64, _dp, C.c_int64, C.c_int32, _dp,

@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <numeric>
 #include <stdexcept>
@@ -332,144 +333,154 @@ struct Timer {
   }
 };
 
-// Runs one homogeneous class of problems (same family, same launch shape,
-// same device) to completion and fills the results.
-void run_class(Device& dev, const std::vector<RunSpec>& runs, const std::vector<specmc_spectrum>& spectra,
-               const std::vector<int>& idx, specmc_smc_result* out, double& device_seconds) {
-  const int G = (int)idx.size();
-  const specmc_model_desc& m0 = runs[idx[0]].m;
-  int64_t Nmax = 0;
-  int dmax = 1, Tmax = 0;
-  for (int r : idx) {
-    Nmax = std::max(Nmax, runs[r].N);
-    dmax = std::max(dmax, runs[r].m.d);
-    Tmax = std::max<int>(Tmax, (int)runs[r].cfg.T);
-  }
-  const Shape shape = pick_shape(Nmax);
-  if ((int64_t)32 * shape.W * shape.PPL < Nmax)
-    throw Error(SPECMC_EINVAL, "spectrum has more points than the device path supports (8192)");
-  const size_t smem = chain_smem_bytes(shape, dmax);
-  if (smem > 227 * 1024) throw Error(SPECMC_EINVAL, "model too large for the device path (shared memory)");
-
-  // spectra prepared once per (spectrum, shift) for this shape
-  std::map<std::pair<int, double>, PreparedSpectrum> prep;
-  for (int r : idx) {
-    const auto key = std::make_pair(runs[r].spectrum, runs[r].x_shift);
-    if (!prep.count(key)) {
-      const auto& sp = spectra[runs[r].spectrum];
-      prep.emplace(key, prepare_spectrum(runs[r].m, sp.xs, sp.ys, sp.n, shape, runs[r].x_shift));
-    }
-  }
-
-  // ---- sizes
-  const int L = 32 * shape.W;
-  const size_t npt = (size_t)shape.PPL * L;
-  size_t bytes = Arena::al(sizeof(GroupDesc) * G) + Arena::al(sizeof(GroupState) * G) + 4 * Arena::al(4 * (G + 1));
-  bytes += prep.size() * (Arena::al(npt * 4) + Arena::al(npt * 8) + Arena::al(npt * 16));
-  for (int r : idx) {
-    const auto& R = runs[r];
-    const size_t T = R.cfg.T, d = R.m.d, S = T / R.cfg.n;
-    bytes += 3 * Arena::al(d * 8) + Arena::al(d * 4);                       // priors + ls0
-    bytes += 2 * Arena::al(d * T * 8) + 2 * Arena::al(T * 8);               // theta, E
-    bytes += Arena::al(S * 4) + Arena::al(d * S * 4) + Arena::al(d * S * 8);  // anc, chain stats
-    bytes += Arena::al(T * 8) + Arena::al(kHist * (1 + 2 * d) * 8);         // wbuf, hist
-    bytes += Arena::al((size_t)R.cfg.max_levels * 4 * 8);                  // diag
-  }
+// One homogeneous class of problems (same family, same launch shape, same
+// device): device buffers, descriptors and the lock-step level loop.
+struct ClassRun {
+  std::vector<int> idx;  // indices into the session's runs
+  Shape shape{};
+  int dmax = 1, Tmax = 0, family = 0, G = 0;
   Arena ar;
-  ar.reserve(bytes);
-  GroupDesc* d_gds = ar.take<GroupDesc>(G);
-  GroupState* d_st = ar.take<GroupState>(G);
-  int* d_list = ar.take<int>(G + 1);
-  int* d_prefix = ar.take<int>(G + 1);
-  int* d_list_all = ar.take<int>(G + 1);
-  int* d_prefix_all = ar.take<int>(G + 1);
-  cudaStream_t st = dev.stream;
+  GroupDesc* d_gds = nullptr;
+  GroupState* d_st = nullptr;
+  int *d_list = nullptr, *d_prefix = nullptr, *d_list_all = nullptr, *d_prefix_all = nullptr;
+  std::vector<GroupDesc> gds;
+  std::vector<int> order;
+  GroupState* h_st = nullptr;
+  int* h_list = nullptr;
+  double device_seconds = 0.0;
 
-  std::map<std::pair<int, double>, const PreparedSpectrum*> pmap;
-  std::map<std::pair<int, double>, std::tuple<float*, float2*, float4*>> dspec;
-  for (auto& kv : prep) {
-    float* x = ar.take<float>(npt);
-    float2* c = ar.take<float2>(npt);
-    float4* y = ar.take<float4>(npt);
-    h2d(x, kv.second.x.data(), npt, st);
-    h2d(reinterpret_cast<float*>(c), kv.second.c.data(), 2 * npt, st);
-    h2d(reinterpret_cast<float*>(y), kv.second.y.data(), 4 * npt, st);
-    dspec[kv.first] = std::make_tuple(x, c, y);
+  ClassRun() = default;
+  ClassRun(const ClassRun&) = delete;
+  ~ClassRun() {
+    if (h_st) cudaFreeHost(h_st);
+    if (h_list) cudaFreeHost(h_list);
   }
 
-  std::vector<GroupDesc> gds(G);
-  std::vector<GroupState> sts(G);
-  for (int gi = 0; gi < G; ++gi) {
-    const RunSpec& R = runs[idx[gi]];
-    const auto key = std::make_pair(R.spectrum, R.x_shift);
-    const PreparedSpectrum& ps = prep.at(key);
-    GroupDesc& g = gds[gi];
-    std::memset(&g, 0, sizeof(g));
-    g.family = R.m.family;
-    g.K = R.m.K;
-    g.d = R.m.d;
-    g.noise = ps.nz;
-    g.T = (int)R.cfg.T;
-    g.n = R.cfg.n;
-    g.S = (int)(R.cfg.T / R.cfg.n);
-    g.max_levels = R.cfg.max_levels;
-    g.ess_target = R.cfg.ess_target;
-    g.n_data = (double)R.N;
-    const uint64_t k = mix64(R.cfg.seed);
-    g.key0 = (uint32_t)k;
-    g.key1 = (uint32_t)(k >> 32);
-    g.chain_base = 0;
-    g.N = (int)R.N;
-    g.e_a0 = ps.e_a0;
-    g.e_a1 = ps.e_a1;
-    g.nz_a0 = ps.a0;
-    g.nz_a1 = ps.a1;
-    g.nz_a2 = ps.a2;
-    g.nz_q = ps.q;
-    g.x0s = ps.x0s;
-    g.inv_range = ps.inv_range;
-    g.range = ps.range;
-    g.x_shift_f = (float)R.x_shift;
-    auto t = dspec.at(key);
-    g.spec_x = std::get<0>(t);
-    g.spec_c = std::get<1>(t);
-    g.spec_y = std::get<2>(t);
-    const size_t T = R.cfg.T, d = R.m.d, S = g.S;
-    int* pk = ar.take<int>(d);
-    double* pa = ar.take<double>(d);
-    double* pb = ar.take<double>(d);
-    h2d(pk, R.pk.data(), d, st);
-    h2d(pa, R.pa.data(), d, st);
-    h2d(pb, R.pb.data(), d, st);
-    g.pkind = pk;
-    g.pa = pa;
-    g.pb = pb;
-    g.theta[0] = ar.take<double>(d * T);
-    g.theta[1] = ar.take<double>(d * T);
-    g.E[0] = ar.take<double>(T);
-    g.E[1] = ar.take<double>(T);
-    g.anc = ar.take<int>(S);
-    g.ls0 = ar.take<double>(d);
-    g.chain_acc = ar.take<int>(d * S);
-    g.chain_ls = ar.take<double>(d * S);
-    g.wbuf = ar.take<double>(T);
-    g.hist = ar.take<double>(kHist * (1 + 2 * d));
-    g.diag = ar.take<double>((size_t)R.cfg.max_levels * 4);
-    g.st = d_st + gi;
-    GroupState& s = sts[gi];
-    std::memset(&s, 0, sizeof(s));
-    s.active = 1;
+  // allocation + H2D of spectra, priors and descriptors
+  void prepare(Device& dev, const std::vector<RunSpec>& runs, const std::vector<specmc_spectrum>& spectra) {
+    G = (int)idx.size();
+    family = runs[idx[0]].m.family;
+    int64_t Nmax = 0;
+    for (int r : idx) {
+      Nmax = std::max(Nmax, runs[r].N);
+      dmax = std::max(dmax, runs[r].m.d);
+      Tmax = std::max<int>(Tmax, (int)runs[r].cfg.T);
+    }
+    shape = pick_shape(Nmax);
+    if ((int64_t)32 * shape.W * shape.PPL < Nmax)
+      throw Error(SPECMC_EINVAL, "spectrum has more points than the device path supports (8192)");
+    if (chain_smem_bytes(shape, dmax) > 227 * 1024)
+      throw Error(SPECMC_EINVAL, "model too large for the device path (shared memory)");
+
+    std::map<std::pair<int, double>, PreparedSpectrum> prep;
+    for (int r : idx) {
+      const auto key = std::make_pair(runs[r].spectrum, runs[r].x_shift);
+      if (!prep.count(key)) {
+        const auto& sp = spectra[runs[r].spectrum];
+        prep.emplace(key, prepare_spectrum(runs[r].m, sp.xs, sp.ys, sp.n, shape, runs[r].x_shift));
+      }
+    }
+    const size_t npt = (size_t)shape.PPL * 32 * shape.W;
+    size_t bytes = Arena::al(sizeof(GroupDesc) * G) + Arena::al(sizeof(GroupState) * G) + 4 * Arena::al(4 * (G + 1));
+    bytes += prep.size() * (Arena::al(npt * 4) + Arena::al(npt * 8) + Arena::al(npt * 16));
+    for (int r : idx) {
+      const auto& R = runs[r];
+      const size_t T = R.cfg.T, d = R.m.d, S = T / R.cfg.n;
+      bytes += 3 * Arena::al(d * 8) + Arena::al(d * 4);
+      bytes += 2 * Arena::al(d * T * 8) + 2 * Arena::al(T * 8);
+      bytes += Arena::al(S * 4) + Arena::al(d * S * 4) + Arena::al(d * S * 8);
+      bytes += Arena::al(T * 8) + Arena::al(kHist * (1 + 2 * d) * 8);
+      bytes += Arena::al((size_t)R.cfg.max_levels * 4 * 8);
+    }
+    ar.reserve(bytes);
+    d_gds = ar.take<GroupDesc>(G);
+    d_st = ar.take<GroupState>(G);
+    d_list = ar.take<int>(G + 1);
+    d_prefix = ar.take<int>(G + 1);
+    d_list_all = ar.take<int>(G + 1);
+    d_prefix_all = ar.take<int>(G + 1);
+    cudaStream_t st = dev.stream;
+
+    std::map<std::pair<int, double>, std::tuple<float*, float2*, float4*>> dspec;
+    for (auto& kv : prep) {
+      float* x = ar.take<float>(npt);
+      float2* c = ar.take<float2>(npt);
+      float4* y = ar.take<float4>(npt);
+      h2d(x, kv.second.x.data(), npt, st);
+      h2d(reinterpret_cast<float*>(c), kv.second.c.data(), 2 * npt, st);
+      h2d(reinterpret_cast<float*>(y), kv.second.y.data(), 4 * npt, st);
+      dspec[kv.first] = std::make_tuple(x, c, y);
+    }
+    gds.resize(G);
+    for (int gi = 0; gi < G; ++gi) {
+      const RunSpec& R = runs[idx[gi]];
+      const auto key = std::make_pair(R.spectrum, R.x_shift);
+      const PreparedSpectrum& ps = prep.at(key);
+      GroupDesc& g = gds[gi];
+      std::memset(&g, 0, sizeof(g));
+      g.family = R.m.family;
+      g.K = R.m.K;
+      g.d = R.m.d;
+      g.noise = ps.nz;
+      g.T = (int)R.cfg.T;
+      g.n = R.cfg.n;
+      g.S = (int)(R.cfg.T / R.cfg.n);
+      g.max_levels = R.cfg.max_levels;
+      g.ess_target = R.cfg.ess_target;
+      g.n_data = (double)R.N;
+      const uint64_t k = mix64(R.cfg.seed);
+      g.key0 = (uint32_t)k;
+      g.key1 = (uint32_t)(k >> 32);
+      g.chain_base = 0;
+      g.N = (int)R.N;
+      g.e_a0 = ps.e_a0;
+      g.e_a1 = ps.e_a1;
+      g.nz_a0 = ps.a0;
+      g.nz_a1 = ps.a1;
+      g.nz_a2 = ps.a2;
+      g.nz_q = ps.q;
+      g.x0s = ps.x0s;
+      g.inv_range = ps.inv_range;
+      g.range = ps.range;
+      g.x_shift_f = (float)R.x_shift;
+      auto t = dspec.at(key);
+      g.spec_x = std::get<0>(t);
+      g.spec_c = std::get<1>(t);
+      g.spec_y = std::get<2>(t);
+      const size_t T = R.cfg.T, d = R.m.d, S = g.S;
+      int* pk = ar.take<int>(d);
+      double* pa = ar.take<double>(d);
+      double* pb = ar.take<double>(d);
+      h2d(pk, R.pk.data(), d, st);
+      h2d(pa, R.pa.data(), d, st);
+      h2d(pb, R.pb.data(), d, st);
+      g.pkind = pk;
+      g.pa = pa;
+      g.pb = pb;
+      g.theta[0] = ar.take<double>(d * T);
+      g.theta[1] = ar.take<double>(d * T);
+      g.E[0] = ar.take<double>(T);
+      g.E[1] = ar.take<double>(T);
+      g.anc = ar.take<int>(S);
+      g.ls0 = ar.take<double>(d);
+      g.chain_acc = ar.take<int>(d * S);
+      g.chain_ls = ar.take<double>(d * S);
+      g.wbuf = ar.take<double>(T);
+      g.hist = ar.take<double>(kHist * (1 + 2 * d));
+      g.diag = ar.take<double>((size_t)R.cfg.max_levels * 4);
+      g.st = d_st + gi;
+    }
+    h2d(d_gds, gds.data(), G, st);
+    // longest chains first (d descending) so the move grid drains in LPT order
+    order.resize(G);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return gds[a].d > gds[b].d; });
+    cuda_check(cudaMallocHost(&h_st, sizeof(GroupState) * G), "cudaMallocHost");
+    cuda_check(cudaMallocHost(&h_list, sizeof(int) * 2 * (G + 1)), "cudaMallocHost");
+    dev.sync();
   }
-  h2d(d_gds, gds.data(), G, st);
-  h2d(d_st, sts.data(), G, st);
 
-  // longest chains first (d descending) so the move grid drains in LPT order
-  std::vector<int> order(G);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return gds[a].d > gds[b].d; });
-
-  auto build_list = [&](const std::vector<int>& groups, bool energy, std::vector<int>& list,
-                        std::vector<int>& prefix) -> int {
+  int build_list(const std::vector<int>& groups, bool energy, std::vector<int>& list, std::vector<int>& prefix) {
     list.clear();
     prefix.clear();
     int total = 0;
@@ -481,64 +492,57 @@ void run_class(Device& dev, const std::vector<RunSpec>& runs, const std::vector<
     }
     prefix.push_back(total);
     return total;
-  };
-
-  Timer whole;
-  cuda_check(cudaEventRecord(whole.a, st), "event");
-
-  // ---- init_ensemble: prior draws + full energies
-  std::vector<int> list, prefix;
-  int total = build_list(order, true, list, prefix);
-  h2d(d_list_all, list.data(), list.size(), st);
-  h2d(d_prefix_all, prefix.data(), prefix.size(), st);
-  cuda_check(launch_init_draw(d_gds, d_list_all, G, Tmax, st), "k_init_draw");
-  cuda_check(launch_energy(m0.family, shape, dmax, d_gds, d_list_all, d_prefix_all, G, total, st), "k_chain<energy>");
-  count_launch(2);
-
-  // pinned staging for the per-round state read-back
-  GroupState* h_st = nullptr;
-  int* h_list = nullptr;
-  cuda_check(cudaMallocHost(&h_st, sizeof(GroupState) * G), "cudaMallocHost");
-  cuda_check(cudaMallocHost(&h_list, sizeof(int) * 2 * (G + 1)), "cudaMallocHost");
-  struct PinnedFree {
-    void* a;
-    void* b;
-    ~PinnedFree() {
-      cudaFreeHost(a);
-      cudaFreeHost(b);
-    }
-  } pf{h_st, h_list};
-
-  std::vector<int> active = order;
-  Timer mv;
-  double move_ms = 0.0;
-  int64_t move_launches = 0;
-  while (!active.empty()) {
-    total = build_list(active, false, list, prefix);
-    const int na = (int)list.size();
-    std::memcpy(h_list, list.data(), sizeof(int) * na);
-    std::memcpy(h_list + (G + 1), prefix.data(), sizeof(int) * (na + 1));
-    h2d(d_list, h_list, na, st);
-    h2d(d_prefix, h_list + (G + 1), na + 1, st);
-    cuda_check(launch_temper(d_gds, d_list, na, st), "k_temper");
-    cuda_check(cudaEventRecord(mv.a, st), "event");
-    cuda_check(launch_move(m0.family, shape, dmax, d_gds, d_list, d_prefix, na, total, st), "k_chain<move>");
-    cuda_check(cudaEventRecord(mv.b, st), "event");
-    cuda_check(launch_stats(d_gds, d_list, na, st), "k_stats");
-    count_launch(3);
-    d2h(h_st, d_st, G, st);
-    dev.sync();
-    move_ms += mv.ms();
-    ++move_launches;
-    std::vector<int> next;
-    for (int gi : active)
-      if (h_st[gi].active) next.push_back(gi);
-    active.swap(next);
   }
-  cuda_check(cudaEventRecord(whole.b, st), "event");
-  dev.sync();
-  device_seconds = whole.ms() * 1e-3;
-  {
+
+  // init_ensemble + the level loop of smc_run (smc.cpp:186-211), all groups in lock-step
+  void run(Device& dev) {
+    cudaStream_t st = dev.stream;
+    std::vector<GroupState> sts(G);
+    for (auto& s : sts) {
+      std::memset(&s, 0, sizeof(s));
+      s.active = 1;
+    }
+    Timer whole, mv;
+    cuda_check(cudaEventRecord(whole.a, st), "event");
+    h2d(d_st, sts.data(), G, st);
+    std::vector<int> list, prefix;
+    int total = build_list(order, true, list, prefix);
+    std::memcpy(h_list, list.data(), sizeof(int) * G);
+    std::memcpy(h_list + (G + 1), prefix.data(), sizeof(int) * (G + 1));
+    h2d(d_list_all, h_list, G, st);
+    h2d(d_prefix_all, h_list + (G + 1), G + 1, st);
+    cuda_check(launch_init_draw(d_gds, d_list_all, G, Tmax, st), "k_init_draw");
+    cuda_check(launch_energy(family, shape, dmax, d_gds, d_list_all, d_prefix_all, G, total, st), "k_chain<energy>");
+    count_launch(2);
+    std::vector<int> active = order;
+    double move_ms = 0.0;
+    int64_t move_launches = 0;
+    while (!active.empty()) {
+      total = build_list(active, false, list, prefix);
+      const int na = (int)list.size();
+      dev.sync();  // h_list is reused: the previous round's copies must be done
+      std::memcpy(h_list, list.data(), sizeof(int) * na);
+      std::memcpy(h_list + (G + 1), prefix.data(), sizeof(int) * (na + 1));
+      h2d(d_list, h_list, na, st);
+      h2d(d_prefix, h_list + (G + 1), na + 1, st);
+      cuda_check(launch_temper(d_gds, d_list, na, st), "k_temper");
+      cuda_check(cudaEventRecord(mv.a, st), "event");
+      cuda_check(launch_move(family, shape, dmax, d_gds, d_list, d_prefix, na, total, st), "k_chain<move>");
+      cuda_check(cudaEventRecord(mv.b, st), "event");
+      cuda_check(launch_stats(d_gds, d_list, na, st), "k_stats");
+      count_launch(3);
+      d2h(h_st, d_st, G, st);
+      dev.sync();
+      move_ms += mv.ms();
+      ++move_launches;
+      std::vector<int> next;
+      for (int gi : active)
+        if (h_st[gi].active) next.push_back(gi);
+      active.swap(next);
+    }
+    cuda_check(cudaEventRecord(whole.b, st), "event");
+    dev.sync();
+    device_seconds = whole.ms() * 1e-3;
     std::lock_guard<std::mutex> lk(g_stats_mu);
     g_stats.move_kernel_ms += move_ms;
     g_stats.move_launches += move_launches;
@@ -547,56 +551,56 @@ void run_class(Device& dev, const std::vector<RunSpec>& runs, const std::vector<
     g_stats.point_evals += pe;
   }
 
-  // ---- results
-  for (int gi = 0; gi < G; ++gi) {
-    const RunSpec& R = runs[idx[gi]];
-    specmc_smc_result& o = out[idx[gi]];
-    const GroupState& s = h_st[gi];
-    const size_t T = R.cfg.T, d = R.m.d;
-    o.d = (int)d;
-    o.T = (int64_t)T;
-    o.levels = s.level;
-    o.trials = (int64_t)s.trials;
-    o.proposals = (int64_t)T * (int64_t)d * s.level;
-    if (s.error == GE_MAX_LEVELS) {
-      o.status = SPECMC_ERUNTIME;
-      continue;
-    }
-    if (s.error == GE_ZERO_WEIGHT) {
-      o.status = SPECMC_ERUNTIME;
-      continue;
-    }
-    o.status = SPECMC_OK;
-    o.F = s.neg_log_z;
-    o.diverged = !std::isfinite(o.F);
-    const int Lv = s.level;
-    std::vector<double> diag((size_t)Lv * 4);
-    d2h(diag.data(), gds[gi].diag, diag.size(), st);
-    std::vector<double> th(d * T);
-    d2h(th.data(), gds[gi].theta[s.cur], th.size(), st);
-    o.energies = static_cast<double*>(std::malloc(sizeof(double) * T));
-    d2h(o.energies, gds[gi].E[s.cur], T, st);
-    dev.sync();
-    o.ladder = static_cast<double*>(std::malloc(sizeof(double) * (Lv + 1)));
-    o.level_ess_ratio = static_cast<double*>(std::malloc(sizeof(double) * std::max(Lv, 1)));
-    o.level_log_mean_w = static_cast<double*>(std::malloc(sizeof(double) * std::max(Lv, 1)));
-    o.level_acc_rate = static_cast<double*>(std::malloc(sizeof(double) * std::max(Lv, 1)));
-    o.ladder[0] = 0.0;
-    for (int l = 0; l < Lv; ++l) {
-      o.ladder[l + 1] = diag[4 * l];
-      o.level_ess_ratio[l] = diag[4 * l + 1];
-      o.level_log_mean_w[l] = diag[4 * l + 2];
-      o.level_acc_rate[l] = diag[4 * l + 3];
-    }
-    o.posterior = static_cast<double*>(std::malloc(sizeof(double) * d * T));
-    for (size_t c = 0; c < T; ++c)
-      for (size_t i = 0; i < d; ++i) {
-        double v = th[i * T + c];
-        if (is_location(R.m.family, R.m.K, (int)i) && R.x_shift != 0.0) v += R.x_shift;
-        o.posterior[c * d + i] = v;
+  // D2H of diagnostics, posterior and energies (report fields of smc.cpp:221-247)
+  void fetch(Device& dev, const std::vector<RunSpec>& runs, specmc_smc_result* out) {
+    cudaStream_t st = dev.stream;
+    for (int gi = 0; gi < G; ++gi) {
+      const RunSpec& R = runs[idx[gi]];
+      specmc_smc_result& o = out[idx[gi]];
+      const GroupState& s = h_st[gi];
+      const size_t T = R.cfg.T, d = R.m.d;
+      o.d = (int)d;
+      o.T = (int64_t)T;
+      o.levels = s.level;
+      o.trials = (int64_t)s.trials;
+      o.proposals = (int64_t)T * (int64_t)d * s.level;
+      o.device_seconds = device_seconds;
+      if (s.error != GE_NONE) {
+        o.status = SPECMC_ERUNTIME;
+        continue;
       }
+      o.status = SPECMC_OK;
+      o.F = s.neg_log_z;
+      o.diverged = !std::isfinite(o.F);
+      const int Lv = s.level;
+      std::vector<double> diag((size_t)Lv * 4);
+      d2h(diag.data(), gds[gi].diag, diag.size(), st);
+      std::vector<double> th(d * T);
+      d2h(th.data(), gds[gi].theta[s.cur], th.size(), st);
+      o.energies = static_cast<double*>(std::malloc(sizeof(double) * T));
+      d2h(o.energies, gds[gi].E[s.cur], T, st);
+      dev.sync();
+      o.ladder = static_cast<double*>(std::malloc(sizeof(double) * (Lv + 1)));
+      o.level_ess_ratio = static_cast<double*>(std::malloc(sizeof(double) * std::max(Lv, 1)));
+      o.level_log_mean_w = static_cast<double*>(std::malloc(sizeof(double) * std::max(Lv, 1)));
+      o.level_acc_rate = static_cast<double*>(std::malloc(sizeof(double) * std::max(Lv, 1)));
+      o.ladder[0] = 0.0;
+      for (int l = 0; l < Lv; ++l) {
+        o.ladder[l + 1] = diag[4 * l];
+        o.level_ess_ratio[l] = diag[4 * l + 1];
+        o.level_log_mean_w[l] = diag[4 * l + 2];
+        o.level_acc_rate[l] = diag[4 * l + 3];
+      }
+      o.posterior = static_cast<double*>(std::malloc(sizeof(double) * d * T));
+      for (size_t c = 0; c < T; ++c)
+        for (size_t i = 0; i < d; ++i) {
+          double v = th[i * T + c];
+          if (is_location(R.m.family, R.m.K, (int)i) && R.x_shift != 0.0) v += R.x_shift;
+          o.posterior[c * d + i] = v;
+        }
+    }
   }
-}
+};
 
 void copy_err(char* err, size_t errlen, const std::string& m) {
   if (err && errlen) {
@@ -633,45 +637,75 @@ RunSpec make_runspec(const specmc_model_desc& m, int spectrum, const specmc_smc_
   return R;
 }
 
+// A batch of SMC runs resident on one device: create (validate, allocate,
+// upload) -> run (device only) -> fetch (D2H).  specmc_smc_run_batch is
+// create + run + fetch.
+struct Session {
+  std::vector<specmc_spectrum> spectra;
+  std::vector<RunSpec> runs;
+  std::unique_ptr<Device> dev;
+  std::vector<std::unique_ptr<ClassRun>> classes;
+  double device_seconds = 0.0;
+
+  Session(int n_problems, const specmc_problem* problems, int n_spectra, const specmc_spectrum* sps) {
+    if (n_problems < 1 || !problems) throw Error(SPECMC_EINVAL, "batch: no problems");
+    if (n_spectra < 1 || !sps) throw Error(SPECMC_EINVAL, "batch: no spectra");
+    spectra.assign(sps, sps + n_spectra);
+    for (int i = 0; i < n_problems; ++i) {
+      const auto& p = problems[i];
+      if (p.spectrum < 0 || p.spectrum >= n_spectra) throw Error(SPECMC_EINVAL, "batch: spectrum index out of range");
+      runs.push_back(make_runspec(p.model, p.spectrum, p.cfg, spectra[p.spectrum]));
+    }
+    const int device = runs[0].cfg.device;
+    for (auto& r : runs)
+      if (r.cfg.device != device) throw Error(SPECMC_EINVAL, "batch: all problems must target the same device");
+    dev = std::make_unique<Device>(device);
+    std::map<std::pair<int, int>, std::vector<int>> cls;
+    for (int i = 0; i < n_problems; ++i) {
+      const Shape s = pick_shape(runs[i].N);
+      cls[{runs[i].m.family, s.W * 100 + s.PPL}].push_back(i);
+    }
+    for (auto& kv : cls) {
+      classes.push_back(std::make_unique<ClassRun>());
+      classes.back()->idx = kv.second;
+      classes.back()->prepare(*dev, runs, spectra);
+    }
+    spectra.clear();  // host inputs are borrowed only for the call
+  }
+
+  void run() {
+    cuda_check(cudaSetDevice(dev->ordinal), "cudaSetDevice");
+    device_seconds = 0.0;
+    for (auto& c : classes) {
+      c->run(*dev);
+      device_seconds += c->device_seconds;
+    }
+  }
+
+  int fetch(specmc_smc_result* out) {
+    cuda_check(cudaSetDevice(dev->ordinal), "cudaSetDevice");
+    for (size_t i = 0; i < runs.size(); ++i) std::memset(&out[i], 0, sizeof(specmc_smc_result));
+    for (auto& c : classes) c->fetch(*dev, runs, out);
+    int first = SPECMC_OK;
+    for (size_t i = 0; i < runs.size(); ++i) {
+      out[i].device_seconds = device_seconds;
+      if (out[i].status != SPECMC_OK && first == SPECMC_OK) first = out[i].status;
+    }
+    return first;
+  }
+};
+
 int run_batch(int n_problems, const specmc_problem* problems, int n_spectra, const specmc_spectrum* spectra,
               specmc_smc_result* out, char* err, size_t errlen) {
   const auto t0 = std::chrono::steady_clock::now();
-  if (n_problems < 1 || !problems || !out) throw Error(SPECMC_EINVAL, "batch: no problems");
-  if (n_spectra < 1 || !spectra) throw Error(SPECMC_EINVAL, "batch: no spectra");
-  for (int i = 0; i < n_problems; ++i) std::memset(&out[i], 0, sizeof(specmc_smc_result));
-  std::vector<specmc_spectrum> sps(spectra, spectra + n_spectra);
-  std::vector<RunSpec> runs;
-  for (int i = 0; i < n_problems; ++i) {
-    const auto& p = problems[i];
-    if (p.spectrum < 0 || p.spectrum >= n_spectra) throw Error(SPECMC_EINVAL, "batch: spectrum index out of range");
-    runs.push_back(make_runspec(p.model, p.spectrum, p.cfg, sps[p.spectrum]));
-  }
-  const int device = runs[0].cfg.device;
-  for (auto& r : runs)
-    if (r.cfg.device != device) throw Error(SPECMC_EINVAL, "batch: all problems must target the same device");
-  Device dev(device);
-  // classes: same family and same launch shape
-  std::map<std::pair<int, int>, std::vector<int>> classes;
-  for (int i = 0; i < n_problems; ++i) {
-    const Shape s = pick_shape(runs[i].N);
-    classes[{runs[i].m.family, s.W * 100 + s.PPL}].push_back(i);
-  }
-  double dev_s = 0.0;
-  for (auto& kv : classes) {
-    double s = 0.0;
-    run_class(dev, runs, sps, kv.second, out, s);
-    dev_s += s;
-  }
+  if (!out) throw Error(SPECMC_EINVAL, "batch: null results");
+  Session s(n_problems, problems, n_spectra, spectra);
+  s.run();
+  const int first = s.fetch(out);
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  int first = SPECMC_OK;
-  for (int i = 0; i < n_problems; ++i) {
-    out[i].wall_seconds = wall;
-    out[i].device_seconds = dev_s;
-    if (out[i].status != SPECMC_OK && first == SPECMC_OK) {
-      first = out[i].status;
-      copy_err(err, errlen, "smc: max_levels exceeded before reaching beta = 1 (or total weight is zero)");
-    }
-  }
+  for (int i = 0; i < n_problems; ++i) out[i].wall_seconds = wall;
+  if (first != SPECMC_OK)
+    copy_err(err, errlen, "smc: max_levels exceeded before reaching beta = 1 (or total weight is zero)");
   return first;
 }
 
@@ -726,6 +760,37 @@ int specmc_smc_run_batch(int32_t n_problems, const specmc_problem* problems, int
                          const specmc_spectrum* spectra, specmc_smc_result* out, char* err, size_t errlen) {
   return guarded(err, errlen, [&]() -> int { return run_batch(n_problems, problems, n_spectra, spectra, out, err, errlen); });
 }
+
+int specmc_session_create(int32_t n_problems, const specmc_problem* problems, int32_t n_spectra,
+                          const specmc_spectrum* spectra, specmc_session** out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> int {
+    if (!out) throw Error(SPECMC_EINVAL, "null session pointer");
+    *out = reinterpret_cast<specmc_session*>(new Session(n_problems, problems, n_spectra, spectra));
+    return SPECMC_OK;
+  });
+}
+
+int specmc_session_run(specmc_session* s, double* device_seconds, char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> int {
+    if (!s) throw Error(SPECMC_EINVAL, "null session");
+    auto* S = reinterpret_cast<Session*>(s);
+    S->run();
+    if (device_seconds) *device_seconds = S->device_seconds;
+    return SPECMC_OK;
+  });
+}
+
+int specmc_session_fetch(specmc_session* s, specmc_smc_result* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> int {
+    if (!s || !out) throw Error(SPECMC_EINVAL, "null argument");
+    const int rc = reinterpret_cast<Session*>(s)->fetch(out);
+    if (rc != SPECMC_OK)
+      copy_err(err, errlen, "smc: max_levels exceeded before reaching beta = 1 (or total weight is zero)");
+    return rc;
+  });
+}
+
+void specmc_session_destroy(specmc_session* s) { delete reinterpret_cast<Session*>(s); }
 
 void specmc_result_free(specmc_smc_result* r) {
   if (!r) return;
@@ -985,6 +1050,27 @@ int specmc_launch_shape(int64_t n_points, int32_t* W, int32_t* PPL, int32_t* U) 
   if (PPL) *PPL = s.PPL;
   if (U) *U = s.U;
   return (int64_t)32 * s.W * s.PPL >= n_points ? SPECMC_OK : SPECMC_EINVAL;
+}
+
+int specmc_probe_mufu(int32_t device, double* ops, char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> int {
+    if (!ops) throw Error(SPECMC_EINVAL, "null output");
+    Device dev(device);
+    int sms = 0;
+    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
+    const int blocks = sms * 8, iters = 4096;
+    Scratch sc;
+    float* d = sc.alloc<float>(blocks);
+    Timer t;
+    cuda_check(launch_probe_mufu(d, blocks, 64, dev.stream), "probe warmup");
+    cuda_check(cudaEventRecord(t.a, dev.stream), "event");
+    cuda_check(launch_probe_mufu(d, blocks, iters, dev.stream), "probe");
+    cuda_check(cudaEventRecord(t.b, dev.stream), "event");
+    dev.sync();
+    count_launch(2);
+    *ops = (double)blocks * 256.0 * iters * 8.0 / (t.ms() * 1e-3);
+    return SPECMC_OK;
+  });
 }
 
 int specmc_device_count(void) {

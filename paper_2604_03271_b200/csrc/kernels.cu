@@ -519,6 +519,24 @@ cudaError_t launch_move(int family, const Shape& s, int dmax, const GroupDesc* g
   return cudaErrorInvalidValue;
 }
 
+// MUFU throughput probe: 8 independent ex2 chains per thread (the SFU roofline
+// denominator reported by bench.py; SASS: MUFU.EX2)
+__global__ void __launch_bounds__(256) k_probe_mufu(float* out, int iters) {
+  float a0 = threadIdx.x * 1e-3f, a1 = a0 + 0.1f, a2 = a0 + 0.2f, a3 = a0 + 0.3f;
+  float a4 = a0 + 0.4f, a5 = a0 + 0.5f, a6 = a0 + 0.6f, a7 = a0 + 0.7f;
+  for (int i = 0; i < iters; ++i) {
+    a0 = ex2f(-a0); a1 = ex2f(-a1); a2 = ex2f(-a2); a3 = ex2f(-a3);
+    a4 = ex2f(-a4); a5 = ex2f(-a5); a6 = ex2f(-a6); a7 = ex2f(-a7);
+  }
+  const float s = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+  if (s == 12345.f) out[blockIdx.x] = s;
+}
+
+cudaError_t launch_probe_mufu(float* out, int blocks, int iters, cudaStream_t st) {
+  k_probe_mufu<<<blocks, 256, 0, st>>>(out, iters);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_init_draw(const GroupDesc* gds, const int* list, int n_list, int Tmax, cudaStream_t st) {
   dim3 grid((Tmax + 255) / 256, n_list);
   k_init_draw<<<grid, 256, 0, st>>>(gds, list);

@@ -44,6 +44,8 @@ cudaError_t launch_temper(const GroupDesc* d_gds, const int* d_list, int n_list,
 // step-size statistics + history + buffer flip (one CTA per group)
 cudaError_t launch_stats(const GroupDesc* d_gds, const int* d_list, int n_list, cudaStream_t st);
 
+cudaError_t launch_probe_mufu(float* d_out, int blocks, int iters, cudaStream_t st);
+
 // ---- parity units (single-array versions of the temper building blocks)
 cudaError_t launch_unit_ess(const double* d_lw, int64_t n, double* d_out, int* d_err, cudaStream_t st);
 cudaError_t launch_unit_log_mean_exp(const double* d_v, int64_t n, double* d_out, cudaStream_t st);

@@ -118,12 +118,7 @@ def smc_run(spec: ModelSpec, data: Spectrum, cfg: SmcConfig) -> RunReport:
     return smc_run_batch([(spec, 0, cfg)], [data])[0]
 
 
-def smc_run_batch(problems: Sequence[Tuple[ModelSpec, int, SmcConfig]], spectra: Sequence[Spectrum],
-                  raise_on_error: bool = True):
-    """Runs every (spec, spectrum index, cfg) concurrently on one GPU.
-
-    Returns a list of RunReport (or, with raise_on_error=False, the exception
-    instance for runs that failed, e.g. max_levels exceeded)."""
+def _pack(problems, spectra):
     n = len(problems)
     keep = []
     probs = (_lib.ProblemC * n)()
@@ -135,13 +130,12 @@ def smc_run_batch(problems: Sequence[Tuple[ModelSpec, int, SmcConfig]], spectra:
     for j, s in enumerate(spectra):
         keep.append(s)
         sps[j] = _lib.SpectrumC(_p(s.xs), _p(s.ys), len(s.xs))
-    res = (_lib.SmcResultC * n)()
-    err = C.create_string_buffer(1024)
-    rc = lib.specmc_smc_run_batch(n, probs, len(spectra), sps, res, err, 1024)
+    return probs, sps, keep
+
+
+def _collect(problems, spectra, res, raise_on_error):
+    out = []
     try:
-        if rc and rc != _lib.SPECMC_ERUNTIME:
-            _raise(rc, err)
-        out = []
         for i, (spec, si, cfg) in enumerate(problems):
             r = res[i]
             if r.status != _lib.SPECMC_OK:
@@ -153,8 +147,76 @@ def smc_run_batch(problems: Sequence[Tuple[ModelSpec, int, SmcConfig]], spectra:
                 out.append(_report(spec, cfg, len(spectra[si].xs), r))
         return out
     finally:
-        for i in range(n):
+        for i in range(len(problems)):
             lib.specmc_result_free(C.byref(res[i]))
+
+
+def smc_run_batch(problems: Sequence[Tuple[ModelSpec, int, SmcConfig]], spectra: Sequence[Spectrum],
+                  raise_on_error: bool = True):
+    """Runs every (spec, spectrum index, cfg) concurrently on one GPU.
+
+    Returns a list of RunReport (or, with raise_on_error=False, the exception
+    instance for runs that failed, e.g. max_levels exceeded)."""
+    probs, sps, keep = _pack(problems, spectra)
+    res = (_lib.SmcResultC * len(problems))()
+    err = C.create_string_buffer(1024)
+    rc = lib.specmc_smc_run_batch(len(problems), probs, len(spectra), sps, res, err, 1024)
+    if rc and rc != _lib.SPECMC_ERUNTIME:
+        for i in range(len(problems)):
+            lib.specmc_result_free(C.byref(res[i]))
+        _raise(rc, err)
+    return _collect(problems, spectra, res, raise_on_error)
+
+
+class Session:
+    """Device-resident batch (specmc_session_*): inputs stay in HBM across runs."""
+
+    def __init__(self, problems, spectra):
+        self.problems, self.spectra = list(problems), list(spectra)
+        probs, sps, self._keep = _pack(self.problems, self.spectra)
+        self._h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        rc = lib.specmc_session_create(len(self.problems), probs, len(self.spectra), sps, C.byref(self._h), err, 1024)
+        if rc:
+            _raise(rc, err)
+
+    def run(self) -> float:
+        """Runs every problem from init_ensemble to beta = 1; returns device seconds."""
+        ds = C.c_double()
+        err = C.create_string_buffer(1024)
+        rc = lib.specmc_session_run(self._h, C.byref(ds), err, 1024)
+        if rc:
+            _raise(rc, err)
+        return ds.value
+
+    def fetch(self, raise_on_error: bool = True):
+        res = (_lib.SmcResultC * len(self.problems))()
+        err = C.create_string_buffer(1024)
+        rc = lib.specmc_session_fetch(self._h, res, err, 1024)
+        if rc and rc != _lib.SPECMC_ERUNTIME:
+            _raise(rc, err)
+        return _collect(self.problems, self.spectra, res, raise_on_error)
+
+    def close(self):
+        if self._h:
+            lib.specmc_session_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def probe_mufu(device: int = 0) -> float:
+    """Measured MUFU ex2 throughput (ops/s) of the device."""
+    v = C.c_double()
+    err = C.create_string_buffer(512)
+    rc = lib.specmc_probe_mufu(device, C.byref(v), err, 512)
+    if rc:
+        _raise(rc, err)
+    return v.value
 
 
 # ---------------------------------------------------------------- parity units

@@ -1,0 +1,102 @@
+"""Pin the C restatement (oracle/liboracle.so) against the UNCHANGED reference
+sources built in this container (oracle/_ref/libspecmc_ref.so, Eigen-subset
+shim): bit-for-bit equality of every hot-path function and of whole smc_run
+results (CPU only; skipped where the reference build is unavailable)."""
+import numpy as np
+import pytest
+
+from helpers import conjugate, oracle_model, ramp
+from paper_2604_03271_b200 import model as M
+from paper_2604_03271_b200 import synthetic as syn
+
+
+def _models():
+    out = []
+    d = ramp(60, 0.0, 3.0, 0.2, 2.0)
+    out.append((M.gm_model(3, 0.0, 3.0, 0.1, "normal15"), d))
+    sp, _ = syn.gen_xps(3, 5)
+    out.append((M.xps_model(3, sp), sp))
+    out.append((M.ModelSpec("xps", 3, M.xps_model(3, sp).layout, M.PoissonNoise()), sp))
+    out.append((M.ModelSpec("xps", 3, M.xps_model(3, sp).layout, M.GaussianApproxPoissonNoise()), sp))
+    return out
+
+
+@pytest.mark.parametrize("i", range(4))
+def test_energy_and_forward_bitwise(port, ref, i):
+    spec, data = _models()[i]
+    om = oracle_model(spec, data)
+    th, E = port.init_ensemble(om, 64, 17)
+    for t, e in zip(th, E):
+        assert ref.energy(om, t) == e or (np.isinf(e) and np.isinf(ref.energy(om, t)))
+        assert np.array_equal(port.forward(om, t), ref.forward(om, t))
+
+
+def test_tempering_and_resampling_bitwise(port, ref):
+    rng = np.random.default_rng(0)
+    for T in (2, 100, 4096):
+        E = 3 + rng.exponential(size=T)
+        E[::7] = np.inf
+        for bp in (0.0, 0.25):
+            assert port.next_beta(E, 300.0, bp, 0.5) == ref.next_beta(E, 300.0, bp, 0.5)
+        lw = rng.normal(size=T) * 3
+        assert port.ess(lw) == ref.ess(lw)
+        assert port.log_mean_exp(lw) == ref.log_mean_exp(lw)
+        for seed in (1, 2, 3):
+            u = ref.uniform01(seed)
+            S = max(2, T // 8)
+            assert np.array_equal(port.systematic_resample(lw, S, u), ref.systematic_resample(lw, S, seed))
+
+
+def test_predictor_and_rm_bitwise(port, ref):
+    rng = np.random.default_rng(1)
+    pk = np.array([0, 1, 2], dtype=np.int32)
+    pa, pb = np.array([0.0, 2.0, 0.0]), np.array([4.0, 3.0, 12.0])
+    for H in range(0, 8):
+        hb = np.sort(rng.uniform(1e-3, 1, H))
+        ha, hs = rng.uniform(0, 1, 3 * H), rng.uniform(0.1, 3, 3 * H)
+        assert np.array_equal(port.predict_step_size(hb, ha, hs, 0.5, pk, pa, pb),
+                              ref.predict_step_size(hb, ha, hs, 0.5, pk, pa, pb))
+    for t in range(1, 20):
+        assert port.rm_update(0.7, t % 2, t) == ref.rm_update(0.7, t % 2, t)
+
+
+@pytest.mark.parametrize("case", ["conjugate", "gm", "xps"])
+def test_smc_run_bitwise(port, ref, case):
+    if case == "conjugate":
+        spec, data, *_ = conjugate(20, 404, port)
+        T, n, seed = 400, 5, 7
+    elif case == "gm":
+        data = syn.gen_gm(syn.GM3_TRUTH[:3], 8, 40, 0.0, 3.0, 0.1)
+        spec, T, n, seed = M.gm_model(1, 0.0, 3.0, 0.1), 300, 5, 21
+    else:
+        data, _ = syn.gen_xps(2, 11)
+        spec, T, n, seed = M.xps_model(2, data), 100, 5, 3
+    om = oracle_model(spec, data)
+    a = port.smc_run(om, T, n, 0.5, seed=seed)
+    b = ref.smc_run(om, T, n, 0.5, seed=seed)
+    assert a.F == b.F
+    assert a.levels == b.levels
+    assert np.array_equal(a.ladder, b.ladder)
+    assert np.array_equal(a.log_mean_w, b.log_mean_w)
+    assert np.array_equal(a.acc_rate, b.acc_rate)
+    assert np.array_equal(a.thetas, b.thetas)
+
+
+def test_worker_count_invariance_of_reference(ref, port):  # acceptance criterion 7 / test_smc.cpp:159-184
+    spec, data, *_ = conjugate(15, 2024, port)
+    om = oracle_model(spec, data)
+    r1 = ref.smc_run(om, 400, 5, 0.5, seed=3, workers=1)
+    r3 = ref.smc_run(om, 400, 5, 0.5, seed=3, workers=3)
+    assert r1.F == r3.F and np.array_equal(r1.thetas, r3.thetas)
+
+
+def test_model_select_matches_reference(ref):
+    from paper_2604_03271_b200 import smc as SM
+    ks = [1, 1, 2, 2, 3, 3]
+    fs = [10.0, 10.2, 5.0, 5.1, 5.05, 5.0]
+    dv = [0, 0, 0, 0, 0, 0]
+    rows = [(k, SM.RunReport(F=f, diverged=bool(v))) for k, f, v in zip(ks, fs, dv)]
+    assert SM.model_select(rows).K_best == ref.model_select(ks, fs, dv) == 3
+    fs2 = [1.0, 1.0, float("nan"), 0.5, 0.8, 0.8]
+    rows = [(k, SM.RunReport(F=f)) for k, f in zip(ks, fs2)]
+    assert SM.model_select(rows).K_best == ref.model_select(ks, fs2, dv) == 3
