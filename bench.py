@@ -241,31 +241,17 @@ def run_ours(args, ws, rank, local):
     # ---- model selection over all trials (ranks); max-over-ranks timing
     Fs = [r.F if not isinstance(r, Exception) else float("nan") for r in reps]
     if dist:
-        t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
-        tot = torch.tensor([evals_step * args.steps], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tot)
-        total_evals = float(tot.item())
-        gathered = [None] * ws
-        dist.all_gather_object(gathered, Fs)
+        from paper_2604_03271_b200 import dist as D
+        elapsed, total_evals = D.reduce_timing(elapsed, evals_step * args.steps)
+        k_sel, _ = D.gather_selection(ks, Fs)
         if e2e:
-            te = torch.tensor([e2e["t"]], device="cuda", dtype=torch.float64)
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-            ee = torch.tensor([float(e2e["value"])], device="cuda", dtype=torch.float64)
-            dist.all_reduce(ee)
-            e2e["t"], e2e["value"] = float(te.item()), float(ee.item())
+            e2e["t"], e2e["value"] = D.reduce_timing(e2e["t"], float(e2e["value"]))
     else:
         total_evals = evals_step * args.steps
-        gathered = [Fs]
-    rows = []
-    for Ftr in gathered:
-        for K, F in zip(ks, Ftr):
-            rows.append((K, S.RunReport(F=F)))
-    try:
-        k_sel = S.model_select(rows).K_best
-    except RuntimeError:
-        k_sel = None
+        try:
+            k_sel = S.model_select([(K, S.RunReport(F=F)) for K, F in zip(ks, Fs)]).K_best
+        except RuntimeError:
+            k_sel = None
 
     if rank != 0:
         if dist:

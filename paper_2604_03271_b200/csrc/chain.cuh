@@ -66,7 +66,7 @@ __device__ __forceinline__ BlockC block_consts(const double* p) {
     c.c1 = (float)(A * eta);
     c.c2 = (float)(A * (1.0 - eta));
     const float s = (float)sig;
-    c.c3 = __frcp_rn(s * s);
+    c.c3 = rcpf(s * s);
   } else {
     c.c1 = (float)p[0];
     c.mu = 0.f;
@@ -134,25 +134,27 @@ struct Unit {
   }
 };
 
-// P_k = sum_b g_b(x_k) in layout order, optionally with component ovr_i := ovr_v
+// P_k = sum over non-faulty blocks of g_b(x_k), in layout order (combine,
+// model.cpp:287-288).  Returns the bit mask of faulty blocks (eval_block
+// returning false, model.cpp:272-275): any set bit means E = +inf.
 template <int FAM, int PPL, int W>
-__device__ __forceinline__ bool full_signal(const GroupDesc& g, const double* th, int ovr_i, double ovr_v,
-                                            const Unit<PPL, W>& u, float (&P)[PPL]) {
+__device__ __forceinline__ unsigned long long full_signal(const GroupDesc& g, const double* th,
+                                                          const Unit<PPL, W>& u, float (&P)[PPL]) {
   constexpr int stride = block_stride<FAM>();
 #pragma unroll
   for (int k = 0; k < PPL; ++k) P[k] = 0.f;
   const int nb = FAM == FAM_OFFSET ? 1 : g.K;
-  bool ok = true;
+  unsigned long long fmask = 0ull;
   for (int b = 0; b < nb; ++b) {
-    double p[stride];
-#pragma unroll
-    for (int j = 0; j < stride; ++j) p[j] = (b * stride + j == ovr_i) ? ovr_v : th[b * stride + j];
-    const BlockC c = block_consts<FAM>(p);
-    ok = ok && c.ok;
+    const BlockC c = block_consts<FAM>(th + b * stride);
+    if (!c.ok) {
+      fmask |= 1ull << b;
+      continue;
+    }
 #pragma unroll
     for (int k = 0; k < PPL; ++k) P[k] += shape<FAM>(c, u.x(k));
   }
-  return ok;
+  return fmask;
 }
 
 // fp64 reduction of the lane partials over the unit (identical in every warp)
@@ -173,6 +175,7 @@ __device__ __forceinline__ double unit_sum(Unit<PPL, W>& u, float acc) {
 // per-point centred NLL term, in units of 1/2 ln 2 for the hetero model:
 //   gauss:   r^2                                        E = a0 + a1 * sum
 //   hetero:  lg2(var/s) + q' r^2/var, q' = q / (ln2/2)  E = a0 + a1 (ln2/2) sum
+//            (hlin: the same with var linear in f)
 //   poisson: f - y - y ln(f/y)                          E = a0 + a1 * sum
 template <int NZ>
 __device__ __forceinline__ float noise_term(const GroupDesc& g, float f, float4 yq) {
@@ -181,6 +184,9 @@ __device__ __forceinline__ float noise_term(const GroupDesc& g, float f, float4 
     return r * r;
   } else if (NZ == NZ_HETERO) {
     const float var = fmaf(fmaf(g.nz_a1, f, g.nz_a0), f, g.nz_a2);
+    return fmaf(g.nz_q, (r * r) * rcpf(var), lg2f(var * yq.y));
+  } else if (NZ == NZ_HLIN) {  // s1 = 0: var = s0^2 f + s2^2 (GaussApprox-Poisson when (1, 0, 0))
+    const float var = fmaf(g.nz_a0, f, g.nz_a2);
     return fmaf(g.nz_q, (r * r) * rcpf(var), lg2f(var * yq.y));
   } else {
     return (f - yq.x) - yq.x * (kLn2 * lg2f(f * yq.y));
@@ -254,9 +260,10 @@ __device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, 
   float acc = 0.f;
   if (!degen) {
     const float scale = ba / total;
+    const float base = fmaf(scale, prefix, bga);
 #pragma unroll
     for (int k = 0; k < PPL; ++k) {
-      const float B = fmaf(scale, prefix + Cn[k], bga);
+      const float B = fmaf(scale, Cn[k], base);
       const float4 yq = u.y(k);
       acc = fmaf(yq.z, noise_term<NZ>(g, Pn[k] + B, yq), acc);
     }
@@ -278,12 +285,14 @@ __device__ __forceinline__ double evaluate(const GroupDesc& g, Unit<PPL, W>& u, 
     switch (g.noise) {
       case NZ_GAUSS: return eval_shirley_nz<PPL, W, NZ_GAUSS>(g, u, Pn, bga, bgb, amp_bound);
       case NZ_HETERO: return eval_shirley_nz<PPL, W, NZ_HETERO>(g, u, Pn, bga, bgb, amp_bound);
+      case NZ_HLIN: return eval_shirley_nz<PPL, W, NZ_HLIN>(g, u, Pn, bga, bgb, amp_bound);
       default: return eval_shirley_nz<PPL, W, NZ_POISSON>(g, u, Pn, bga, bgb, amp_bound);
     }
   } else {
     switch (g.noise) {
       case NZ_GAUSS: return eval_plain_nz<PPL, W, NZ_GAUSS>(g, u, Pn);
       case NZ_HETERO: return eval_plain_nz<PPL, W, NZ_HETERO>(g, u, Pn);
+      case NZ_HLIN: return eval_plain_nz<PPL, W, NZ_HLIN>(g, u, Pn);
       default: return eval_plain_nz<PPL, W, NZ_POISSON>(g, u, Pn);
     }
   }
@@ -323,10 +332,10 @@ __device__ __forceinline__ int find_group(const int* prefix, int n, int x) {
 }
 
 template <int FAM>
-__device__ __forceinline__ float amp_bound(const GroupDesc& g, const double* th, int ovr_i, double ovr_v) {
+__device__ __forceinline__ float amp_sum(const GroupDesc& g, const double* th) {
   if (FAM != FAM_XPS) return 0.f;
   float s = 0.f;
-  for (int b = 0; b < g.K; ++b) s += fabsf((float)(4 * b == ovr_i ? ovr_v : th[4 * b]));
+  for (int b = 0; b < g.K; ++b) s += fabsf((float)th[4 * b]);
   return s;
 }
 
@@ -335,7 +344,6 @@ __global__ void __launch_bounds__(W >= 8 ? 32 * W : 256, W >= 8 ? 1 : 2)
     k_chain(const GroupDesc* __restrict__ gds, const int* __restrict__ list, const int* __restrict__ cta_prefix,
             int n_list, int U, int dpad) {
   using SM = Smem<PPL, W>;
-  constexpr int L = 32 * W;
   constexpr int stride = block_stride<FAM>();
   extern __shared__ __align__(16) unsigned char smem[];
   const int gi = find_group(cta_prefix, n_list, blockIdx.x);
@@ -400,11 +408,11 @@ __global__ void __launch_bounds__(W >= 8 ? 32 * W : 256, W >= 8 ? 1 : 2)
 
   const int ibg = 4 * g.K;  // xps Shirley endpoints (a, b) at ibg, ibg + 1
   float P[PPL];
-  bool pvalid = full_signal<FAM, PPL, W>(g, th, -1, 0.0, u, P);
-  double e = pvalid ? evaluate<FAM, PPL, W>(g, u, P, FAM == FAM_XPS ? (float)th[ibg] : 0.f,
-                                            FAM == FAM_XPS ? (float)th[ibg + 1] : 0.f,
-                                            amp_bound<FAM>(g, th, -1, 0.0))
-                    : dinf();
+  unsigned long long fmask = full_signal<FAM, PPL, W>(g, th, u, P);
+  float asum = amp_sum<FAM>(g, th);
+  double e = fmask ? dinf()
+                   : evaluate<FAM, PPL, W>(g, u, P, FAM == FAM_XPS ? (float)th[ibg] : 0.f,
+                                           FAM == FAM_XPS ? (float)th[ibg + 1] : 0.f, asum);
   if (ENERGY) {
     if (wiu == 0 && lane == 0) g.E[cur][c] = e;
     return;
@@ -421,9 +429,9 @@ __global__ void __launch_bounds__(W >= 8 ? 32 * W : 256, W >= 8 ? 1 : 2)
   double* En = g.E[cur ^ 1];
   const int npeak = FAM == FAM_OFFSET ? 0 : stride * g.K;
   unsigned long long trials = 0;
-  float G[PPL];
-  float Pn[PPL];
-  bool gvalid = false;
+  float G[PPL];  // g_b(x) of the block being swept (0 for a faulty block)
+#pragma unroll
+  for (int k = 0; k < PPL; ++k) G[k] = 0.f;
 
   for (int t = 1; t <= n; ++t) {
     // Philox draws of this sweep: lane i handles components i, i+32, ...
@@ -434,15 +442,18 @@ __global__ void __launch_bounds__(W >= 8 ? 32 * W : 256, W >= 8 ? 1 : 2)
     }
     __syncwarp();
     const float gam = (t <= adapt_sweeps) ? exp2f(-0.6f * log2f((float)t)) : 0.f;  // t^-0.6 (mcmc.cpp:15)
+    asum = amp_sum<FAM>(g, th);
     for (int i = 0; i < d; ++i) {
       const int b = i / stride, j = i - b * stride;
       const bool peak = i < npeak;
-      if (peak && j == 0) {  // entering block b: cache g_b(x)
+      if (FAM != FAM_OFFSET && peak && j == 0) {  // entering block b: cache g_b(x)
         const BlockC cb = block_consts<FAM>(th + b * stride);
-        gvalid = cb.ok && pvalid;
-        if (gvalid) {
+        if (cb.ok) {
 #pragma unroll
           for (int k = 0; k < PPL; ++k) G[k] = shape<FAM>(cb, u.x(k));
+        } else {
+#pragma unroll
+          for (int k = 0; k < PPL; ++k) G[k] = 0.f;
         }
       }
       const double old_i = th[i];
@@ -452,34 +463,47 @@ __global__ void __launch_bounds__(W >= 8 ? 32 * W : 256, W >= 8 ? 1 : 2)
       bool accept = false;
       if (in_support) {
         ++trials;
-        bool nvalid = true;
-        if (FAM == FAM_OFFSET || !pvalid || (peak && !gvalid)) {
-          nvalid = full_signal<FAM, PPL, W>(g, th, i, new_i, u, Pn);
+        // ---- trial signal Pn = P + D (the reference's BlockEvaluator::trial, energy.cpp:57-84)
+        float D[PPL];
+        unsigned long long fnew = fmask;
+        float dA = 0.f;
+        if (FAM == FAM_OFFSET) {
+          const float dv = (float)new_i - (float)old_i;
+#pragma unroll
+          for (int k = 0; k < PPL; ++k) D[k] = dv;
         } else if (!peak) {  // Shirley endpoint: enters combine() only (block -1)
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) Pn[k] = P[k];
-        } else if (j == 0 && old_i != 0.0) {  // amplitude: g' = (A'/A) g
+          for (int k = 0; k < PPL; ++k) D[k] = 0.f;
+        } else if (j == 0 && old_i != 0.0 && !((fmask >> b) & 1ull)) {  // amplitude: g' = (A'/A) g
           const float r = (float)(new_i / old_i - 1.0);
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) Pn[k] = fmaf(r, G[k], P[k]);
+          for (int k = 0; k < PPL; ++k) D[k] = r * G[k];
+          dA = fabsf((float)new_i) - fabsf((float)old_i);
         } else {
           double pn[stride];
 #pragma unroll
           for (int q = 0; q < stride; ++q) pn[q] = (q == j) ? new_i : th[b * stride + q];
           const BlockC cn = block_consts<FAM>(pn);
-          nvalid = cn.ok;
-          if (nvalid) {
+          if (cn.ok) {
+            fnew &= ~(1ull << b);
 #pragma unroll
-            for (int k = 0; k < PPL; ++k) Pn[k] = P[k] + (shape<FAM>(cn, u.x(k)) - G[k]);
+            for (int k = 0; k < PPL; ++k) D[k] = shape<FAM>(cn, u.x(k)) - G[k];
+          } else {
+            fnew |= 1ull << b;
+#pragma unroll
+            for (int k = 0; k < PPL; ++k) D[k] = -G[k];
           }
+          if (j == 0) dA = fabsf((float)new_i) - fabsf((float)old_i);
         }
-        float bga = 0.f, bgb = 0.f, ab = 0.f;
+        float Pn[PPL];
+#pragma unroll
+        for (int k = 0; k < PPL; ++k) Pn[k] = P[k] + D[k];
+        float bga = 0.f, bgb = 0.f;
         if (FAM == FAM_XPS) {
           bga = (float)(i == ibg ? new_i : th[ibg]);
           bgb = (float)(i == ibg + 1 ? new_i : th[ibg + 1]);
-          ab = amp_bound<FAM>(g, th, i, new_i);
         }
-        const double e_new = nvalid ? evaluate<FAM, PPL, W>(g, u, Pn, bga, bgb, ab) : dinf();
+        const double e_new = fnew ? dinf() : evaluate<FAM, PPL, W>(g, u, Pn, bga, bgb, asum + dA);
         // mcmc.cpp:72-80
         double lr;
         const bool inf_new = e_new == dinf(), inf_old = e == dinf();
@@ -492,17 +516,16 @@ __global__ void __launch_bounds__(W >= 8 ? 32 * W : 256, W >= 8 ? 1 : 2)
         else
           lr = -beta * nd * (e_new - e) + dlp;
         accept = lr >= 0.0 || (double)ub[i] < lr;
+        // branch-free commit: the register arrays are updated in place
+        const float af = accept ? 1.f : 0.f;
+#pragma unroll
+        for (int k = 0; k < PPL; ++k) {
+          P[k] = accept ? Pn[k] : P[k];
+          G[k] = fmaf(af, D[k], G[k]);
+        }
         if (accept) {
-          if (peak && gvalid && nvalid) {
-#pragma unroll
-            for (int k = 0; k < PPL; ++k) G[k] += Pn[k] - P[k];
-          } else if (peak) {
-            gvalid = false;
-          }
-#pragma unroll
-          for (int k = 0; k < PPL; ++k) P[k] = Pn[k];
-          if (pvalid != nvalid) gvalid = false;
-          pvalid = nvalid;
+          fmask = fnew;
+          asum += dA;
           e = e_new;
           if (lane == 0) {
             th[i] = new_i;

@@ -236,7 +236,7 @@ PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, 
         q = m.paper_literal ? 1.0 : 0.5;
       }
       // device terms are lg2(var/s) + q' r^2/var with q' = q / (ln2/2)
-      ps.nz = NZ_HETERO;
+      ps.nz = h1 == 0.0 ? NZ_HLIN : NZ_HETERO;
       ps.a0 = (float)h0;
       ps.a1 = (float)h1;
       ps.a2 = (float)h2;

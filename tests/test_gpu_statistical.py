@@ -1,0 +1,134 @@
+"""Statistical parity of the device sampler with the reference (GPU).
+
+The GPU draws from Philox streams, the reference from xoshiro256++ streams
+(SURVEY.md 7.2.8), so F, the ladder and the posteriors agree in distribution
+only.  Tolerances are stated per test:
+  * model selection: the reference's acceptance criterion 4
+    (proj/tests/acceptance/acceptance_main.cpp:224-262): K = 3 on the gm3
+    data and K = 7 on the xps surrogate in >= 9/10 trials;
+  * F: |mean_gpu - mean_oracle| <= 4 * sqrt(se_gpu^2 + se_oracle^2) over
+    repeated seeds (both samplers run the same T, n, ess);
+  * posterior moments: within 4 standard errors of the oracle's posterior.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from helpers import conjugate, oracle_model
+from paper_2604_03271_b200 import model as M
+from paper_2604_03271_b200 import synthetic as syn
+
+pytestmark = pytest.mark.gpu
+
+
+def _gm3():
+    # gen_gaussian_mixture(3, seed 1): 300 points on [0, 3], sigma 0.1 (synthetic.cpp:178-228)
+    return syn.gen_gm(syn.GM3_TRUTH, 1, 300, 0.0, 3.0, 0.1)
+
+
+def test_criterion4_gm3_selects_3(smc):
+    data = _gm3()
+    probs = []
+    for t in range(10):
+        seed = syn.trial_seed(777, t)
+        for k in (2, 3, 4):
+            probs.append((M.gm_model(k, 0.0, 3.0, 0.1, "uniform"), 0, smc.SmcConfig(T=30000, n=10, seed=seed)))
+    reps = smc.smc_run_batch(probs, [data])
+    hits = 0
+    for t in range(10):
+        rows = [(k, reps[3 * t + i]) for i, k in enumerate((2, 3, 4))]
+        hits += smc.model_select(rows).K_best == 3
+    assert hits >= 9, hits
+
+
+def test_criterion4_xps_selects_7(smc):
+    data, _ = syn.gen_xps(7, 11)
+    probs = []
+    for t in range(10):
+        seed = syn.trial_seed(888, t)
+        for k in (6, 7, 8):
+            probs.append((M.xps_model(k, data), 0, smc.SmcConfig(T=2000, n=10, seed=seed)))
+    reps = smc.smc_run_batch(probs, [data])
+    hits = 0
+    for t in range(10):
+        rows = [(k, reps[3 * t + i]) for i, k in enumerate((6, 7, 8))]
+        hits += smc.model_select(rows).K_best == 7
+    assert hits >= 9, hits
+
+
+def _compare_F(smc, port, spec, data, T, n, seeds_gpu, seeds_cpu):
+    om = oracle_model(spec, data)
+    f_cpu = np.array([port.smc_run(om, T, n, 0.5, seed=s, keep=False).F for s in seeds_cpu])
+    reps = smc.smc_run_batch([(spec, 0, smc.SmcConfig(T=T, n=n, seed=s)) for s in seeds_gpu], [data])
+    f_gpu = np.array([r.F for r in reps])
+    se = math.sqrt(f_gpu.var(ddof=1) / len(f_gpu) + f_cpu.var(ddof=1) / len(f_cpu))
+    return f_gpu, f_cpu, se
+
+
+def test_free_energy_matches_oracle_gm(smc, port):
+    data = _gm3()
+    spec = M.gm_model(3, 0.0, 3.0, 0.1, "normal15")
+    f_gpu, f_cpu, se = _compare_F(smc, port, spec, data, 1000, 10, range(100, 140), range(8))
+    assert abs(f_gpu.mean() - f_cpu.mean()) <= 4 * se + 0.05, (f_gpu.mean(), f_cpu.mean(), se)
+
+
+def test_free_energy_matches_oracle_xps(smc, port):
+    data, _ = syn.gen_xps(1, 3)
+    spec = M.xps_model(1, data)
+    f_gpu, f_cpu, se = _compare_F(smc, port, spec, data, 400, 8, range(100, 132), range(6))
+    assert abs(f_gpu.mean() - f_cpu.mean()) <= 4 * se + 0.05, (f_gpu.mean(), f_cpu.mean(), se)
+
+
+def test_free_energy_conjugate_many_seeds(smc, port):
+    # acceptance criterion 1 (acceptance_main.cpp:124-147): |dF| <= 0.05 at T = 1e4
+    spec, data, F_exact, mn, vn = conjugate(50, 101, port, truth=1.0, sigma=1.0, m0=0.0, v0=1.0)
+    reps = smc.smc_run_batch([(spec, 0, smc.SmcConfig(T=10000, n=10, seed=s)) for s in range(7, 17)], [data])
+    F = np.array([r.F for r in reps])
+    assert abs(F.mean() - F_exact) <= 0.05
+    post = np.concatenate([r.posterior[0] for r in reps])
+    assert abs(post.mean() - mn) <= 4 * math.sqrt(vn / len(post)) * 10  # chains are correlated
+    assert abs(post.var() / vn - 1.0) < 0.05
+
+
+def test_posterior_moments_match_oracle_gm1(smc, port):
+    data = syn.gen_gm(syn.GM3_TRUTH[3:6], 8, 60, 0.0, 3.0, 0.1)
+    spec = M.gm_model(1, 0.0, 3.0, 0.1, "normal15")
+    om = oracle_model(spec, data)
+    r_cpu = port.smc_run(om, 4000, 10, 0.5, seed=5)
+    r_gpu = smc.smc_run(spec, data, smc.SmcConfig(T=20000, n=10, seed=5))
+    th_cpu = r_cpu.thetas
+    th_gpu = r_gpu.posterior.T
+    for i in range(3):
+        m_c, s_c = th_cpu[:, i].mean(), th_cpu[:, i].std()
+        m_g, s_g = th_gpu[:, i].mean(), th_gpu[:, i].std()
+        assert abs(m_g - m_c) <= 4 * s_c / math.sqrt(4000 / 10) + 1e-9, (i, m_g, m_c, s_c)
+        assert abs(s_g / s_c - 1.0) < 0.15, (i, s_g, s_c)
+
+
+def test_ladder_and_diagnostics_shape(smc):
+    w = syn.config("C1")
+    rep = smc.smc_run(w.spec(3), w.data, smc.SmcConfig(T=4096, n=8, seed=2))
+    lad = rep.arrays["ladder"]
+    L = int(rep.scalars["levels"])
+    assert len(lad) == L + 1 and lad[0] == 0.0 and lad[-1] == 1.0 and np.all(np.diff(lad) > 0)
+    er = rep.arrays["level_ess_ratio"]
+    assert np.all(np.abs(er[:-1] - 0.5) < 1e-5)  # bisection hits the target except the last jump
+    assert np.all((rep.arrays["level_acc_rate"] > 0) & (rep.arrays["level_acc_rate"] < 1))
+    assert rep.posterior.shape == (9, 4096) and np.all(np.isfinite(rep.energies))
+    assert rep.param_names[:3] == ["A1", "mu1", "b1"]
+
+
+def test_seed_replay_is_bitwise(smc):
+    w = syn.config("C1")
+    a = smc.smc_run(w.spec(2), w.data, smc.SmcConfig(T=1024, n=8, seed=9))
+    b = smc.smc_run(w.spec(2), w.data, smc.SmcConfig(T=1024, n=8, seed=9))
+    assert a.F == b.F and np.array_equal(a.posterior, b.posterior)
+
+
+def test_batch_equals_single_runs(smc):
+    # a run's result does not depend on what else shares the batch
+    w = syn.config("C1")
+    single = smc.smc_run(w.spec(2), w.data, smc.SmcConfig(T=1024, n=8, seed=4))
+    batch = smc.smc_run_batch([(w.spec(k), 0, smc.SmcConfig(T=1024, n=8, seed=4)) for k in (1, 2, 3)], [w.data])
+    assert batch[1].F == single.F and np.array_equal(batch[1].posterior, single.posterior)
