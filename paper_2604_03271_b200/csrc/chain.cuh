@@ -12,7 +12,7 @@
 // consecutive points [l*PPL, (l+1)*PPL) of the spectrum and keeps, in
 // registers,
 //   P[k]  committed peak signal  sum_b g_b(x)      (combine, model.cpp:287-288)
-//   G[k]  cached g_b(x) of the block being swept
+//   G[k]  cached g_b(x) of the block being swept (shared memory, lane-transposed)
 // A proposal changes one block: the trial signal is Pn = P + g_new - G, and an
 // amplitude proposal needs no transcendental at all (Pn = P + (A'/A - 1) G).
 // The Shirley background (lineshapes.hpp:65-83) needs the cumulative
@@ -100,7 +100,7 @@ struct Xch {  // per-unit cross-warp exchange, double-buffered by parity
 //   sc  float2 [PPL][L]   (c_k, h_{k+1})
 //   sy  float4 [PPL][L]   (y_k, 1/s_k, weight, 0)
 //   per warp: th f64[dpad], ls f64[dpad], acc i32[dpad], z f32[dpad], u f32[dpad]
-//   per unit: Xch
+//   per unit: Xch, then G float [PPL][L] (cached g_b(x) of the block being swept)
 template <int PPL, int W>
 struct Smem {
   static constexpr int L = 32 * W;
@@ -113,7 +113,7 @@ struct Smem {
   __host__ __device__ static size_t bytes(int U, int dpad) {
     size_t b = off_w + (size_t)U * W * per_warp(dpad);
     b = (b + 15) & ~(size_t)15;
-    return b + (size_t)U * sizeof(Xch);
+    return b + (size_t)U * sizeof(Xch) + (size_t)U * NPT * 4;  // + per-unit block-shape cache G
   }
 };
 
@@ -339,8 +339,15 @@ __device__ __forceinline__ float amp_sum(const GroupDesc& g, const double* th) {
   return s;
 }
 
+// registers: PPL <= 8 -> 3 CTAs of 256 threads per SM (<= 85 regs), else 2 (<= 128)
+template <int W, int PPL>
+struct Bounds {
+  static constexpr int threads = W >= 8 ? 32 * W : 256;
+  static constexpr int min_blocks = (65536 / threads) / (PPL <= 8 ? 85 : 128) > 0 ? (65536 / threads) / (PPL <= 8 ? 85 : 128) : 1;
+};
+
 template <int FAM, int PPL, int W, bool ENERGY>
-__global__ void __launch_bounds__(W >= 8 ? 32 * W : 256, W >= 8 ? 1 : 2)
+__global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_blocks)
     k_chain(const GroupDesc* __restrict__ gds, const int* __restrict__ list, const int* __restrict__ cta_prefix,
             int n_list, int U, int dpad) {
   using SM = Smem<PPL, W>;
@@ -363,6 +370,7 @@ __global__ void __launch_bounds__(W >= 8 ? 32 * W : 256, W >= 8 ? 1 : 2)
   float* ub = zb + dpad;
   const size_t xoff = ((SM::off_w + (size_t)U * W * SM::per_warp(dpad)) + 15) & ~(size_t)15;
   Xch* xcs = reinterpret_cast<Xch*>(smem + xoff);
+  float* gcache = reinterpret_cast<float*>(smem + xoff + (size_t)U * sizeof(Xch));
 
   // ---- stage the spectrum: cp.async.bulk (UBLKCP) completing on an mbarrier
   if (threadIdx.x == 0) {
@@ -429,9 +437,8 @@ __global__ void __launch_bounds__(W >= 8 ? 32 * W : 256, W >= 8 ? 1 : 2)
   double* En = g.E[cur ^ 1];
   const int npeak = FAM == FAM_OFFSET ? 0 : stride * g.K;
   unsigned long long trials = 0;
-  float G[PPL];  // g_b(x) of the block being swept (0 for a faulty block)
-#pragma unroll
-  for (int k = 0; k < PPL; ++k) G[k] = 0.f;
+  float* Gs = gcache + (size_t)unit * SM::NPT + u.lg;  // G[k] at Gs[k * L]: g_b(x) of the swept block
+  constexpr int L = SM::L;
 
   for (int t = 1; t <= n; ++t) {
     // Philox draws of this sweep: lane i handles components i, i+32, ...
@@ -450,10 +457,10 @@ __global__ void __launch_bounds__(W >= 8 ? 32 * W : 256, W >= 8 ? 1 : 2)
         const BlockC cb = block_consts<FAM>(th + b * stride);
         if (cb.ok) {
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) G[k] = shape<FAM>(cb, u.x(k));
+          for (int k = 0; k < PPL; ++k) Gs[k * L] = shape<FAM>(cb, u.x(k));
         } else {
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) G[k] = 0.f;
+          for (int k = 0; k < PPL; ++k) Gs[k * L] = 0.f;
         }
       }
       const double old_i = th[i];
@@ -463,21 +470,21 @@ __global__ void __launch_bounds__(W >= 8 ? 32 * W : 256, W >= 8 ? 1 : 2)
       bool accept = false;
       if (in_support) {
         ++trials;
-        // ---- trial signal Pn = P + D (the reference's BlockEvaluator::trial, energy.cpp:57-84)
-        float D[PPL];
+        // ---- trial signal Pn = P + (g_new - G) (the reference's BlockEvaluator::trial, energy.cpp:57-84)
+        float Pn[PPL];
         unsigned long long fnew = fmask;
         float dA = 0.f;
         if (FAM == FAM_OFFSET) {
           const float dv = (float)new_i - (float)old_i;
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) D[k] = dv;
+          for (int k = 0; k < PPL; ++k) Pn[k] = P[k] + dv;
         } else if (!peak) {  // Shirley endpoint: enters combine() only (block -1)
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) D[k] = 0.f;
+          for (int k = 0; k < PPL; ++k) Pn[k] = P[k];
         } else if (j == 0 && old_i != 0.0 && !((fmask >> b) & 1ull)) {  // amplitude: g' = (A'/A) g
           const float r = (float)(new_i / old_i - 1.0);
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) D[k] = r * G[k];
+          for (int k = 0; k < PPL; ++k) Pn[k] = fmaf(r, Gs[k * L], P[k]);
           dA = fabsf((float)new_i) - fabsf((float)old_i);
         } else {
           double pn[stride];
@@ -487,17 +494,14 @@ __global__ void __launch_bounds__(W >= 8 ? 32 * W : 256, W >= 8 ? 1 : 2)
           if (cn.ok) {
             fnew &= ~(1ull << b);
 #pragma unroll
-            for (int k = 0; k < PPL; ++k) D[k] = shape<FAM>(cn, u.x(k)) - G[k];
+            for (int k = 0; k < PPL; ++k) Pn[k] = P[k] + (shape<FAM>(cn, u.x(k)) - Gs[k * L]);
           } else {
             fnew |= 1ull << b;
 #pragma unroll
-            for (int k = 0; k < PPL; ++k) D[k] = -G[k];
+            for (int k = 0; k < PPL; ++k) Pn[k] = P[k] - Gs[k * L];
           }
           if (j == 0) dA = fabsf((float)new_i) - fabsf((float)old_i);
         }
-        float Pn[PPL];
-#pragma unroll
-        for (int k = 0; k < PPL; ++k) Pn[k] = P[k] + D[k];
         float bga = 0.f, bgb = 0.f;
         if (FAM == FAM_XPS) {
           bga = (float)(i == ibg ? new_i : th[ibg]);
@@ -516,13 +520,13 @@ __global__ void __launch_bounds__(W >= 8 ? 32 * W : 256, W >= 8 ? 1 : 2)
         else
           lr = -beta * nd * (e_new - e) + dlp;
         accept = lr >= 0.0 || (double)ub[i] < lr;
-        // branch-free commit: the register arrays are updated in place
-        const float af = accept ? 1.f : 0.f;
+        // commit: the register array is updated in place (select), the block cache in smem
+        if (accept && peak) {
 #pragma unroll
-        for (int k = 0; k < PPL; ++k) {
-          P[k] = accept ? Pn[k] : P[k];
-          G[k] = fmaf(af, D[k], G[k]);
+          for (int k = 0; k < PPL; ++k) Gs[k * L] += Pn[k] - P[k];
         }
+#pragma unroll
+        for (int k = 0; k < PPL; ++k) P[k] = accept ? Pn[k] : P[k];
         if (accept) {
           fmask = fnew;
           asum += dA;
@@ -572,7 +576,8 @@ cudaError_t launch_chain_t(int U, int dmax, const GroupDesc* gds, const int* lis
 // (W, PPL) pairs compiled (see pick_shape in kernels.cu)
 #define SMC_FOR_EACH_SHAPE(X) \
   X(1, 2) X(1, 4) X(1, 6) X(1, 8) X(1, 10) X(1, 12) X(1, 14) X(1, 16) \
-  X(2, 12) X(2, 14) X(2, 16) X(4, 12) X(4, 14) X(4, 16) X(8, 12) X(8, 14) X(8, 16) X(16, 12) X(16, 14) X(16, 16)
+  X(2, 12) X(2, 14) X(2, 16) X(4, 12) X(4, 14) X(4, 16) X(8, 12) X(8, 14) X(8, 16) X(16, 12) X(16, 14) X(16, 16) \
+  X(4, 8) X(8, 8) X(16, 8)
 
 template <int FAM, bool ENERGY>
 cudaError_t launch_chain_fam(const Shape& s, int dmax, const GroupDesc* gds, const int* list, const int* prefix,

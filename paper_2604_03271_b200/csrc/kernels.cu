@@ -10,6 +10,8 @@
 // Reference paths are relative to the reference root (proj/...).
 #include <cfloat>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "chain.cuh"
 
@@ -470,6 +472,15 @@ bool ppl_supported(int ppl) { return ppl >= 2 && ppl <= 16 && ppl % 2 == 0; }
 // W warps per chain, PPL points per lane; must match SMC_FOR_EACH_SHAPE (chain.cuh)
 Shape pick_shape(int64_t N) {
   Shape s;
+  if (const char* env = getenv("SPECMC_SHAPE")) {  // "W,PPL" override for tuning experiments
+    int w = 0, p = 0;
+    if (sscanf(env, "%d,%d", &w, &p) == 2 && (int64_t)32 * w * p >= N) {
+      s.W = w;
+      s.PPL = p;
+      s.U = s.W >= 8 ? 1 : 8 / s.W;
+      return s;
+    }
+  }
   if (N <= 32 * 16) {
     s.W = 1;
     s.PPL = 16;
@@ -497,7 +508,7 @@ size_t chain_smem_bytes(const Shape& s, int dmax) {
   const size_t npt = (size_t)s.PPL * 32 * s.W;
   size_t b = 16 + npt * (4 + 8 + 16) + (size_t)s.U * s.W * dpad * (8 + 8 + 4 + 4 + 4);
   b = (b + 15) & ~(size_t)15;
-  return b + (size_t)s.U * sizeof(Xch);
+  return b + (size_t)s.U * sizeof(Xch) + (size_t)s.U * npt * 4;
 }
 
 cudaError_t launch_energy(int family, const Shape& s, int dmax, const GroupDesc* gds, const int* list,
