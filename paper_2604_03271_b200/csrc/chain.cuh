@@ -99,7 +99,7 @@ struct Xch {  // per-unit cross-warp exchange, double-buffered by parity
 //   sx  float  [PPL][L]   shifted abscissa
 //   sc  float2 [PPL][L]   (c_k, h_{k+1})
 //   sy  float4 [PPL][L]   (y_k, 1/s_k, weight, 0)
-//   per warp: th f64[dpad], ls f64[dpad], acc i32[dpad], z f32[dpad], u f32[dpad]
+//   per warp: th f64, ls f64, acc i32, proposal f64, dlp f64, log u f32, flags i32  (x dpad)
 //   per unit: Xch, then G float [PPL][L] (cached g_b(x) of the block being swept)
 template <int PPL, int W>
 struct Smem {
@@ -109,7 +109,7 @@ struct Smem {
   static constexpr size_t off_c = off_x + (size_t)NPT * 4;
   static constexpr size_t off_y = off_c + (size_t)NPT * 8;
   static constexpr size_t off_w = off_y + (size_t)NPT * 16;
-  __host__ __device__ static size_t per_warp(int dpad) { return (size_t)dpad * (8 + 8 + 4 + 4 + 4); }
+  __host__ __device__ static size_t per_warp(int dpad) { return (size_t)dpad * (8 + 8 + 4 + 8 + 8 + 4 + 4); }
   __host__ __device__ static size_t bytes(int U, int dpad) {
     size_t b = off_w + (size_t)U * W * per_warp(dpad);
     b = (b + 15) & ~(size_t)15;
@@ -259,7 +259,7 @@ __device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, 
   }
   float acc = 0.f;
   if (!degen) {
-    const float scale = ba / total;
+    const float scale = ba * rcpf(total);
     const float base = fmaf(scale, prefix, bga);
 #pragma unroll
     for (int k = 0; k < PPL; ++k) {
@@ -366,8 +366,10 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   double* th = reinterpret_cast<double*>(wb);
   double* lsv = th + dpad;
   int* acc = reinterpret_cast<int*>(lsv + dpad);
-  float* zb = reinterpret_cast<float*>(acc + dpad);
-  float* ub = zb + dpad;
+  double* nvb = reinterpret_cast<double*>(acc + dpad);  // dpad is even: 8-byte aligned
+  double* dlpb = nvb + dpad;
+  float* lub = reinterpret_cast<float*>(dlpb + dpad);
+  int* flg = reinterpret_cast<int*>(lub + dpad);
   const size_t xoff = ((SM::off_w + (size_t)U * W * SM::per_warp(dpad)) + 15) & ~(size_t)15;
   Xch* xcs = reinterpret_cast<Xch*>(smem + xoff);
   float* gcache = reinterpret_cast<float*>(smem + xoff + (size_t)U * sizeof(Xch));
@@ -440,15 +442,24 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   float* Gs = gcache + (size_t)unit * SM::NPT + u.lg;  // G[k] at Gs[k * L]: g_b(x) of the swept block
   constexpr int L = SM::L;
 
+  const double bnd = beta * nd;
   for (int t = 1; t <= n; ++t) {
-    // Philox draws of this sweep: lane i handles components i, i+32, ...
+    // ---- sweep prologue, lane-parallel over components.  Component i's value
+    // and step only change at its own proposal, so the proposal, its prior
+    // check (mcmc.cpp:61-68) and the Philox draws are all fixed at sweep start.
     for (int i = lane; i < d; i += 32) {
       const u32x4 o = philox(u32x4{cg, (uint32_t)level, (uint32_t)((t - 1) * d + i), ROLE_CHAIN}, g.key0, g.key1);
-      zb[i] = normal_f32(o.x, o.y);
-      ub[i] = __logf(u01_open_lo(o.z));
+      const double old_i = th[i];
+      const double nv = old_i + (double)__expf((float)lsv[i]) * (double)normal_f32(o.x, o.y);
+      double dlp = 0.0;
+      const bool ok = prior_delta(g.pkind[i], g.pa[i], g.pb[i], old_i, nv, dlp);
+      nvb[i] = nv;
+      dlpb[i] = dlp;
+      lub[i] = __logf(u01_open_lo(o.z));
+      flg[i] = ok ? 1 : 0;
+      trials += ok ? 1 : 0;
     }
     __syncwarp();
-    const float gam = (t <= adapt_sweeps) ? exp2f(-0.6f * log2f((float)t)) : 0.f;  // t^-0.6 (mcmc.cpp:15)
     asum = amp_sum<FAM>(g, th);
     for (int i = 0; i < d; ++i) {
       const int b = i / stride, j = i - b * stride;
@@ -463,86 +474,93 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
           for (int k = 0; k < PPL; ++k) Gs[k * L] = 0.f;
         }
       }
+      if (!(flg[i] & 1)) continue;  // outside the prior support: no trial (mcmc.cpp:68)
       const double old_i = th[i];
-      const double new_i = old_i + (double)__expf((float)lsv[i]) * (double)zb[i];
-      double dlp = 0.0;
-      const bool in_support = prior_delta(g.pkind[i], g.pa[i], g.pb[i], old_i, new_i, dlp);
-      bool accept = false;
-      if (in_support) {
-        ++trials;
-        // ---- trial signal Pn = P + (g_new - G) (the reference's BlockEvaluator::trial, energy.cpp:57-84)
-        float Pn[PPL];
-        unsigned long long fnew = fmask;
-        float dA = 0.f;
-        if (FAM == FAM_OFFSET) {
-          const float dv = (float)new_i - (float)old_i;
+      const double new_i = nvb[i];
+      // ---- trial signal Pn = P + (g_new - G) (the reference's BlockEvaluator::trial, energy.cpp:57-84)
+      float Pn[PPL];
+      unsigned long long fnew = fmask;
+      float dA = 0.f;
+      if (FAM == FAM_OFFSET) {
+        const float dv = (float)new_i - (float)old_i;
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) Pn[k] = P[k] + dv;
-        } else if (!peak) {  // Shirley endpoint: enters combine() only (block -1)
+        for (int k = 0; k < PPL; ++k) Pn[k] = P[k] + dv;
+      } else if (!peak) {  // Shirley endpoint: enters combine() only (block -1)
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) Pn[k] = P[k];
-        } else if (j == 0 && old_i != 0.0 && !((fmask >> b) & 1ull)) {  // amplitude: g' = (A'/A) g
-          const float r = (float)(new_i / old_i - 1.0);
+        for (int k = 0; k < PPL; ++k) Pn[k] = P[k];
+      } else if (j == 0 && old_i != 0.0 && !((fmask >> b) & 1ull)) {  // amplitude: g' = (A'/A) g
+        const float r = (float)(new_i / old_i - 1.0);
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) Pn[k] = fmaf(r, Gs[k * L], P[k]);
-          dA = fabsf((float)new_i) - fabsf((float)old_i);
+        for (int k = 0; k < PPL; ++k) Pn[k] = fmaf(r, Gs[k * L], P[k]);
+        dA = fabsf((float)new_i) - fabsf((float)old_i);
+      } else {
+        double pn[stride];
+#pragma unroll
+        for (int q = 0; q < stride; ++q) pn[q] = (q == j) ? new_i : th[b * stride + q];
+        const BlockC cn = block_consts<FAM>(pn);
+        if (cn.ok) {
+          fnew &= ~(1ull << b);
+#pragma unroll
+          for (int k = 0; k < PPL; ++k) Pn[k] = P[k] + (shape<FAM>(cn, u.x(k)) - Gs[k * L]);
         } else {
-          double pn[stride];
+          fnew |= 1ull << b;
 #pragma unroll
-          for (int q = 0; q < stride; ++q) pn[q] = (q == j) ? new_i : th[b * stride + q];
-          const BlockC cn = block_consts<FAM>(pn);
-          if (cn.ok) {
-            fnew &= ~(1ull << b);
-#pragma unroll
-            for (int k = 0; k < PPL; ++k) Pn[k] = P[k] + (shape<FAM>(cn, u.x(k)) - Gs[k * L]);
-          } else {
-            fnew |= 1ull << b;
-#pragma unroll
-            for (int k = 0; k < PPL; ++k) Pn[k] = P[k] - Gs[k * L];
-          }
-          if (j == 0) dA = fabsf((float)new_i) - fabsf((float)old_i);
+          for (int k = 0; k < PPL; ++k) Pn[k] = P[k] - Gs[k * L];
         }
-        float bga = 0.f, bgb = 0.f;
-        if (FAM == FAM_XPS) {
-          bga = (float)(i == ibg ? new_i : th[ibg]);
-          bgb = (float)(i == ibg + 1 ? new_i : th[ibg + 1]);
-        }
-        const double e_new = fnew ? dinf() : evaluate<FAM, PPL, W>(g, u, Pn, bga, bgb, asum + dA);
-        // mcmc.cpp:72-80
-        double lr;
+        if (j == 0) dA = fabsf((float)new_i) - fabsf((float)old_i);
+      }
+      float bga = 0.f, bgb = 0.f;
+      if (FAM == FAM_XPS) {
+        bga = (float)(i == ibg ? new_i : th[ibg]);
+        bgb = (float)(i == ibg + 1 ? new_i : th[ibg + 1]);
+      }
+      const double e_new = fnew ? dinf() : evaluate<FAM, PPL, W>(g, u, Pn, bga, bgb, asum + dA);
+      // mcmc.cpp:72-80
+      const double dlp = dlpb[i];
+      double lr;
+      if (e_new < dinf() && e < dinf() && beta != 0.0) {
+        lr = fma(-bnd, e_new - e, dlp);
+      } else {
         const bool inf_new = e_new == dinf(), inf_old = e == dinf();
         if (beta == 0.0 || (inf_new && inf_old))
           lr = dlp;
         else if (inf_new)
           lr = -dinf();
-        else if (inf_old)
-          lr = dinf();
         else
-          lr = -beta * nd * (e_new - e) + dlp;
-        accept = lr >= 0.0 || (double)ub[i] < lr;
-        // commit: the register array is updated in place (select), the block cache in smem
-        if (accept && peak) {
-#pragma unroll
-          for (int k = 0; k < PPL; ++k) Gs[k * L] += Pn[k] - P[k];
-        }
-#pragma unroll
-        for (int k = 0; k < PPL; ++k) P[k] = accept ? Pn[k] : P[k];
-        if (accept) {
-          fmask = fnew;
-          asum += dA;
-          e = e_new;
-          if (lane == 0) {
-            th[i] = new_i;
-            acc[i] += 1;
-          }
-        }
+          lr = dinf();
       }
-      if (t <= adapt_sweeps && lane == 0) {  // robbins_monro_update in log space (mcmc.cpp:14-18)
-        const double ls = lsv[i] + (double)gam * ((accept ? 1.0 : 0.0) - 0.5);
+      const bool accept = lr >= 0.0 || (double)lub[i] < lr;
+      // commit: the register array is updated in place (select), the block cache in smem
+      if (accept && peak) {
+#pragma unroll
+        for (int k = 0; k < PPL; ++k) Gs[k * L] += Pn[k] - P[k];
+      }
+#pragma unroll
+      for (int k = 0; k < PPL; ++k) P[k] = accept ? Pn[k] : P[k];
+      if (accept) {
+        fmask = fnew;
+        asum += dA;
+        e = e_new;
+        if (lane == 0) {
+          th[i] = new_i;
+          flg[i] = 3;
+        }
+        __syncwarp();
+      }
+    }
+    __syncwarp();
+    // ---- sweep epilogue: tallies and Robbins-Monro in log space (mcmc.cpp:14-18, :89-93);
+    // step i is only read by component i's next proposal, so the update can wait until here
+    const float gam = (t <= adapt_sweeps) ? exp2f(-0.6f * log2f((float)t)) : 0.f;  // t^-0.6
+    for (int i = lane; i < d; i += 32) {
+      const int a = flg[i] >> 1;
+      acc[i] += a;
+      if (t <= adapt_sweeps) {
+        const double ls = lsv[i] + (double)gam * ((double)a - 0.5);
         lsv[i] = fmin(fmax(ls, kLogStepMin), kLogStepMax);
       }
-      __syncwarp();
     }
+    __syncwarp();
     const size_t slot = (size_t)c * n + (t - 1);  // smc.cpp:151
     if (wiu == 0) {
       for (int i = lane; i < d; i += 32) thn[(size_t)i * T + slot] = th[i];
@@ -554,8 +572,9 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
       g.chain_acc[(size_t)i * S + c] = acc[i];
       g.chain_ls[(size_t)i * S + c] = lsv[i];
     }
-    if (lane == 0) atomicAdd(&g.st->trials, trials);
   }
+  trials = __reduce_add_sync(0xffffffffu, (unsigned)trials);
+  if (wiu == 0 && lane == 0) atomicAdd(&g.st->trials, trials);
 }
 
 // ------------------------------------------------------------------ launch
