@@ -12,7 +12,7 @@ import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libspecmc_b200.so"
+LIB_PATH = Path(os.environ.get("SPECMC_LIB", str(PKG / "libspecmc_b200.so")))  # override: tuning experiments
 
 SPECMC_OK, SPECMC_EINVAL, SPECMC_ERUNTIME, SPECMC_ECUDA, SPECMC_ECOMM = 0, 2, 3, 4, 5
 

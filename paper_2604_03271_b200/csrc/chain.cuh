@@ -91,7 +91,7 @@ __device__ __forceinline__ float shape(const BlockC& b, float x) {
 
 struct Xch {  // per-unit cross-warp exchange, double-buffered by parity
   float scan[2][16];
-  double en[2][16];
+  int4 lim[2][16];  // energy partial sums: three fixed-point limbs + fault flag
 };
 
 // Per-CTA shared memory (dynamic):
@@ -157,19 +157,42 @@ __device__ __forceinline__ unsigned long long full_signal(const GroupDesc& g, co
   return fmask;
 }
 
-// fp64 reduction of the lane partials over the unit (identical in every warp)
+// Reduction of the lane partials over the unit, exact and order-independent:
+// each lane's fp32 partial becomes a 2^-24 fixed-point int64 split into three
+// 26-bit limbs, each summed with redux.sync (integer warp reduction, one
+// instruction instead of five dependent shuffle rounds) and then across the
+// unit's warps in int64.  Every warp obtains the identical value.  A
+// non-finite partial (the fault sentinel) or one beyond 2^38 (a state whose
+// likelihood underflows any weight) yields NaN, i.e. E = +inf.
 template <int PPL, int W>
 __device__ __forceinline__ double unit_sum(Unit<PPL, W>& u, float acc) {
-  double s = warp_sum_d((double)acc);
+  const bool bad = __any_sync(0xffffffffu, !(fabsf(acc) < 2.7e11f));
+  const long long q = bad ? 0ll : __double2ll_rn((double)acc * 16777216.0);
+  const unsigned a0 = (unsigned)(q & 0x3ffffff), a1 = (unsigned)((q >> 26) & 0x3ffffff);
+  const int a2 = (int)(q >> 52);
+  long long s0 = __reduce_add_sync(0xffffffffu, a0);
+  long long s1 = __reduce_add_sync(0xffffffffu, a1);
+  long long s2 = __reduce_add_sync(0xffffffffu, a2);
+  bool any = bad;
   if (W > 1) {
-    if (u.lane == 0) u.xc->en[u.par][u.wiu] = s;
+    if (u.lane == 0) {
+      u.xc->lim[u.par][u.wiu] = make_int4((int)s0, (int)s1, (int)s2, bad ? 1 : 0);
+    }
     u.sync();
-    s = 0.0;
+    s0 = s1 = s2 = 0;
+    any = false;
 #pragma unroll
-    for (int w = 0; w < W; ++w) s += u.xc->en[u.par][w];
+    for (int w = 0; w < W; ++w) {
+      const int4 v = u.xc->lim[u.par][w];
+      s0 += (unsigned)v.x;
+      s1 += (unsigned)v.y;
+      s2 += v.z;
+      any = any || v.w;
+    }
   }
   u.par ^= 1;
-  return s;
+  const long long tot = s0 + (s1 << 26) + (s2 << 52);
+  return any ? nan("") : (double)tot * 5.9604644775390625e-08;
 }
 
 // per-point centred NLL term, in units of 1/2 ln 2 for the hetero model:
@@ -216,13 +239,16 @@ __device__ __forceinline__ double eval_plain_nz(const GroupDesc& g, Unit<PPL, W>
 template <int PPL, int W, int NZ>
 __device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, W>& u, const float (&Pn)[PPL],
                                                   float bga, float bgb, float amp_bound) {
-  float Cn[PPL];
+  // pass 1: lane-local inclusive scan of c_k Pn_k; C_k is kept for PPL <= 16 and
+  // recomputed in pass 2 for longer lanes (register budget)
+  constexpr bool kKeepC = PPL <= 16;
+  float Cn[kKeepC ? PPL : 1];
   float run = 0.f;
 #pragma unroll
   for (int k = 0; k < PPL; ++k) {
     const float2 c = u.c(k);
     run = fmaf(c.x, Pn[k], run);
-    Cn[k] = fmaf(-c.y, Pn[k], run);
+    if (kKeepC) Cn[k] = fmaf(-c.y, Pn[k], run);
   }
   const float incl = warp_incl_scan_f(run, u.lane);
   float prefix = incl - run;
@@ -261,9 +287,18 @@ __device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, 
   if (!degen) {
     const float scale = ba * rcpf(total);
     const float base = fmaf(scale, prefix, bga);
+    float run2 = 0.f;
 #pragma unroll
     for (int k = 0; k < PPL; ++k) {
-      const float B = fmaf(scale, Cn[k], base);
+      float Ck;  // C_k = sum_{j<=k} c_j Pn_j - h_{k+1} Pn_k (lane-local part)
+      if (kKeepC) {
+        Ck = Cn[k];
+      } else {
+        const float2 c = u.c(k);
+        run2 = fmaf(c.x, Pn[k], run2);
+        Ck = fmaf(-c.y, Pn[k], run2);
+      }
+      const float B = fmaf(scale, Ck, base);
       const float4 yq = u.y(k);
       acc = fmaf(yq.z, noise_term<NZ>(g, Pn[k] + B, yq), acc);
     }
@@ -281,6 +316,9 @@ __device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, 
 template <int FAM, int PPL, int W>
 __device__ __forceinline__ double evaluate(const GroupDesc& g, Unit<PPL, W>& u, const float (&Pn)[PPL], float bga,
                                            float bgb, float amp_bound) {
+#ifdef SMC_FORCE_NZ
+  if (FAM == FAM_XPS) return eval_shirley_nz<PPL, W, SMC_FORCE_NZ>(g, u, Pn, bga, bgb, amp_bound);
+#endif
   if (FAM == FAM_XPS) {
     switch (g.noise) {
       case NZ_GAUSS: return eval_shirley_nz<PPL, W, NZ_GAUSS>(g, u, Pn, bga, bgb, amp_bound);
@@ -344,6 +382,7 @@ template <int W, int PPL>
 struct Bounds {
   static constexpr int threads = W >= 8 ? 32 * W : 256;
   static constexpr int min_blocks = (65536 / threads) / (PPL <= 8 ? 85 : 128) > 0 ? (65536 / threads) / (PPL <= 8 ? 85 : 128) : 1;
+  // (PPL = 32: 2 x 256 threads at <= 128 registers as well)
 };
 
 template <int FAM, int PPL, int W, bool ENERGY>
@@ -596,7 +635,7 @@ cudaError_t launch_chain_t(int U, int dmax, const GroupDesc* gds, const int* lis
 #define SMC_FOR_EACH_SHAPE(X) \
   X(1, 2) X(1, 4) X(1, 6) X(1, 8) X(1, 10) X(1, 12) X(1, 14) X(1, 16) \
   X(2, 12) X(2, 14) X(2, 16) X(4, 12) X(4, 14) X(4, 16) X(8, 12) X(8, 14) X(8, 16) X(16, 12) X(16, 14) X(16, 16) \
-  X(4, 8) X(8, 8) X(16, 8)
+  X(4, 8) X(8, 8) X(16, 8) X(1, 32) X(2, 32) X(4, 32)
 
 template <int FAM, bool ENERGY>
 cudaError_t launch_chain_fam(const Shape& s, int dmax, const GroupDesc* gds, const int* list, const int* prefix,
