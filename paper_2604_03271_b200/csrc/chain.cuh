@@ -51,24 +51,23 @@ __device__ __forceinline__ constexpr int block_stride() {
 //      (= A [eta exp(-ln2 d^2/s^2) + (1-eta) s^2/(s^2+d^2)], model.cpp:269-280)
 // offset: g = theta_0                              (conjugate_oracle.hpp:22-26)
 template <int FAM>
-__device__ __forceinline__ BlockC block_consts(const double* p) {
+__device__ __forceinline__ BlockC block_consts(const float* p) {  // p: fp32 shadow of the block's parameters
   BlockC c;
   c.ok = true;
   c.c3 = 0.f;
   if (FAM == FAM_GM) {
-    c.c1 = (float)p[0];
-    c.mu = (float)p[1];
-    c.c2 = (float)p[2] * -0.72134752044448170f;  // -b/2 * log2(e)
+    c.c1 = p[0];
+    c.mu = p[1];
+    c.c2 = p[2] * -0.72134752044448170f;  // -b/2 * log2(e)
   } else if (FAM == FAM_XPS) {
-    const double A = p[0], sig = p[2], eta = p[3];
-    c.ok = sig > 0.0;
-    c.mu = (float)p[1];
-    c.c1 = (float)(A * eta);
-    c.c2 = (float)(A * (1.0 - eta));
-    const float s = (float)sig;
-    c.c3 = rcpf(s * s);
+    const float A = p[0], sig = p[2], eta = p[3];
+    c.ok = sig > 0.f;
+    c.mu = p[1];
+    c.c1 = A * eta;
+    c.c2 = A - c.c1;
+    c.c3 = rcpf(sig * sig);
   } else {
-    c.c1 = (float)p[0];
+    c.c1 = p[0];
     c.mu = 0.f;
     c.c2 = 0.f;
   }
@@ -99,7 +98,8 @@ struct Xch {  // per-unit cross-warp exchange, double-buffered by parity
 //   sx  float  [PPL][L]   shifted abscissa
 //   sc  float2 [PPL][L]   (c_k, h_{k+1})
 //   sy  float4 [PPL][L]   (y_k, 1/s_k, weight, 0)
-//   per warp: th f64, ls f64, acc i32, proposal f64, dlp f64, log u f32, flags i32  (x dpad)
+//   per warp: th f64, ls f64, acc i32, proposal f64, dlp f64, log u f32, flags i32,
+//             fp32 shadows of th and of the proposal  (x dpad)
 //   per unit: Xch, then G float [PPL][L] (cached g_b(x) of the block being swept)
 template <int PPL, int W>
 struct Smem {
@@ -109,7 +109,7 @@ struct Smem {
   static constexpr size_t off_c = off_x + (size_t)NPT * 4;
   static constexpr size_t off_y = off_c + (size_t)NPT * 8;
   static constexpr size_t off_w = off_y + (size_t)NPT * 16;
-  __host__ __device__ static size_t per_warp(int dpad) { return (size_t)dpad * (8 + 8 + 4 + 8 + 8 + 4 + 4); }
+  __host__ __device__ static size_t per_warp(int dpad) { return (size_t)dpad * (8 + 8 + 4 + 8 + 8 + 4 + 4 + 4 + 4); }
   __host__ __device__ static size_t bytes(int U, int dpad) {
     size_t b = off_w + (size_t)U * W * per_warp(dpad);
     b = (b + 15) & ~(size_t)15;
@@ -138,7 +138,7 @@ struct Unit {
 // model.cpp:287-288).  Returns the bit mask of faulty blocks (eval_block
 // returning false, model.cpp:272-275): any set bit means E = +inf.
 template <int FAM, int PPL, int W>
-__device__ __forceinline__ unsigned long long full_signal(const GroupDesc& g, const double* th,
+__device__ __forceinline__ unsigned long long full_signal(const GroupDesc& g, const float* th,
                                                           const Unit<PPL, W>& u, float (&P)[PPL]) {
   constexpr int stride = block_stride<FAM>();
 #pragma unroll
@@ -370,10 +370,10 @@ __device__ __forceinline__ int find_group(const int* prefix, int n, int x) {
 }
 
 template <int FAM>
-__device__ __forceinline__ float amp_sum(const GroupDesc& g, const double* th) {
+__device__ __forceinline__ float amp_sum(const GroupDesc& g, const float* thf) {
   if (FAM != FAM_XPS) return 0.f;
   float s = 0.f;
-  for (int b = 0; b < g.K; ++b) s += fabsf((float)th[4 * b]);
+  for (int b = 0; b < g.K; ++b) s += fabsf(thf[4 * b]);
   return s;
 }
 
@@ -409,6 +409,8 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   double* dlpb = nvb + dpad;
   float* lub = reinterpret_cast<float*>(dlpb + dpad);
   int* flg = reinterpret_cast<int*>(lub + dpad);
+  float* thf = reinterpret_cast<float*>(flg + dpad);  // fp32 shadow of th (block constants)
+  float* nvf = thf + dpad;                            // fp32 shadow of the proposals
   const size_t xoff = ((SM::off_w + (size_t)U * W * SM::per_warp(dpad)) + 15) & ~(size_t)15;
   Xch* xcs = reinterpret_cast<Xch*>(smem + xoff);
   float* gcache = reinterpret_cast<float*>(smem + xoff + (size_t)U * sizeof(Xch));
@@ -448,6 +450,7 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   const int src = ENERGY ? c : g.anc[c];
   for (int i = lane; i < d; i += 32) {
     th[i] = thc[(size_t)i * T + src];
+    thf[i] = (float)th[i];
     if (!ENERGY) {
       lsv[i] = g.ls0[i];
       acc[i] = 0;
@@ -457,11 +460,11 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
 
   const int ibg = 4 * g.K;  // xps Shirley endpoints (a, b) at ibg, ibg + 1
   float P[PPL];
-  unsigned long long fmask = full_signal<FAM, PPL, W>(g, th, u, P);
-  float asum = amp_sum<FAM>(g, th);
+  unsigned long long fmask = full_signal<FAM, PPL, W>(g, thf, u, P);
+  float asum = amp_sum<FAM>(g, thf);
   double e = fmask ? dinf()
-                   : evaluate<FAM, PPL, W>(g, u, P, FAM == FAM_XPS ? (float)th[ibg] : 0.f,
-                                           FAM == FAM_XPS ? (float)th[ibg + 1] : 0.f, asum);
+                   : evaluate<FAM, PPL, W>(g, u, P, FAM == FAM_XPS ? thf[ibg] : 0.f,
+                                           FAM == FAM_XPS ? thf[ibg + 1] : 0.f, asum);
   if (ENERGY) {
     if (wiu == 0 && lane == 0) g.E[cur][c] = e;
     return;
@@ -493,18 +496,20 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
       double dlp = 0.0;
       const bool ok = prior_delta(g.pkind[i], g.pa[i], g.pb[i], old_i, nv, dlp);
       nvb[i] = nv;
+      nvf[i] = (float)nv;
+      thf[i] = (float)old_i;
       dlpb[i] = dlp;
       lub[i] = __logf(u01_open_lo(o.z));
       flg[i] = ok ? 1 : 0;
       trials += ok ? 1 : 0;
     }
     __syncwarp();
-    asum = amp_sum<FAM>(g, th);
+    asum = amp_sum<FAM>(g, thf);
     for (int i = 0; i < d; ++i) {
       const int b = i / stride, j = i - b * stride;
       const bool peak = i < npeak;
       if (FAM != FAM_OFFSET && peak && j == 0) {  // entering block b: cache g_b(x)
-        const BlockC cb = block_consts<FAM>(th + b * stride);
+        const BlockC cb = block_consts<FAM>(thf + b * stride);
         if (cb.ok) {
 #pragma unroll
           for (int k = 0; k < PPL; ++k) Gs[k * L] = shape<FAM>(cb, u.x(k));
@@ -514,28 +519,27 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
         }
       }
       if (!(flg[i] & 1)) continue;  // outside the prior support: no trial (mcmc.cpp:68)
-      const double old_i = th[i];
-      const double new_i = nvb[i];
+      const float oldf = thf[i], newf = nvf[i];
       // ---- trial signal Pn = P + (g_new - G) (the reference's BlockEvaluator::trial, energy.cpp:57-84)
       float Pn[PPL];
       unsigned long long fnew = fmask;
       float dA = 0.f;
       if (FAM == FAM_OFFSET) {
-        const float dv = (float)new_i - (float)old_i;
+        const float dv = newf - oldf;
 #pragma unroll
         for (int k = 0; k < PPL; ++k) Pn[k] = P[k] + dv;
       } else if (!peak) {  // Shirley endpoint: enters combine() only (block -1)
 #pragma unroll
         for (int k = 0; k < PPL; ++k) Pn[k] = P[k];
-      } else if (j == 0 && old_i != 0.0 && !((fmask >> b) & 1ull)) {  // amplitude: g' = (A'/A) g
-        const float r = (float)(new_i / old_i - 1.0);
+      } else if (j == 0 && oldf != 0.f && !((fmask >> b) & 1ull)) {  // amplitude: g' = (A'/A) g
+        const float r = (newf - oldf) * rcpf(oldf);
 #pragma unroll
         for (int k = 0; k < PPL; ++k) Pn[k] = fmaf(r, Gs[k * L], P[k]);
-        dA = fabsf((float)new_i) - fabsf((float)old_i);
+        dA = fabsf(newf) - fabsf(oldf);
       } else {
-        double pn[stride];
+        float pn[stride];
 #pragma unroll
-        for (int q = 0; q < stride; ++q) pn[q] = (q == j) ? new_i : th[b * stride + q];
+        for (int q = 0; q < stride; ++q) pn[q] = (q == j) ? newf : thf[b * stride + q];
         const BlockC cn = block_consts<FAM>(pn);
         if (cn.ok) {
           fnew &= ~(1ull << b);
@@ -546,12 +550,12 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
 #pragma unroll
           for (int k = 0; k < PPL; ++k) Pn[k] = P[k] - Gs[k * L];
         }
-        if (j == 0) dA = fabsf((float)new_i) - fabsf((float)old_i);
+        if (j == 0) dA = fabsf(newf) - fabsf(oldf);
       }
       float bga = 0.f, bgb = 0.f;
       if (FAM == FAM_XPS) {
-        bga = (float)(i == ibg ? new_i : th[ibg]);
-        bgb = (float)(i == ibg + 1 ? new_i : th[ibg + 1]);
+        bga = i == ibg ? newf : thf[ibg];
+        bgb = i == ibg + 1 ? newf : thf[ibg + 1];
       }
       const double e_new = fnew ? dinf() : evaluate<FAM, PPL, W>(g, u, Pn, bga, bgb, asum + dA);
       // mcmc.cpp:72-80
@@ -581,7 +585,8 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
         asum += dA;
         e = e_new;
         if (lane == 0) {
-          th[i] = new_i;
+          th[i] = nvb[i];
+          thf[i] = newf;
           flg[i] = 3;
         }
         __syncwarp();
