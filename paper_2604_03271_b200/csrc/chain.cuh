@@ -97,9 +97,11 @@ struct Xch {  // per-unit cross-warp exchange, double-buffered by parity
 //   [0,16)     mbarrier of the spectrum bulk copy
 //   sx  float  [PPL][L]   shifted abscissa
 //   sc  float2 [PPL][L]   (c_k, h_{k+1})
-//   sy  float4 [PPL][L]   (y_k, 1/s_k, weight, 0)
-//   per warp: th f64, ls f64, acc i32, proposal f64, dlp f64, log u f32, flags i32,
-//             fp32 shadows of th and of the proposal  (x dpad)
+//   sy  float2 [PPL][L]   (y_k, 1/s_k)   (20 B per point: N = 8192 fits)
+//   per unit: th f64, ls f64, acc i32, proposal f64, dlp f64, log u f32, flags i32,
+//             fp32 shadows of th and of the proposal  (x dpad); every warp of the
+//             unit computes and writes identical values (idempotent), one unit
+//             barrier per sweep orders the sweep-level rewrites
 //   per unit: Xch, then G float [PPL][L] (cached g_b(x) of the block being swept)
 template <int PPL, int W>
 struct Smem {
@@ -108,10 +110,10 @@ struct Smem {
   static constexpr size_t off_x = 16;
   static constexpr size_t off_c = off_x + (size_t)NPT * 4;
   static constexpr size_t off_y = off_c + (size_t)NPT * 8;
-  static constexpr size_t off_w = off_y + (size_t)NPT * 16;
-  __host__ __device__ static size_t per_warp(int dpad) { return (size_t)dpad * (8 + 8 + 4 + 8 + 8 + 4 + 4 + 4 + 4); }
+  static constexpr size_t off_w = off_y + (size_t)NPT * 8;
+  __host__ __device__ static size_t per_unit(int dpad) { return (size_t)dpad * (8 + 8 + 4 + 8 + 8 + 4 + 4 + 4 + 4); }
   __host__ __device__ static size_t bytes(int U, int dpad) {
-    size_t b = off_w + (size_t)U * W * per_warp(dpad);
+    size_t b = off_w + (size_t)U * per_unit(dpad);
     b = (b + 15) & ~(size_t)15;
     return b + (size_t)U * sizeof(Xch) + (size_t)U * NPT * 4;  // + per-unit block-shape cache G
   }
@@ -122,13 +124,14 @@ struct Unit {
   static constexpr int L = 32 * W;
   const float* sx;
   const float2* sc;
-  const float4* sy;
+  const float2* sy;
+  int nv;  // real (non-padding) points of this lane
   Xch* xc;
   int lg, wiu, lane, bar_id;
   int par;
   __device__ __forceinline__ float x(int k) const { return sx[k * L + lg]; }
   __device__ __forceinline__ float2 c(int k) const { return sc[k * L + lg]; }
-  __device__ __forceinline__ float4 y(int k) const { return sy[k * L + lg]; }
+  __device__ __forceinline__ float2 y(int k) const { return sy[k * L + lg]; }
   __device__ __forceinline__ void sync() const {
     if (W > 1) named_bar(bar_id, L);
   }
@@ -201,7 +204,7 @@ __device__ __forceinline__ double unit_sum(Unit<PPL, W>& u, float acc) {
 //            (hlin: the same with var linear in f)
 //   poisson: f - y - y ln(f/y)                          E = a0 + a1 * sum
 template <int NZ>
-__device__ __forceinline__ float noise_term(const GroupDesc& g, float f, float4 yq) {
+__device__ __forceinline__ float noise_term(const GroupDesc& g, float f, float2 yq) {
   const float r = yq.x - f;
   if (NZ == NZ_GAUSS) {
     return r * r;
@@ -227,8 +230,8 @@ __device__ __forceinline__ double eval_plain_nz(const GroupDesc& g, Unit<PPL, W>
   float acc = 0.f;
 #pragma unroll
   for (int k = 0; k < PPL; ++k) {
-    const float4 yq = u.y(k);
-    acc = fmaf(yq.z, noise_term<NZ>(g, Pn[k], yq), acc);
+    const float t = noise_term<NZ>(g, Pn[k], u.y(k));
+    if (k < u.nv) acc += t;
   }
   return finish_energy<NZ>(g, unit_sum(u, acc));
 }
@@ -272,7 +275,7 @@ __device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, 
     float mx = -FLT_MAX;
 #pragma unroll
     for (int k = 0; k < PPL; ++k)
-      if (u.y(k).z > 0.f) mx = fmaxf(mx, Pn[k]);
+      if (k < u.nv) mx = fmaxf(mx, Pn[k]);
     mx = warp_max_f(mx);
     if (W > 1) {
       u.sync();  // everyone has consumed scan[par] above
@@ -299,15 +302,15 @@ __device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, 
         Ck = fmaf(-c.y, Pn[k], run2);
       }
       const float B = fmaf(scale, Ck, base);
-      const float4 yq = u.y(k);
-      acc = fmaf(yq.z, noise_term<NZ>(g, Pn[k] + B, yq), acc);
+      const float t = noise_term<NZ>(g, Pn[k] + B, u.y(k));
+      if (k < u.nv) acc += t;
     }
   } else {  // linear ramp a -> b
 #pragma unroll
     for (int k = 0; k < PPL; ++k) {
       const float B = fmaf(ba, (u.x(k) - g.x0s) * g.inv_range, bga);
-      const float4 yq = u.y(k);
-      acc = fmaf(yq.z, noise_term<NZ>(g, Pn[k] + B, yq), acc);
+      const float t = noise_term<NZ>(g, Pn[k] + B, u.y(k));
+      if (k < u.nv) acc += t;
     }
   }
   return finish_energy<NZ>(g, unit_sum(u, acc));
@@ -399,9 +402,10 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   float* sx = reinterpret_cast<float*>(smem + SM::off_x);
   float2* sc = reinterpret_cast<float2*>(smem + SM::off_c);
-  float4* sy = reinterpret_cast<float4*>(smem + SM::off_y);
+  float2* sy = reinterpret_cast<float2*>(smem + SM::off_y);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wb = smem + SM::off_w + (size_t)warp * SM::per_warp(dpad);
+  const int unit = warp / W, wiu = warp - unit * W;
+  unsigned char* wb = smem + SM::off_w + (size_t)unit * SM::per_unit(dpad);
   double* th = reinterpret_cast<double*>(wb);
   double* lsv = th + dpad;
   int* acc = reinterpret_cast<int*>(lsv + dpad);
@@ -411,14 +415,14 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   int* flg = reinterpret_cast<int*>(lub + dpad);
   float* thf = reinterpret_cast<float*>(flg + dpad);  // fp32 shadow of th (block constants)
   float* nvf = thf + dpad;                            // fp32 shadow of the proposals
-  const size_t xoff = ((SM::off_w + (size_t)U * W * SM::per_warp(dpad)) + 15) & ~(size_t)15;
+  const size_t xoff = ((SM::off_w + (size_t)U * SM::per_unit(dpad)) + 15) & ~(size_t)15;
   Xch* xcs = reinterpret_cast<Xch*>(smem + xoff);
   float* gcache = reinterpret_cast<float*>(smem + xoff + (size_t)U * sizeof(Xch));
 
   // ---- stage the spectrum: cp.async.bulk (UBLKCP) completing on an mbarrier
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
-    constexpr uint32_t bx = SM::NPT * 4u, bc = SM::NPT * 8u, by = SM::NPT * 16u;
+    constexpr uint32_t bx = SM::NPT * 4u, bc = SM::NPT * 8u, by = SM::NPT * 8u;
     mbar_expect_tx(bar, bx + (FAM == FAM_XPS ? bc : 0u) + by);
     bulk_g2s(sx, g.spec_x, bx, bar);
     if (FAM == FAM_XPS) bulk_g2s(sc, g.spec_c, bc, bar);
@@ -427,7 +431,6 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   __syncthreads();
   mbar_wait(bar, 0);
 
-  const int unit = warp / W, wiu = warp - unit * W;
   const int c = cta_in_group * U + unit;
   const int units = ENERGY ? g.T : g.S;
   if (c >= units) return;  // the whole unit leaves; no CTA-wide barrier follows
@@ -442,6 +445,7 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   u.lane = lane;
   u.bar_id = 1 + unit;
   u.par = 0;
+  u.nv = min(max(g.N - u.lg * PPL, 0), PPL);
 
   const GroupState* st = g.st;
   const int cur = st->cur;
@@ -486,6 +490,7 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
 
   const double bnd = beta * nd;
   for (int t = 1; t <= n; ++t) {
+    u.sync();  // every warp of the unit is done with the previous sweep's shared arrays
     // ---- sweep prologue, lane-parallel over components.  Component i's value
     // and step only change at its own proposal, so the proposal, its prior
     // check (mcmc.cpp:61-68) and the Philox draws are all fixed at sweep start.

@@ -59,7 +59,7 @@ struct GroupDesc {  // immutable per group
   // spectrum (lane-transposed, see header)
   const float* spec_x;   // shifted abscissa x' = x - x_shift
   const float2* spec_c;  // (c_k, h_{k+1}): trapezoid weights of the Shirley scan
-  const float4* spec_y;  // (y_k, 1/s_k, weight, 0): observation, inverse noise scale, 0 on padding
+  const float2* spec_y;  // (y_k, 1/s_k): observation and inverse noise scale
   // priors (layout order, location components already shifted)
   const int* pkind;
   const double* pa;

@@ -182,7 +182,7 @@ struct Arena {
 struct PreparedSpectrum {
   std::vector<float> x;
   std::vector<float> c;  // (c_k, h_{k+1}) pairs
-  std::vector<float> y;  // (y_k, 1/s_k, weight, 0) quads
+  std::vector<float> y;  // (y_k, 1/s_k) pairs
   double x_shift = 0.0;
   float x0s = 0.f, inv_range = 0.f, range = 0.f;
   double e_a0 = 0.0, e_a1 = 0.0;
@@ -199,7 +199,7 @@ PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, 
   const size_t npt = (size_t)s.PPL * L;
   ps.x.assign(npt, 0.f);
   ps.c.assign(2 * npt, 0.f);
-  ps.y.assign(4 * npt, 0.f);
+  ps.y.assign(2 * npt, 0.f);
   ps.x_shift = x_shift;
   const double range = xs[N - 1] - xs[0];
   ps.range = (float)range;
@@ -253,7 +253,7 @@ PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, 
       break;
     }
   }
-  // padding points replicate the last real point with weight 0 (no masks in the kernel)
+  // padding points replicate the last real point; the kernel skips them by lane count
   for (size_t p = 0; p < npt; ++p) {
     const int64_t q = p < (size_t)N ? (int64_t)p : N - 1;
     const bool real = p < (size_t)N;
@@ -264,10 +264,8 @@ PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, 
     ps.x[idx] = (float)(xs[q] - x_shift);
     ps.c[2 * idx] = real ? (float)(hk + hk1) : 0.f;
     ps.c[2 * idx + 1] = real ? (float)hk1 : 0.f;
-    ps.y[4 * idx] = (float)ys[q];
-    ps.y[4 * idx + 1] = (float)inv_s[q];
-    ps.y[4 * idx + 2] = real ? 1.f : 0.f;
-    ps.y[4 * idx + 3] = 0.f;
+    ps.y[2 * idx] = (float)ys[q];
+    ps.y[2 * idx + 1] = (float)inv_s[q];
   }
   return ps;
 }
@@ -382,7 +380,7 @@ struct ClassRun {
     }
     const size_t npt = (size_t)shape.PPL * 32 * shape.W;
     size_t bytes = Arena::al(sizeof(GroupDesc) * G) + Arena::al(sizeof(GroupState) * G) + 4 * Arena::al(4 * (G + 1));
-    bytes += prep.size() * (Arena::al(npt * 4) + Arena::al(npt * 8) + Arena::al(npt * 16));
+    bytes += prep.size() * (Arena::al(npt * 4) + 2 * Arena::al(npt * 8));
     for (int r : idx) {
       const auto& R = runs[r];
       const size_t T = R.cfg.T, d = R.m.d, S = T / R.cfg.n;
@@ -401,14 +399,14 @@ struct ClassRun {
     d_prefix_all = ar.take<int>(G + 1);
     cudaStream_t st = dev.stream;
 
-    std::map<std::pair<int, double>, std::tuple<float*, float2*, float4*>> dspec;
+    std::map<std::pair<int, double>, std::tuple<float*, float2*, float2*>> dspec;
     for (auto& kv : prep) {
       float* x = ar.take<float>(npt);
       float2* c = ar.take<float2>(npt);
-      float4* y = ar.take<float4>(npt);
+      float2* y = ar.take<float2>(npt);
       h2d(x, kv.second.x.data(), npt, st);
       h2d(reinterpret_cast<float*>(c), kv.second.c.data(), 2 * npt, st);
-      h2d(reinterpret_cast<float*>(y), kv.second.y.data(), 4 * npt, st);
+      h2d(reinterpret_cast<float*>(y), kv.second.y.data(), 2 * npt, st);
       dspec[kv.first] = std::make_tuple(x, c, y);
     }
     gds.resize(G);
@@ -746,6 +744,7 @@ int specmc_smc_run(const specmc_model_desc* model, const double* xs, const doubl
                    const specmc_smc_config* cfg, specmc_smc_result* out, char* err, size_t errlen) {
   return guarded(err, errlen, [&]() -> int {
     if (!model || !cfg || !out) throw Error(SPECMC_EINVAL, "null argument");
+    std::memset(out, 0, sizeof(*out));
     specmc_problem p;
     p.model = *model;
     p.spectrum = 0;
@@ -758,7 +757,12 @@ int specmc_smc_run(const specmc_model_desc* model, const double* xs, const doubl
 
 int specmc_smc_run_batch(int32_t n_problems, const specmc_problem* problems, int32_t n_spectra,
                          const specmc_spectrum* spectra, specmc_smc_result* out, char* err, size_t errlen) {
-  return guarded(err, errlen, [&]() -> int { return run_batch(n_problems, problems, n_spectra, spectra, out, err, errlen); });
+  if (out && n_problems > 0) std::memset(out, 0, sizeof(specmc_smc_result) * (size_t)n_problems);
+  const int rc = guarded(err, errlen, [&]() -> int { return run_batch(n_problems, problems, n_spectra, spectra, out, err, errlen); });
+  if (rc != SPECMC_OK && out)  // an ABI-level failure leaves every run with that status
+    for (int i = 0; i < n_problems; ++i)
+      if (out[i].status == SPECMC_OK && !out[i].posterior) out[i].status = rc;
+  return rc;
 }
 
 int specmc_session_create(int32_t n_problems, const specmc_problem* problems, int32_t n_spectra,
@@ -841,7 +845,7 @@ int specmc_energy_batch(const specmc_model_desc* model, const double* xs, const 
     const size_t npt = ps.x.size();
     float* dx = sc.alloc<float>(npt);
     float2* dc = sc.alloc<float2>(npt);
-    float4* dy = sc.alloc<float4>(npt);
+    float2* dy = sc.alloc<float2>(npt);
     int* pk = sc.alloc<int>(d);
     double* pa = sc.alloc<double>(d);
     double* pb = sc.alloc<double>(d);
@@ -854,7 +858,7 @@ int specmc_energy_batch(const specmc_model_desc* model, const double* xs, const 
     cudaStream_t st = dev.stream;
     h2d(dx, ps.x.data(), npt, st);
     h2d(reinterpret_cast<float*>(dc), ps.c.data(), 2 * npt, st);
-    h2d(reinterpret_cast<float*>(dy), ps.y.data(), 4 * npt, st);
+    h2d(reinterpret_cast<float*>(dy), ps.y.data(), 2 * npt, st);
     h2d(pk, R.pk.data(), d, st);
     h2d(pa, R.pa.data(), d, st);
     h2d(pb, R.pb.data(), d, st);

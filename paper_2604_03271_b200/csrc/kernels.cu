@@ -503,10 +503,10 @@ Shape pick_shape(int64_t N) {
   return s;
 }
 
-size_t chain_smem_bytes(const Shape& s, int dmax) {
+size_t chain_smem_bytes(const Shape& s, int dmax) {  // must match Smem<PPL, W>::bytes (chain.cuh)
   const int dpad = (dmax + 1) & ~1;
   const size_t npt = (size_t)s.PPL * 32 * s.W;
-  size_t b = 16 + npt * (4 + 8 + 16) + (size_t)s.U * s.W * dpad * (8 + 8 + 4 + 4 + 4);
+  size_t b = 16 + npt * (4 + 8 + 8) + (size_t)s.U * dpad * (8 + 8 + 4 + 8 + 8 + 4 + 4 + 4 + 4);
   b = (b + 15) & ~(size_t)15;
   return b + (size_t)s.U * sizeof(Xch) + (size_t)s.U * npt * 4;
 }
