@@ -637,15 +637,16 @@ cudaError_t launch_chain_t(int U, int dmax, const GroupDesc* gds, const int* lis
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
-  kern<<<total_ctas, 32 * W * U, smem, st>>>(gds, list, prefix, n_list, U, dpad);
+  kern<<<total_ctas, Bounds<W, PPL>::threads, smem, st>>>(gds, list, prefix, n_list, U, dpad);
   return cudaGetLastError();
 }
 
-// (W, PPL) pairs compiled (see pick_shape in kernels.cu)
-#define SMC_FOR_EACH_SHAPE(X) \
-  X(1, 2) X(1, 4) X(1, 6) X(1, 8) X(1, 10) X(1, 12) X(1, 14) X(1, 16) \
-  X(2, 12) X(2, 14) X(2, 16) X(4, 12) X(4, 14) X(4, 16) X(8, 12) X(8, 14) X(8, 16) X(16, 12) X(16, 14) X(16, 16) \
-  X(4, 8) X(8, 8) X(16, 8) X(1, 32) X(2, 32) X(4, 32)
+// (W, PPL) pairs compiled (see pick_shape in kernels.cu): W = 1 for N <= 512,
+// W = 2 for N <= 2048, W = 4 for N <= 4096, W = 8 for N <= 8192
+#define SMC_FOR_EACH_SHAPE(X)                                                                          \
+  X(1, 2) X(1, 4) X(1, 6) X(1, 8) X(1, 10) X(1, 12) X(1, 14) X(1, 16)                                 \
+  X(2, 10) X(2, 12) X(2, 14) X(2, 16) X(2, 20) X(2, 24) X(2, 28) X(2, 32)                             \
+  X(4, 20) X(4, 24) X(4, 28) X(4, 32) X(8, 20) X(8, 24) X(8, 28) X(8, 32)
 
 template <int FAM, bool ENERGY>
 cudaError_t launch_chain_fam(const Shape& s, int dmax, const GroupDesc* gds, const int* list, const int* prefix,

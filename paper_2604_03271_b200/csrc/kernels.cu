@@ -469,37 +469,41 @@ __global__ void k_unit_predict(const double* hist, int H, int d, double beta_nex
 // ============================================================== launchers
 bool ppl_supported(int ppl) { return ppl >= 2 && ppl <= 16 && ppl % 2 == 0; }
 
-// W warps per chain, PPL points per lane; must match SMC_FOR_EACH_SHAPE (chain.cuh)
+// W warps per chain, PPL points per lane; must match SMC_FOR_EACH_SHAPE (chain.cuh).
+// Fewest warps per chain first (fewer cross-warp barriers per proposal), then
+// the smallest PPL that covers N (least padding).
 Shape pick_shape(int64_t N) {
   Shape s;
+  static const int w1[] = {2, 4, 6, 8, 10, 12, 14, 16};
+  static const int w2[] = {10, 12, 14, 16, 20, 24, 28, 32};
+  static const int w48[] = {20, 24, 28, 32};
   if (const char* env = getenv("SPECMC_SHAPE")) {  // "W,PPL" override for tuning experiments
     int w = 0, p = 0;
     if (sscanf(env, "%d,%d", &w, &p) == 2 && (int64_t)32 * w * p >= N) {
       s.W = w;
       s.PPL = p;
-      s.U = s.W >= 8 ? 1 : 8 / s.W;
+      s.U = 8 / s.W;
       return s;
     }
   }
-  if (N <= 32 * 16) {
-    s.W = 1;
-    s.PPL = 16;
-    for (int p = 2; p <= 16; p += 2)
-      if (32 * p >= N) {
-        s.PPL = p;
-        break;
-      }
+  const int* list;
+  int nl;
+  if (N <= 512) {
+    s.W = 1, list = w1, nl = 8;
+  } else if (N <= 2048) {
+    s.W = 2, list = w2, nl = 8;
+  } else if (N <= 4096) {
+    s.W = 4, list = w48, nl = 4;
   } else {
-    s.W = 2;
-    while (s.W < 16 && (int64_t)32 * s.W * 16 < N) s.W *= 2;
-    s.PPL = 16;
-    for (int p = 12; p <= 16; p += 2)
-      if ((int64_t)32 * s.W * p >= N) {
-        s.PPL = p;
-        break;
-      }
+    s.W = 8, list = w48, nl = 4;
   }
-  s.U = s.W >= 8 ? 1 : 8 / s.W;
+  s.PPL = list[nl - 1];
+  for (int i = 0; i < nl; ++i)
+    if ((int64_t)32 * s.W * list[i] >= N) {
+      s.PPL = list[i];
+      break;
+    }
+  s.U = 8 / s.W;
   return s;
 }
 

@@ -219,3 +219,15 @@ def config(name: str, T: int | None = None) -> Workload:
         data, _ = gen_xps_grid(20, 5, 8192, 5.0, 105.0, noise, margin=3.0)
         return Workload("C5", data, "xps", (1, 20), T or (1 << 18), 16, noise, 20)
     raise KeyError(name)
+
+
+def config_c4(n_spectra: int = 1024, T: int | None = None):
+    """C4: n_spectra independent gen_xps spectra (k_true = 1 + (i mod 6), seed = i;
+    SURVEY.md 8d), each fitted for K = 1..6.  Returns (spectra, k_true list, T, n)."""
+    noise = XpsHeteroNoise()
+    spectra, ks = [], []
+    for i in range(n_spectra):
+        sp, _ = gen_xps(1 + (i % 6), i, noise)
+        spectra.append(sp)
+        ks.append(1 + (i % 6))
+    return spectra, ks, T or 16384, 8

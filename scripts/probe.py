@@ -25,7 +25,33 @@ def run(name, T=None, kmax=None, seed=7):
                launches=st["kernel_launches"])
     print(json.dumps(out), flush=True)
 
+def run_c4(n_spec, T):
+    spectra, kt, T, n = syn.config_c4(n_spec, T)
+    probs = []
+    for si, sp in enumerate(spectra):
+        for K in range(1, 7):
+            probs.append((S.xps_model(K, sp), si, S.SmcConfig(T=T, n=n, seed=si)))
+    S.stats_reset()
+    t = time.perf_counter()
+    reps = S.smc_run_batch(probs, spectra, raise_on_error=False)
+    wall = time.perf_counter() - t
+    st = S.stats()
+    hits = 0
+    for si in range(len(spectra)):
+        rows = [(K, reps[6 * si + K - 1]) for K in range(1, 7) if not isinstance(reps[6 * si + K - 1], Exception)]
+        hits += S.model_select(rows).K_best == kt[si]
+    ok = [r for r in reps if not isinstance(r, Exception)]
+    props = sum(r.proposals for r in ok)
+    print(json.dumps(dict(cfg="C4", spectra=len(spectra), T=T, wall=round(wall, 3), dev=round(ok[0].device_seconds, 3),
+                          hits=hits, failed=len(reps) - len(ok), proposals=props,
+                          evals_per_s=props / ok[0].device_seconds,
+                          pt_evals_per_s_move=st["point_evals"] / (st["move_kernel_ms"] * 1e-3))), flush=True)
+
+
 if __name__ == "__main__":
     for arg in sys.argv[1:]:
         name, T = arg.split(":")
-        run(name, int(T) if T != "full" else None)
+        if name.startswith("C4x"):
+            run_c4(int(name[3:]), int(T) if T != "full" else None)
+        else:
+            run(name, int(T) if T != "full" else None)
