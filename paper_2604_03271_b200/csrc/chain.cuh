@@ -12,9 +12,9 @@
 // consecutive points [l*PPL, (l+1)*PPL) of the spectrum and keeps, in
 // registers,
 //   P[k]  committed peak signal  sum_b g_b(x)      (combine, model.cpp:287-288)
-//   G[k]  cached g_b(x) of the block being swept (shared memory, lane-transposed)
-// A proposal changes one block: the trial signal is Pn = P + g_new - G, and an
-// amplitude proposal needs no transcendental at all (Pn = P + (A'/A - 1) G).
+//   Q[k]  P minus g_b(x) of the block being swept (shared memory, lane-transposed)
+// A proposal changes one block: the trial signal is Pn = Q + g_new, and an
+// amplitude proposal needs no transcendental at all (Pn = P + (A'/A - 1)(P - Q)).
 // The Shirley background (lineshapes.hpp:65-83) needs the cumulative
 // trapezoid of Pn: C_k = sum_{j<=k} c_j Pn_j - h_{k+1} Pn_k with
 // c_j = h_j + h_{j+1}, h_j = (x_j - x_{j-1})/2, i.e. a lane-local scan and one
@@ -47,7 +47,8 @@ __device__ __forceinline__ constexpr int block_stride() {
 }
 
 // gm:  g = A exp(-b/2 (x-mu)^2) = c1 2^(c2 d^2)                   (model.cpp:216-220)
-// xps: g = c1 2^(-u) + c2 / (1 + u), u = d^2 c3, c1 = A eta, c2 = A (1-eta), c3 = 1/sigma^2
+// xps: g = c1 2^(-t^2) + c2 / (1 + t^2), t = x/sigma - mu/sigma = fma(x, c3, mu'),
+//      c1 = A eta, c2 = A (1-eta)
 //      (= A [eta exp(-ln2 d^2/s^2) + (1-eta) s^2/(s^2+d^2)], model.cpp:269-280)
 // offset: g = theta_0                              (conjugate_oracle.hpp:22-26)
 template <int FAM>
@@ -62,10 +63,10 @@ __device__ __forceinline__ BlockC block_consts(const float* p) {  // p: fp32 sha
   } else if (FAM == FAM_XPS) {
     const float A = p[0], sig = p[2], eta = p[3];
     c.ok = sig > 0.f;
-    c.mu = p[1];
+    c.c3 = rcpf(sig);
+    c.mu = -p[1] * c.c3;
     c.c1 = A * eta;
     c.c2 = A - c.c1;
-    c.c3 = rcpf(sig * sig);
   } else {
     c.c1 = p[0];
     c.mu = 0.f;
@@ -80,9 +81,8 @@ __device__ __forceinline__ float shape(const BlockC& b, float x) {
     const float d = x - b.mu;
     return b.c1 * ex2f(b.c2 * (d * d));
   } else if (FAM == FAM_XPS) {
-    const float d = x - b.mu;
-    const float u = (d * d) * b.c3;
-    return fmaf(b.c1, ex2f(-u), b.c2 * rcpf(1.0f + u));
+    const float t = fmaf(x, b.c3, b.mu);
+    return fmaf(b.c1, ex2f(-(t * t)), b.c2 * rcpf(fmaf(t, t, 1.0f)));
   } else {
     return b.c1;
   }
@@ -125,7 +125,8 @@ struct Unit {
   const float* sx;
   const float2* sc;
   const float2* sy;
-  int nv;  // real (non-padding) points of this lane
+  int nv;      // real (non-padding) points of this lane
+  float npad;  // PPL - nv
   Xch* xc;
   int lg, wiu, lane, bar_id;
   int par;
@@ -211,9 +212,12 @@ __device__ __forceinline__ float noise_term(const GroupDesc& g, float f, float2 
   } else if (NZ == NZ_HETERO) {
     const float var = fmaf(fmaf(g.nz_a1, f, g.nz_a0), f, g.nz_a2);
     return fmaf(g.nz_q, (r * r) * rcpf(var), lg2f(var * yq.y));
-  } else if (NZ == NZ_HLIN) {  // s1 = 0: var = s0^2 f + s2^2 (GaussApprox-Poisson when (1, 0, 0))
+  } else if (NZ == NZ_HLIN) {  // s1 = 0: var = s0^2 f + s2^2
     const float var = fmaf(g.nz_a0, f, g.nz_a2);
     return fmaf(g.nz_q, (r * r) * rcpf(var), lg2f(var * yq.y));
+  } else if (NZ == NZ_HPROP) {  // s1 = s2 = 0: var = s0^2 f (GaussApprox-Poisson when s0 = 1);
+                                // 1/s_k and q carry the s0^2 factor (host)
+    return fmaf(g.nz_q, (r * r) * rcpf(f), lg2f(f * yq.y));
   } else {
     return (f - yq.x) - yq.x * (kLn2 * lg2f(f * yq.y));
   }
@@ -227,13 +231,14 @@ __device__ __forceinline__ double finish_energy(const GroupDesc& g, double s) {
 
 template <int PPL, int W, int NZ>
 __device__ __forceinline__ double eval_plain_nz(const GroupDesc& g, Unit<PPL, W>& u, const float (&Pn)[PPL]) {
-  float acc = 0.f;
+  float acc = 0.f, tl = 0.f;
 #pragma unroll
   for (int k = 0; k < PPL; ++k) {
-    const float t = noise_term<NZ>(g, Pn[k], u.y(k));
-    if (k < u.nv) acc += t;
+    tl = noise_term<NZ>(g, Pn[k], u.y(k));
+    acc += tl;
   }
-  return finish_energy<NZ>(g, unit_sum(u, acc));
+  // padding points (k >= nv) replicate the lane's last point: remove them at once
+  return finish_energy<NZ>(g, unit_sum(u, fmaf(-u.npad, tl, acc)));
 }
 
 // Shirley background + energy (lineshapes.hpp:65-83, model.cpp:289-292).
@@ -286,7 +291,7 @@ __device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, 
     }
     degen = !(total > 1e-12f * mx * g.range);
   }
-  float acc = 0.f;
+  float acc = 0.f, tl = 0.f;
   if (!degen) {
     const float scale = ba * rcpf(total);
     const float base = fmaf(scale, prefix, bga);
@@ -302,18 +307,19 @@ __device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, 
         Ck = fmaf(-c.y, Pn[k], run2);
       }
       const float B = fmaf(scale, Ck, base);
-      const float t = noise_term<NZ>(g, Pn[k] + B, u.y(k));
-      if (k < u.nv) acc += t;
+      tl = noise_term<NZ>(g, Pn[k] + B, u.y(k));
+      acc += tl;
     }
   } else {  // linear ramp a -> b
 #pragma unroll
     for (int k = 0; k < PPL; ++k) {
       const float B = fmaf(ba, (u.x(k) - g.x0s) * g.inv_range, bga);
-      const float t = noise_term<NZ>(g, Pn[k] + B, u.y(k));
-      if (k < u.nv) acc += t;
+      tl = noise_term<NZ>(g, Pn[k] + B, u.y(k));
+      acc += tl;
     }
   }
-  return finish_energy<NZ>(g, unit_sum(u, acc));
+  // padding points (k >= nv, c = h = 0) replicate the lane's last point exactly
+  return finish_energy<NZ>(g, unit_sum(u, fmaf(-u.npad, tl, acc)));
 }
 
 template <int FAM, int PPL, int W>
@@ -327,6 +333,7 @@ __device__ __forceinline__ double evaluate(const GroupDesc& g, Unit<PPL, W>& u, 
       case NZ_GAUSS: return eval_shirley_nz<PPL, W, NZ_GAUSS>(g, u, Pn, bga, bgb, amp_bound);
       case NZ_HETERO: return eval_shirley_nz<PPL, W, NZ_HETERO>(g, u, Pn, bga, bgb, amp_bound);
       case NZ_HLIN: return eval_shirley_nz<PPL, W, NZ_HLIN>(g, u, Pn, bga, bgb, amp_bound);
+      case NZ_HPROP: return eval_shirley_nz<PPL, W, NZ_HPROP>(g, u, Pn, bga, bgb, amp_bound);
       default: return eval_shirley_nz<PPL, W, NZ_POISSON>(g, u, Pn, bga, bgb, amp_bound);
     }
   } else {
@@ -334,6 +341,7 @@ __device__ __forceinline__ double evaluate(const GroupDesc& g, Unit<PPL, W>& u, 
       case NZ_GAUSS: return eval_plain_nz<PPL, W, NZ_GAUSS>(g, u, Pn);
       case NZ_HETERO: return eval_plain_nz<PPL, W, NZ_HETERO>(g, u, Pn);
       case NZ_HLIN: return eval_plain_nz<PPL, W, NZ_HLIN>(g, u, Pn);
+      case NZ_HPROP: return eval_plain_nz<PPL, W, NZ_HPROP>(g, u, Pn);
       default: return eval_plain_nz<PPL, W, NZ_POISSON>(g, u, Pn);
     }
   }
@@ -446,6 +454,7 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   u.bar_id = 1 + unit;
   u.par = 0;
   u.nv = min(max(g.N - u.lg * PPL, 0), PPL);
+  u.npad = (float)(PPL - u.nv);
 
   const GroupState* st = g.st;
   const int cur = st->cur;
@@ -485,7 +494,8 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   double* En = g.E[cur ^ 1];
   const int npeak = FAM == FAM_OFFSET ? 0 : stride * g.K;
   unsigned long long trials = 0;
-  float* Gs = gcache + (size_t)unit * SM::NPT + u.lg;  // G[k] at Gs[k * L]: g_b(x) of the swept block
+  // Q[k] at Qs[k * L]: signal of every block except the one being swept (P - g_b)
+  float* Qs = gcache + (size_t)unit * SM::NPT + u.lg;
   constexpr int L = SM::L;
 
   const double bnd = beta * nd;
@@ -513,14 +523,14 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
     for (int i = 0; i < d; ++i) {
       const int b = i / stride, j = i - b * stride;
       const bool peak = i < npeak;
-      if (FAM != FAM_OFFSET && peak && j == 0) {  // entering block b: cache g_b(x)
+      if (FAM != FAM_OFFSET && peak && j == 0) {  // entering block b: Q = P - g_b(x)
         const BlockC cb = block_consts<FAM>(thf + b * stride);
         if (cb.ok) {
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) Gs[k * L] = shape<FAM>(cb, u.x(k));
+          for (int k = 0; k < PPL; ++k) Qs[k * L] = P[k] - shape<FAM>(cb, u.x(k));
         } else {
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) Gs[k * L] = 0.f;
+          for (int k = 0; k < PPL; ++k) Qs[k * L] = P[k];
         }
       }
       if (!(flg[i] & 1)) continue;  // outside the prior support: no trial (mcmc.cpp:68)
@@ -539,7 +549,7 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
       } else if (j == 0 && oldf != 0.f && !((fmask >> b) & 1ull)) {  // amplitude: g' = (A'/A) g
         const float r = (newf - oldf) * rcpf(oldf);
 #pragma unroll
-        for (int k = 0; k < PPL; ++k) Pn[k] = fmaf(r, Gs[k * L], P[k]);
+        for (int k = 0; k < PPL; ++k) Pn[k] = fmaf(r, P[k] - Qs[k * L], P[k]);
         dA = fabsf(newf) - fabsf(oldf);
       } else {
         float pn[stride];
@@ -549,11 +559,11 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
         if (cn.ok) {
           fnew &= ~(1ull << b);
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) Pn[k] = P[k] + (shape<FAM>(cn, u.x(k)) - Gs[k * L]);
+          for (int k = 0; k < PPL; ++k) Pn[k] = Qs[k * L] + shape<FAM>(cn, u.x(k));
         } else {
           fnew |= 1ull << b;
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) Pn[k] = P[k] - Gs[k * L];
+          for (int k = 0; k < PPL; ++k) Pn[k] = Qs[k * L];
         }
         if (j == 0) dA = fabsf(newf) - fabsf(oldf);
       }
@@ -578,11 +588,7 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
           lr = dinf();
       }
       const bool accept = lr >= 0.0 || (double)lub[i] < lr;
-      // commit: the register array is updated in place (select), the block cache in smem
-      if (accept && peak) {
-#pragma unroll
-        for (int k = 0; k < PPL; ++k) Gs[k * L] += Pn[k] - P[k];
-      }
+      // commit: the register array is updated in place (select); Q (other blocks) is unchanged
 #pragma unroll
       for (int k = 0; k < PPL; ++k) P[k] = accept ? Pn[k] : P[k];
       if (accept) {

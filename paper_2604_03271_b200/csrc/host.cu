@@ -235,17 +235,19 @@ PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, 
         h2 = m.s2 * m.s2;
         q = m.paper_literal ? 1.0 : 0.5;
       }
-      // device terms are lg2(var/s) + q' r^2/var with q' = q / (ln2/2)
-      ps.nz = h1 == 0.0 ? NZ_HLIN : NZ_HETERO;
+      // device terms are lg2(var/s) + q' r^2/var with q' = q / (ln2/2); with
+      // s1 = s2 = 0 (var = s0^2 f) the s0^2 factor moves into 1/s and q'
+      const bool prop = h1 == 0.0 && h2 == 0.0;
+      ps.nz = prop ? NZ_HPROP : (h1 == 0.0 ? NZ_HLIN : NZ_HETERO);
       ps.a0 = (float)h0;
       ps.a1 = (float)h1;
       ps.a2 = (float)h2;
-      ps.q = (float)(q / (0.5 * M_LN2));
+      ps.q = (float)(q / (0.5 * M_LN2) / (prop ? h0 : 1.0));
       for (int64_t i = 0; i < N; ++i) {
         const double y = std::fabs(ys[i]);
         double sc = h0 * y + h1 * y * y + h2;
         if (!(sc > 0.0)) sc = 1.0;
-        inv_s[i] = 1.0 / sc;
+        inv_s[i] = (prop ? h0 : 1.0) / sc;
         a0 += 0.5 * std::log(2.0 * M_PI * sc);
       }
       ps.e_a0 = a0 / (double)N;

@@ -2,6 +2,7 @@
 import sys, time, json
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import subprocess
 import numpy as np
 import paper_2604_03271_b200 as S
 from paper_2604_03271_b200 import synthetic as syn
@@ -48,7 +49,16 @@ def run_c4(n_spec, T):
                           pt_evals_per_s_move=st["point_evals"] / (st["move_kernel_ms"] * 1e-3))), flush=True)
 
 
+def clocks():
+    try:
+        return subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm,power.draw,temperature.gpu,clocks_event_reasons.active",
+                               "--format=csv,noheader"], capture_output=True, text=True, timeout=10).stdout.strip()
+    except Exception:
+        return "?"
+
+
 if __name__ == "__main__":
+    print("clocks before:", clocks(), flush=True)
     for arg in sys.argv[1:]:
         name, T = arg.split(":")
         if name.startswith("C4x"):
