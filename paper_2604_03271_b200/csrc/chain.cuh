@@ -103,6 +103,11 @@ struct Xch {  // per-unit cross-warp exchange, double-buffered by parity
 //             unit computes and writes identical values (idempotent), one unit
 //             barrier per sweep orders the sweep-level rewrites
 //   per unit: Xch, then G float [PPL][L] (cached g_b(x) of the block being swept)
+// committed peak signal P: registers, except for W == 4 where shared memory was
+// measured faster (register pressure); chosen per shape
+template <int W>
+__host__ __device__ constexpr bool p_in_smem() { return W == 4; }
+
 template <int PPL, int W>
 struct Smem {
   static constexpr int L = 32 * W;
@@ -115,7 +120,7 @@ struct Smem {
   __host__ __device__ static size_t bytes(int U, int dpad) {
     size_t b = off_w + (size_t)U * per_unit(dpad);
     b = (b + 15) & ~(size_t)15;
-    return b + (size_t)U * sizeof(Xch) + (size_t)U * NPT * 4;  // + per-unit block-shape cache G
+    return b + (size_t)U * sizeof(Xch) + (size_t)U * NPT * (p_in_smem<W>() ? 8 : 4);  // + caches Q (and P)
   }
 };
 
@@ -426,6 +431,7 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   const size_t xoff = ((SM::off_w + (size_t)U * SM::per_unit(dpad)) + 15) & ~(size_t)15;
   Xch* xcs = reinterpret_cast<Xch*>(smem + xoff);
   float* gcache = reinterpret_cast<float*>(smem + xoff + (size_t)U * sizeof(Xch));
+  float* pcache = gcache + (size_t)U * SM::NPT;
 
   // ---- stage the spectrum: cp.async.bulk (UBLKCP) completing on an mbarrier
   if (threadIdx.x == 0) {
@@ -496,7 +502,15 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   unsigned long long trials = 0;
   // Q[k] at Qs[k * L]: signal of every block except the one being swept (P - g_b)
   float* Qs = gcache + (size_t)unit * SM::NPT + u.lg;
+  // committed peak signal: registers, or shared memory (Ps[k * L]) when p_in_smem<W>()
+  constexpr bool kPsm = p_in_smem<W>();
+  float* Ps = pcache + (size_t)unit * SM::NPT + u.lg;
   constexpr int L = SM::L;
+  if (kPsm) {
+#pragma unroll
+    for (int k = 0; k < PPL; ++k) Ps[k * L] = P[k];
+  }
+#define SMC_P(k) (kPsm ? Ps[(k) * L] : P[k])
 
   const double bnd = beta * nd;
   for (int t = 1; t <= n; ++t) {
@@ -527,10 +541,10 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
         const BlockC cb = block_consts<FAM>(thf + b * stride);
         if (cb.ok) {
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) Qs[k * L] = P[k] - shape<FAM>(cb, u.x(k));
+          for (int k = 0; k < PPL; ++k) Qs[k * L] = SMC_P(k) - shape<FAM>(cb, u.x(k));
         } else {
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) Qs[k * L] = P[k];
+          for (int k = 0; k < PPL; ++k) Qs[k * L] = SMC_P(k);
         }
       }
       if (!(flg[i] & 1)) continue;  // outside the prior support: no trial (mcmc.cpp:68)
@@ -542,14 +556,17 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
       if (FAM == FAM_OFFSET) {
         const float dv = newf - oldf;
 #pragma unroll
-        for (int k = 0; k < PPL; ++k) Pn[k] = P[k] + dv;
+        for (int k = 0; k < PPL; ++k) Pn[k] = SMC_P(k) + dv;
       } else if (!peak) {  // Shirley endpoint: enters combine() only (block -1)
 #pragma unroll
-        for (int k = 0; k < PPL; ++k) Pn[k] = P[k];
+        for (int k = 0; k < PPL; ++k) Pn[k] = SMC_P(k);
       } else if (j == 0 && oldf != 0.f && !((fmask >> b) & 1ull)) {  // amplitude: g' = (A'/A) g
         const float r = (newf - oldf) * rcpf(oldf);
 #pragma unroll
-        for (int k = 0; k < PPL; ++k) Pn[k] = fmaf(r, P[k] - Qs[k * L], P[k]);
+        for (int k = 0; k < PPL; ++k) {
+          const float pk = SMC_P(k);
+          Pn[k] = fmaf(r, pk - Qs[k * L], pk);
+        }
         dA = fabsf(newf) - fabsf(oldf);
       } else {
         float pn[stride];
@@ -588,10 +605,16 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
           lr = dinf();
       }
       const bool accept = lr >= 0.0 || (double)lub[i] < lr;
-      // commit: the register array is updated in place (select); Q (other blocks) is unchanged
+      // commit: Q (other blocks) is unchanged; P updated in place (select) or in shared memory
+      if (!kPsm) {
 #pragma unroll
-      for (int k = 0; k < PPL; ++k) P[k] = accept ? Pn[k] : P[k];
+        for (int k = 0; k < PPL; ++k) P[k] = accept ? Pn[k] : P[k];
+      }
       if (accept) {
+        if (kPsm) {
+#pragma unroll
+          for (int k = 0; k < PPL; ++k) Ps[k * L] = Pn[k];
+        }
         fmask = fnew;
         asum += dA;
         e = e_new;
@@ -628,6 +651,7 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
       g.chain_ls[(size_t)i * S + c] = lsv[i];
     }
   }
+#undef SMC_P
   trials = __reduce_add_sync(0xffffffffu, (unsigned)trials);
   if (wiu == 0 && lane == 0) atomicAdd(&g.st->trials, trials);
 }
