@@ -48,6 +48,8 @@ enum specmc_prior { SPECMC_PRIOR_NORMAL = 0, SPECMC_PRIOR_GAMMA = 1, SPECMC_PRIO
  * d = model_dim(spec) in the reference layout order (model.hpp:43-49):
  *   gm:  (A_k, mu_k, b_k) per peak                 d = 3K
  *   xps: (A_k, mu_k, sigma_k, eta_k) per peak, a, b d = 4K + 2
+ *   xrd: (A, d2t, r, alpha, u, v, w, s, t) per phase,
+ *        then (bg_a, bg_sigma, bg_r, bg_b)          d = 9K + 4
  *   offset: (theta)                                d = 1
  * Normal(a = mean, b = var), Gamma(a = shape, b = rate), Uniform(a = lo, b = hi). */
 typedef struct {
@@ -61,6 +63,12 @@ typedef struct {
   const int32_t* prior_kind;
   const double* prior_a;
   const double* prior_b;
+  /* xrd only: reflection list of every phase (PhaseRef, model.hpp:25-32),
+   * grouped by phase in phase order: phase index, mu_ref (deg 2theta), rel. intensity */
+  int32_t n_refl;
+  const int32_t* refl_phase;
+  const double* refl_mu;
+  const double* refl_int;
 } specmc_model_desc;
 
 /* SmcConfig (proj/include/specmc/smc.hpp:12-19) plus the device ordinal. */

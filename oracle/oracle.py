@@ -44,6 +44,7 @@ class _Model(C.Structure):
         ("paper_literal", C.c_int),
         ("prior_kind", _ip), ("prior_a", _dp), ("prior_b", _dp),
         ("xs", _dp), ("ys", _dp), ("n", C.c_int64),
+        ("n_refl", C.c_int), ("refl_phase", _ip), ("refl_mu", _dp), ("refl_int", _dp),
     ]
 
 
@@ -66,14 +67,21 @@ class OracleModel:
     s1: float = 0.01
     s2: float = 0.0
     paper_literal: bool = False
+    refl_phase: np.ndarray = None  # xrd: phase index of every reflection (phase order)
+    refl_mu: np.ndarray = None
+    refl_int: np.ndarray = None
 
     def struct(self):
+        rp = np.ascontiguousarray(self.refl_phase if self.refl_phase is not None else [0], dtype=np.int32)
+        rm = _d(self.refl_mu if self.refl_mu is not None else [0.0])
+        ri = _d(self.refl_int if self.refl_int is not None else [0.0])
+        nr = 0 if self.refl_phase is None else len(self.refl_phase)
         self._keep = [np.ascontiguousarray(self.prior_kind, dtype=np.int32), _d(self.prior_a), _d(self.prior_b),
-                      _d(self.xs), _d(self.ys)]
-        pk, pa, pb, xs, ys = self._keep
+                      _d(self.xs), _d(self.ys), rp, rm, ri]
+        pk, pa, pb, xs, ys = self._keep[:5]
         return _Model(FAMILY[self.family], self.K, len(pk), NOISE[self.noise], self.sigma, self.s0, self.s1,
                       self.s2, int(self.paper_literal), _ptr(pk, _ip), _ptr(pa), _ptr(pb), _ptr(xs), _ptr(ys),
-                      len(xs))
+                      len(xs), nr, _ptr(rp, _ip), _ptr(rm), _ptr(ri))
 
     @property
     def d(self):
@@ -285,6 +293,8 @@ class Ref:
         L.ref_gen_xps.argtypes = [C.c_int, C.c_uint64, C.c_double, C.c_double, C.c_double, _dp, _dp]
         L.ref_xps_model_priors.argtypes = [C.c_int, _dp, _dp, C.c_int64, _ip, _dp, _dp]
         L.ref_gm_model_priors.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, C.c_int, _ip, _dp, _dp]
+        L.ref_xrd_model_priors.argtypes = [C.c_int, C.c_int, _ip, _dp, _dp, _dp, _dp, C.c_int64, _ip, _dp, _dp]
+        L.ref_gen_xrd.argtypes = [C.c_int64, C.c_uint64, _dp, _dp]
         L.ref_model_select.argtypes = [C.c_int, _ip, _dp, _ip, _ip]
         L.ref_trial_seed.restype = C.c_uint64
         L.ref_trial_seed.argtypes = [C.c_uint64, C.c_int]
@@ -395,6 +405,23 @@ class Ref:
         pa, pb = np.empty(d), np.empty(d)
         self.lib.ref_gm_model_priors(K, x_lo, x_hi, sigma, int(uniform_mu), _ptr(pk, _ip), _ptr(pa), _ptr(pb))
         return pk, pa, pb
+
+    def xrd_model_priors(self, K, refl_phase, refl_mu, refl_int, xs, ys):
+        rp = np.ascontiguousarray(refl_phase, dtype=np.int32)
+        rm, ri, xs, ys = _d(refl_mu), _d(refl_int), _d(xs), _d(ys)
+        d = 9 * K + 4
+        pk = np.empty(d, dtype=np.int32)
+        pa, pb = np.empty(d), np.empty(d)
+        self.lib.ref_xrd_model_priors(K, len(rp), _ptr(rp, _ip), _ptr(rm), _ptr(ri), _ptr(xs), _ptr(ys), len(xs),
+                                      _ptr(pk, _ip), _ptr(pa), _ptr(pb))
+        return pk, pa, pb
+
+    def gen_xrd(self, n_points, seed):
+        xs, ys = np.empty(n_points), np.empty(n_points)
+        rc = self.lib.ref_gen_xrd(n_points, seed, _ptr(xs), _ptr(ys))
+        if rc:
+            raise OracleError(rc, "gen_xrd")
+        return xs, ys
 
     def model_select(self, ks, fs, diverged) -> int:
         ks = np.ascontiguousarray(ks, dtype=np.int32)

@@ -23,7 +23,7 @@ using namespace specmc;
 
 namespace {
 
-enum { FAM_GM = 0, FAM_XPS = 1, FAM_OFFSET = 3 };
+enum { FAM_GM = 0, FAM_XPS = 1, FAM_XRD = 2, FAM_OFFSET = 3 };
 
 PriorSpec make_prior(int kind, double a, double b) {
   if (kind == 0) return NormalPrior{a, b};
@@ -40,14 +40,37 @@ NoiseSpec make_noise(int kind, double sigma, double s0, double s1, double s2, in
   }
 }
 
-// layout names exactly as gm_model / xps_model write them (model.cpp:121-189)
+std::vector<PhaseRef> make_phases(int K, int n_refl, const int* ph, const double* mu, const double* ri) {
+  std::vector<PhaseRef> phases(K);
+  for (int k = 0; k < K; ++k) phases[k].name = "phase" + std::to_string(k + 1);
+  for (int q = 0; q < n_refl; ++q) phases[ph[q]].reflections.push_back(Reflection{mu[q], ri[q]});
+  return phases;
+}
+
+// layout names exactly as gm_model / xps_model / xrd_model write them (model.cpp:121-189)
 ModelSpec make_spec(int family, int K, const int* pk, const double* pa, const double* pb,
-                    NoiseSpec noise) {
+                    NoiseSpec noise, int n_refl = 0, const int* ph = nullptr, const double* mu = nullptr,
+                    const double* ri = nullptr) {
   ModelSpec s;
-  s.family = family == FAM_GM ? Family::GaussianMixture : Family::XpsShirley;
+  s.family = family == FAM_GM ? Family::GaussianMixture
+                              : (family == FAM_XRD ? Family::XrdPseudoVoigt : Family::XpsShirley);
   s.K = K;
   s.noise = noise;
   int i = 0;
+  if (family == FAM_XRD) {
+    s.phases = make_phases(K, n_refl, ph, mu, ri);
+    for (int k = 1; k <= K; ++k)
+      for (const char* stem : {"A", "d2t", "r", "alpha", "u", "v", "w", "s", "t"}) {
+        s.layout.push_back({std::string(stem) + std::to_string(k), make_prior(pk[i], pa[i], pb[i])});
+        ++i;
+      }
+    for (const char* nm : {"bg_a", "bg_sigma", "bg_r", "bg_b"}) {
+      s.layout.push_back({nm, make_prior(pk[i], pa[i], pb[i])});
+      ++i;
+    }
+    validate_model(s);
+    return s;
+  }
   for (int k = 1; k <= K; ++k) {
     if (family == FAM_GM) {
       for (const char* stem : {"A", "mu", "b"}) {
@@ -112,7 +135,16 @@ typedef struct {
   const double* xs;
   const double* ys;
   int64_t n;
+  int n_refl;
+  const int* refl_phase;
+  const double* refl_mu;
+  const double* refl_int;
 } ref_model;
+
+#define REF_SPEC(m)                                                                                          \
+  make_spec((m)->family, (m)->K, (m)->prior_kind, (m)->prior_a, (m)->prior_b,                               \
+            make_noise((m)->noise, (m)->sigma, (m)->s0, (m)->s1, (m)->s2, (m)->paper_literal), (m)->n_refl, \
+            (m)->refl_phase, (m)->refl_mu, (m)->refl_int)
 
 typedef struct {
   double F;
@@ -134,16 +166,14 @@ double ref_energy(const ref_model* m, const double* theta) {
     th[0] = theta[0];
     return p.energy(th);
   }
-  ModelSpec spec = make_spec(m->family, m->K, m->prior_kind, m->prior_a, m->prior_b,
-                             make_noise(m->noise, m->sigma, m->s0, m->s1, m->s2, m->paper_literal));
+  ModelSpec spec = REF_SPEC(m);
   VectorXd th(theta, m->d);
   return energy(spec, th, make_data(m->xs, m->ys, m->n));
 }
 
 int ref_forward(const ref_model* m, const double* theta, double* f_out, char* err, size_t errlen) {
   try {
-    ModelSpec spec = make_spec(m->family, m->K, m->prior_kind, m->prior_a, m->prior_b,
-                               make_noise(m->noise, m->sigma, m->s0, m->s1, m->s2, m->paper_literal));
+    ModelSpec spec = REF_SPEC(m);
     VectorXd th(theta, m->d);
     ArrayXd f = model_forward(spec, th, ArrayXd(m->xs, m->n));
     std::memcpy(f_out, f.data(), sizeof(double) * static_cast<size_t>(m->n));
@@ -249,9 +279,7 @@ int ref_smc_run(const ref_model* m, int64_t T, int n, double ess_target, int max
       post = std::move(r.thetas);
       energies = std::move(r.energies);
     } else {
-      ModelSpec spec =
-          make_spec(m->family, m->K, m->prior_kind, m->prior_a, m->prior_b,
-                    make_noise(m->noise, m->sigma, m->s0, m->s1, m->s2, m->paper_literal));
+      ModelSpec spec = REF_SPEC(m);
       RunReport r = smc_run(spec, make_data(m->xs, m->ys, m->n), cfg);
       out->F = r.F;
       out->diverged = r.diverged;
@@ -307,6 +335,31 @@ int ref_xps_model_priors(int K, const double* xs, const double* ys, int64_t n, i
     else { auto& u = std::get<UniformPrior>(p); pk[i] = 2; pa[i] = u.lo; pb[i] = u.hi; }
   }
   return static_cast<int>(s.layout.size());
+}
+
+// xrd_model(phases, data, noise) priors (model.cpp:138-167)
+int ref_xrd_model_priors(int K, int n_refl, const int* ph, const double* mu, const double* ri, const double* xs,
+                         const double* ys, int64_t n, int* pk, double* pa, double* pb) {
+  ModelSpec s = xrd_model(make_phases(K, n_refl, ph, mu, ri), make_data(xs, ys, n), PoissonNoise{});
+  for (size_t i = 0; i < s.layout.size(); ++i) {
+    const auto& p = s.layout[i].prior;
+    if (auto* a = std::get_if<NormalPrior>(&p)) { pk[i] = 0; pa[i] = a->mean; pb[i] = a->var; }
+    else if (auto* g = std::get_if<GammaPrior>(&p)) { pk[i] = 1; pa[i] = g->shape; pb[i] = g->rate; }
+    else { auto& u = std::get<UniformPrior>(p); pk[i] = 2; pa[i] = u.lo; pb[i] = u.hi; }
+  }
+  return static_cast<int>(s.layout.size());
+}
+
+// gen_xrd(n_points, seed) (synthetic.cpp:230-268): three TiO2 phases, Poisson counts
+int ref_gen_xrd(int64_t n_points, uint64_t seed, double* xs, double* ys) {
+  try {
+    SyntheticDataset ds = gen_xrd(n_points, seed);
+    std::memcpy(xs, ds.data.xs.data(), sizeof(double) * static_cast<size_t>(n_points));
+    std::memcpy(ys, ds.data.ys.data(), sizeof(double) * static_cast<size_t>(n_points));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, nullptr, 0);
+  }
 }
 
 int ref_gm_model_priors(int K, double x_lo, double x_hi, double sigma, int uniform_mu, int* pk,

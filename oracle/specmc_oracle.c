@@ -192,12 +192,20 @@ typedef struct {
   const double* xs;
   const double* ys;
   int64_t n;
+  /* xrd: reflections of every phase, grouped by phase in phase order */
+  int n_refl;
+  const int* refl_phase;
+  const double* refl_mu;
+  const double* refl_int;
 } orc_model;
 
 static int n_blocks(const orc_model* m) {
   if (m->family == ORC_OFFSET) return 1;
+  if (m->family == ORC_XRD) return m->K + 1; /* phases + background (model.cpp:198-202) */
   return m->K;
 }
+
+static const double kFourLn2 = 2.772588722239781237668928485832706272302; /* lineshapes.hpp:11 */
 
 /* model.cpp:213-283, gm and xps branches; lineshapes.hpp:54-59.  Returns 0 on
  * an evaluation fault (E = +inf). */
@@ -224,6 +232,45 @@ static int eval_block(const orc_model* m, int b, const double* th, double* out) 
       double d2 = dx * dx;
       double g = exp(cg * d2);
       out[i] = A * (eta * g + lnum / (s2 + d2));
+    }
+    return 1;
+  }
+  if (m->family == ORC_XRD) {
+    if (b == m->K) { /* background block (model.cpp:223-234) */
+      const int off = 9 * m->K;
+      const double a = th[off], sbg = th[off + 1], rbg = th[off + 2], bg = th[off + 3];
+      if (!(sbg > 0.0)) return 0;
+      for (int64_t i = 0; i < n; ++i) {
+        double t = xs[i] / sbg;
+        double t2 = t * t;
+        out[i] = a * ((1.0 - rbg) * exp((-kFourLn2) * t2) + rbg / (1.0 + 4.0 * t2)) + bg;
+      }
+      return 1;
+    }
+    /* phase block (model.cpp:235-267) */
+    const int off = 9 * b;
+    const double A = th[off], d2t = th[off + 1], r = th[off + 2], alpha = th[off + 3], u = th[off + 4],
+                 v = th[off + 5], w = th[off + 6], s = th[off + 7], t = th[off + 8];
+    const double deg2rad = M_PI / 180.0;
+    for (int64_t i = 0; i < n; ++i) out[i] = 0.0;
+    for (int q = 0; q < m->n_refl; ++q) {
+      if (m->refl_phase[q] != b) continue;
+      const double c = m->refl_mu[q] + d2t;
+      const double half = 0.5 * c * deg2rad;
+      const double tn = tan(half);
+      const double disc = u * tn * tn - v * tn + w;
+      if (!(disc > 0.0)) return 0;
+      const double sig0 = sqrt(disc);
+      const double om0 = s / cos(half) + t * tn;
+      if (!(om0 > 0.0)) return 0;
+      const double amp = A * m->refl_int[q];
+      const double gh = alpha * sig0, lh = alpha * om0;
+      for (int64_t i = 0; i < n; ++i) {
+        const double dx = xs[i] - c;
+        const double wg = dx >= 0.0 ? dx / gh : dx / sig0;
+        const double wl = dx >= 0.0 ? dx / lh : dx / om0;
+        out[i] += amp * ((1.0 - r) * exp((-kFourLn2) * (wg * wg)) + r / (1.0 + 4.0 * (wl * wl)));
+      }
     }
     return 1;
   }

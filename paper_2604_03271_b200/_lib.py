@@ -24,7 +24,8 @@ _lp = C.POINTER(C.c_int64)
 class ModelDesc(C.Structure):
     _fields_ = [("family", C.c_int32), ("K", C.c_int32), ("d", C.c_int32), ("noise", C.c_int32),
                 ("noise_sigma", C.c_double), ("s0", C.c_double), ("s1", C.c_double), ("s2", C.c_double),
-                ("paper_literal", C.c_int32), ("prior_kind", _ip), ("prior_a", _dp), ("prior_b", _dp)]
+                ("paper_literal", C.c_int32), ("prior_kind", _ip), ("prior_a", _dp), ("prior_b", _dp),
+                ("n_refl", C.c_int32), ("refl_phase", _ip), ("refl_mu", _dp), ("refl_int", _dp)]
 
 
 class SmcConfigC(C.Structure):

@@ -43,6 +43,19 @@ struct GroupState {  // mutable per-group scalars; read back by the host every r
   unsigned long long trials;
 };
 
+// Grid-level tempering state of one group (multi-CTA path, k_tp_*): the
+// bisection state machine of next_beta, slice partial sums and the slice
+// offsets of the grid-level CDF scan.
+constexpr int kMaxSlices = 512;
+struct TemperScratch {
+  double emin, lo, hi, full, beta_next;
+  double m, lse, u;
+  int it, done, err, pad;
+  unsigned int counter, pad2;
+  double part[kMaxSlices][2];
+  double offs[kMaxSlices + 1];
+};
+
 struct GroupDesc {  // immutable per group
   int family, K, d, noise;
   int T, n, S, max_levels;
@@ -75,6 +88,10 @@ struct GroupDesc {  // immutable per group
   double* hist;
   double* diag;
   GroupState* st;
+  TemperScratch* ts;  // grid-level tempering (large T)
+  int nslices;        // slices of the grid-level tempering (0: single-CTA path)
+  int slice_len;
+  double* stat_acc;   // [d] per-component accept sums of the level (k_stats_grid)
 };
 
 // ----------------------------------------------------------------- Philox4x32-10

@@ -122,6 +122,9 @@ void validate_spectrum(const double* xs, const double* ys, int64_t n, bool nonne
 }
 
 // location parameters (peak centres mu_k) are shifted by x_shift on the device
+// populations above this use the grid-level (multi-CTA) tempering kernels
+constexpr size_t kGridTemperT = (size_t)1 << 17;
+
 bool is_location(int family, int K, int i) {
   if (family == SPECMC_FAMILY_GM) return i % 3 == 1;
   if (family == SPECMC_FAMILY_XPS) return i < 4 * K && i % 4 == 1;
@@ -343,6 +346,8 @@ struct ClassRun {
   GroupDesc* d_gds = nullptr;
   GroupState* d_st = nullptr;
   int *d_list = nullptr, *d_prefix = nullptr, *d_list_all = nullptr, *d_prefix_all = nullptr;
+  int *d_list_small = nullptr, *d_list_big = nullptr;
+  int max_slices = 0;
   std::vector<GroupDesc> gds;
   std::vector<int> order;
   GroupState* h_st = nullptr;
@@ -381,7 +386,7 @@ struct ClassRun {
       }
     }
     const size_t npt = (size_t)shape.PPL * 32 * shape.W;
-    size_t bytes = Arena::al(sizeof(GroupDesc) * G) + Arena::al(sizeof(GroupState) * G) + 4 * Arena::al(4 * (G + 1));
+    size_t bytes = Arena::al(sizeof(GroupDesc) * G) + Arena::al(sizeof(GroupState) * G) + 6 * Arena::al(4 * (G + 1));
     bytes += prep.size() * (Arena::al(npt * 4) + 2 * Arena::al(npt * 8));
     for (int r : idx) {
       const auto& R = runs[r];
@@ -391,6 +396,8 @@ struct ClassRun {
       bytes += Arena::al(S * 4) + Arena::al(d * S * 4) + Arena::al(d * S * 8);
       bytes += Arena::al(T * 8) + Arena::al(kHist * (1 + 2 * d) * 8);
       bytes += Arena::al((size_t)R.cfg.max_levels * 4 * 8);
+      bytes += Arena::al(d * 8);                                                // stat_acc
+      if (T > kGridTemperT) bytes += Arena::al(sizeof(TemperScratch));         // grid tempering
     }
     ar.reserve(bytes);
     d_gds = ar.take<GroupDesc>(G);
@@ -399,6 +406,8 @@ struct ClassRun {
     d_prefix = ar.take<int>(G + 1);
     d_list_all = ar.take<int>(G + 1);
     d_prefix_all = ar.take<int>(G + 1);
+    d_list_small = ar.take<int>(G + 1);
+    d_list_big = ar.take<int>(G + 1);
     cudaStream_t st = dev.stream;
 
     std::map<std::pair<int, double>, std::tuple<float*, float2*, float2*>> dspec;
@@ -469,6 +478,16 @@ struct ClassRun {
       g.hist = ar.take<double>(kHist * (1 + 2 * d));
       g.diag = ar.take<double>((size_t)R.cfg.max_levels * 4);
       g.st = d_st + gi;
+      g.stat_acc = ar.take<double>(d);
+      if (T > kGridTemperT) {  // grid-level tempering: slices of <= 512 x slice_len particles
+        g.ts = ar.take<TemperScratch>(1);
+        size_t sl = std::max<size_t>(32768, (T + kMaxSlices - 1) / kMaxSlices);
+        sl = (sl + 1023) & ~(size_t)1023;
+        g.slice_len = (int)sl;
+        g.nslices = (int)((T + sl - 1) / sl);
+        max_slices = std::max(max_slices, g.nslices);
+        cuda_check(cudaMemsetAsync(g.ts, 0, sizeof(TemperScratch), st), "memset");
+      }
     }
     h2d(d_gds, gds.data(), G, st);
     // longest chains first (d descending) so the move grid drains in LPT order
@@ -476,7 +495,7 @@ struct ClassRun {
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return gds[a].d > gds[b].d; });
     cuda_check(cudaMallocHost(&h_st, sizeof(GroupState) * G), "cudaMallocHost");
-    cuda_check(cudaMallocHost(&h_list, sizeof(int) * 2 * (G + 1)), "cudaMallocHost");
+    cuda_check(cudaMallocHost(&h_list, sizeof(int) * 4 * (G + 1)), "cudaMallocHost");
     dev.sync();
   }
 
@@ -520,16 +539,29 @@ struct ClassRun {
     while (!active.empty()) {
       total = build_list(active, false, list, prefix);
       const int na = (int)list.size();
+      std::vector<int> small, big;
+      for (int gi : active) (gds[gi].nslices > 0 ? big : small).push_back(gi);
       dev.sync();  // h_list is reused: the previous round's copies must be done
       std::memcpy(h_list, list.data(), sizeof(int) * na);
       std::memcpy(h_list + (G + 1), prefix.data(), sizeof(int) * (na + 1));
+      std::copy(small.begin(), small.end(), h_list + 2 * (G + 1));
+      std::copy(big.begin(), big.end(), h_list + 3 * (G + 1));
       h2d(d_list, h_list, na, st);
       h2d(d_prefix, h_list + (G + 1), na + 1, st);
-      cuda_check(launch_temper(d_gds, d_list, na, st), "k_temper");
+      if (!small.empty()) {
+        h2d(d_list_small, h_list + 2 * (G + 1), small.size(), st);
+        cuda_check(launch_temper(d_gds, d_list_small, (int)small.size(), st), "k_temper");
+        count_launch(1);
+      }
+      if (!big.empty()) {
+        h2d(d_list_big, h_list + 3 * (G + 1), big.size(), st);
+        cuda_check(launch_temper_grid(d_gds, d_list_big, (int)big.size(), max_slices, st), "k_tp_*");
+        count_launch(temper_grid_launches());
+      }
       cuda_check(cudaEventRecord(mv.a, st), "event");
       cuda_check(launch_move(family, shape, dmax, d_gds, d_list, d_prefix, na, total, st), "k_chain<move>");
       cuda_check(cudaEventRecord(mv.b, st), "event");
-      cuda_check(launch_stats(d_gds, d_list, na, st), "k_stats");
+      cuda_check(launch_stats_grid(d_gds, d_list, na, dmax, st), "k_stats_grid");
       count_launch(3);
       d2h(h_st, d_st, G, st);
       dev.sync();

@@ -210,7 +210,11 @@ __device__ __forceinline__ long long count_le(double x, double u, long long S) {
 // systematic resampling over normalised weights w (smc.cpp:95-112): block fp64
 // scan of the CDF, then every element i writes the targets
 // j with c_{i-1} < (j+u)/S <= c_i (running max keeps ranges disjoint).
-__device__ void block_resample(const double* w, int64_t T, long long S, double u, int* anc, TemperShared& sh) {
+// Generalised to one slice of a grid-level scan: the slice starts at CDF value
+// `base`, owns targets [lo_b, hi_b) (its last element takes every target up
+// to hi_b) and element i is global particle idx0 + i.
+__device__ void block_resample_range(const double* w, int64_t T, double base, long long lo_b, long long hi_b,
+                                     long long S, double u, int* anc, int64_t idx0, TemperShared& sh) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int64_t chunk = (T + nt - 1) / nt;
   const int64_t b0 = (int64_t)tid * chunk < T ? (int64_t)tid * chunk : T;
@@ -229,14 +233,18 @@ __device__ void block_resample(const double* w, int64_t T, long long S, double u
     if (lane < nw) sh.red[lane] = vi - v;  // exclusive warp offsets
   }
   __syncthreads();
-  const double prefix = sh.red[warp] + (incl - loc);
+  const double prefix = base + (sh.red[warp] + (incl - loc));
+  auto bound = [&](int64_t i, double cc) -> long long {
+    long long k = (i == T - 1) ? hi_b : count_le(cc, u, S);
+    return k < lo_b ? lo_b : (k > hi_b ? hi_b : k);
+  };
   // running boundary counts; per-thread maximum then block exclusive max-scan
-  long long mymax = 0;
+  long long mymax = lo_b;
   {
     double cc = prefix;
     for (int64_t i = b0; i < b1; ++i) {
       cc += w[i];
-      long long k = (i == T - 1) ? S : count_le(cc, u, S);
+      const long long k = bound(i, cc);
       mymax = k > mymax ? k : mymax;
     }
   }
@@ -250,7 +258,7 @@ __device__ void block_resample(const double* w, int64_t T, long long S, double u
   if (lane == 31) sh.redi[warp] = v;
   __syncthreads();
   if (warp == 0) {
-    long long x = lane < nw ? sh.redi[lane] : 0;
+    long long x = lane < nw ? sh.redi[lane] : lo_b;
     long long xi = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -258,21 +266,26 @@ __device__ void block_resample(const double* w, int64_t T, long long S, double u
       if (lane >= o) xi = xi > t ? xi : t;
     }
     const long long ex = __shfl_up_sync(0xffffffffu, xi, 1);
-    if (lane < nw) sh.redi[lane] = lane == 0 ? 0 : ex;
+    if (lane < nw) sh.redi[lane] = lane == 0 ? lo_b : ex;
   }
   __syncthreads();
   long long excl_lane = __shfl_up_sync(0xffffffffu, v, 1);
-  if (lane == 0) excl_lane = 0;
+  if (lane == 0) excl_lane = lo_b;
   long long lo = sh.redi[warp] > excl_lane ? sh.redi[warp] : excl_lane;
   double cc = prefix;
   for (int64_t i = b0; i < b1; ++i) {
     cc += w[i];
-    long long k = (i == T - 1) ? S : count_le(cc, u, S);
+    long long k = bound(i, cc);
     if (k < lo) k = lo;
-    for (long long j = lo; j < k; ++j) anc[j] = (int)i;
+    for (long long j = lo; j < k; ++j) anc[j] = (int)(idx0 + i);
     lo = k;
   }
   __syncthreads();
+}
+
+__device__ __forceinline__ void block_resample(const double* w, int64_t T, long long S, double u, int* anc,
+                                               TemperShared& sh) {
+  block_resample_range(w, T, 0.0, 0, S, S, u, anc, 0, sh);
 }
 
 // predict_step_size (mcmc.cpp:20-53) for component i; hist is the ring of
@@ -387,6 +400,309 @@ __global__ void __launch_bounds__(256) k_stats(const GroupDesc* __restrict__ gds
     st->cur ^= 1;
     if (beta >= 1.0) st->active = 0;
   }
+}
+
+
+// =================================================================
+// Grid-level tempering for large populations (T > 2^17): the same
+// operations as k_temper, with the T-element reductions and the CDF scan
+// spread over slices of the particle array (one CTA per slice).  A
+// "last block" of each launch combines the slice partials in slice order
+// (deterministic) and advances the state machine; the bisection is one
+// launch per evaluation with exactly the reference's control flow
+// (smc.cpp:68-93).
+// =================================================================
+constexpr int kGridThreads = 512;
+
+__device__ __forceinline__ bool last_block(unsigned int* counter, int n) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(counter, 1u) == (unsigned)(n - 1);
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+struct SliceCtx {
+  const GroupDesc* g;
+  TemperScratch* ts;
+  int64_t i0, i1;
+};
+
+__device__ __forceinline__ bool slice_ctx(const GroupDesc* gds, const int* list, SliceCtx& c) {
+  c.g = &gds[list[blockIdx.y]];
+  c.ts = c.g->ts;
+  if ((int)blockIdx.x >= c.g->nslices) return false;
+  c.i0 = (int64_t)blockIdx.x * c.g->slice_len;
+  c.i1 = c.i0 + c.g->slice_len < c.g->T ? c.i0 + c.g->slice_len : c.g->T;
+  return true;
+}
+
+__global__ void __launch_bounds__(kGridThreads) k_tp_emin(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
+  __shared__ TemperShared sh;
+  SliceCtx c;
+  if (!slice_ctx(gds, list, c)) return;
+  const GroupDesc& g = *c.g;
+  GroupState* st = g.st;
+  TemperScratch* ts = c.ts;
+  if (st->level >= g.max_levels) {  // smc.cpp:195-196
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->error = GE_MAX_LEVELS;
+      st->active = 0;
+      ts->err = 1;
+    }
+    return;
+  }
+  const double* E = g.E[st->cur];
+  double m = dinf();
+  for (int64_t i = c.i0 + threadIdx.x; i < c.i1; i += blockDim.x) m = (E[i] < m) ? E[i] : m;
+  m = block_reduce(m, sh.red, OpMin(), dinf());
+  if (threadIdx.x == 0) ts->part[blockIdx.x][0] = m;
+  if (last_block(&ts->counter, g.nslices) && threadIdx.x == 0) {
+    double e = dinf();
+    for (int s = 0; s < g.nslices; ++s) e = ts->part[s][0] < e ? ts->part[s][0] : e;
+    ts->emin = isfinite(e) ? e : 0.0;
+    ts->full = 1.0 - st->beta;
+    ts->lo = 0.0;
+    ts->hi = ts->full;
+    ts->it = -1;
+    ts->done = 0;
+    ts->err = 0;
+    ts->counter = 0;
+  }
+}
+
+__global__ void __launch_bounds__(kGridThreads) k_tp_ess(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
+  __shared__ TemperShared sh;
+  SliceCtx c;
+  if (!slice_ctx(gds, list, c)) return;
+  const GroupDesc& g = *c.g;
+  TemperScratch* ts = c.ts;
+  if (ts->done || ts->err) return;
+  GroupState* st = g.st;
+  const double delta = ts->it < 0 ? ts->full : 0.5 * (ts->lo + ts->hi);
+  const double cc = -delta * g.n_data, emin = ts->emin;
+  const double* E = g.E[st->cur];
+  double a1 = 0.0, a2 = 0.0;
+  for (int64_t i = c.i0 + threadIdx.x; i < c.i1; i += blockDim.x) {
+    const double w = exp_neg_split(cc * (E[i] - emin));
+    a1 += w;
+    a2 += w * w;
+  }
+  a1 = block_reduce(a1, sh.red, OpAdd(), 0.0);
+  a2 = block_reduce(a2, sh.red, OpAdd(), 0.0);
+  if (threadIdx.x == 0) {
+    ts->part[blockIdx.x][0] = a1;
+    ts->part[blockIdx.x][1] = a2;
+  }
+  if (last_block(&ts->counter, g.nslices) && threadIdx.x == 0) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int s = 0; s < g.nslices; ++s) {
+      s1 += ts->part[s][0];
+      s2 += ts->part[s][1];
+    }
+    ts->counter = 0;
+    if (!(s1 > 0.0)) {  // ess: total weight is zero (smc.cpp:63)
+      ts->err = 1;
+      st->error = GE_ZERO_WEIGHT;
+      st->active = 0;
+      return;
+    }
+    const double r = (s1 * s1 / s2) / (double)g.T;
+    if (ts->it < 0) {
+      if (r >= g.ess_target) {
+        ts->beta_next = 1.0;
+        ts->done = 1;
+      } else {
+        ts->it = 0;
+      }
+    } else {
+      ts->it += 1;
+      if (fabs(r - g.ess_target) <= 1e-6 || ts->it >= 60) {
+        ts->beta_next = st->beta + delta;
+        ts->done = 1;
+      } else if (r > g.ess_target) {
+        ts->lo = delta;
+      } else {
+        ts->hi = delta;
+      }
+    }
+  }
+}
+
+// max of the incremental log-weights (smc.cpp:55-59, math.hpp:20-24)
+__global__ void __launch_bounds__(kGridThreads) k_tp_wmax(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
+  __shared__ TemperShared sh;
+  SliceCtx c;
+  if (!slice_ctx(gds, list, c)) return;
+  const GroupDesc& g = *c.g;
+  TemperScratch* ts = c.ts;
+  if (ts->err) return;
+  const GroupState* st = g.st;
+  const double delta = ts->beta_next - st->beta, cc = -delta * g.n_data;
+  const double* E = g.E[st->cur];
+  double m = -dinf();
+  for (int64_t i = c.i0 + threadIdx.x; i < c.i1; i += blockDim.x) m = fmax(m, delta == 0.0 ? 0.0 : cc * E[i]);
+  m = block_reduce(m, sh.red, OpMax(), -dinf());
+  if (threadIdx.x == 0) ts->part[blockIdx.x][0] = m;
+  if (last_block(&ts->counter, g.nslices) && threadIdx.x == 0) {
+    double mm = -dinf();
+    for (int s = 0; s < g.nslices; ++s) mm = fmax(mm, ts->part[s][0]);
+    ts->m = mm;
+    ts->counter = 0;
+    if (mm == -dinf()) {
+      ts->err = 1;
+      g.st->error = GE_ZERO_WEIGHT;
+      g.st->active = 0;
+    }
+  }
+}
+
+// sum exp(lw - m), sum exp(2(lw - m)) -> lse, ESS, log-mean-w, evidence (smc.cpp:128-130, :201)
+__global__ void __launch_bounds__(kGridThreads) k_tp_wsum(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
+  __shared__ TemperShared sh;
+  SliceCtx c;
+  if (!slice_ctx(gds, list, c)) return;
+  const GroupDesc& g = *c.g;
+  TemperScratch* ts = c.ts;
+  if (ts->err) return;
+  GroupState* st = g.st;
+  const double delta = ts->beta_next - st->beta, cc = -delta * g.n_data, m = ts->m;
+  const double* E = g.E[st->cur];
+  double a1 = 0.0, a2 = 0.0;
+  for (int64_t i = c.i0 + threadIdx.x; i < c.i1; i += blockDim.x) {
+    const double w = exp((delta == 0.0 ? 0.0 : cc * E[i]) - m);
+    a1 += w;
+    a2 += w * w;
+  }
+  a1 = block_reduce(a1, sh.red, OpAdd(), 0.0);
+  a2 = block_reduce(a2, sh.red, OpAdd(), 0.0);
+  if (threadIdx.x == 0) {
+    ts->part[blockIdx.x][0] = a1;
+    ts->part[blockIdx.x][1] = a2;
+  }
+  if (last_block(&ts->counter, g.nslices) && threadIdx.x == 0) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int s = 0; s < g.nslices; ++s) {
+      s1 += ts->part[s][0];
+      s2 += ts->part[s][1];
+    }
+    ts->counter = 0;
+    const double lse = m + log(s1);
+    const double lmw = lse - log((double)g.T);
+    ts->lse = lse;
+    double* dg = g.diag + (size_t)st->level * 4;
+    dg[0] = ts->beta_next;
+    dg[1] = (s1 * s1 / s2) / (double)g.T;
+    dg[2] = lmw;
+    st->neg_log_z -= lmw;
+    const u32x4 o = philox(u32x4{0u, (uint32_t)(st->level + 1), 0u, ROLE_RESAMPLE}, g.key0, g.key1);
+    ts->u = u53(o.x, o.y);
+  }
+}
+
+// normalised weights exp(lw - lse) and the grid-level fp64 CDF scan: slice
+// totals, then the exclusive slice offsets in slice order (monotone)
+__global__ void __launch_bounds__(kGridThreads) k_tp_offsets(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
+  __shared__ TemperShared sh;
+  SliceCtx c;
+  if (!slice_ctx(gds, list, c)) return;
+  const GroupDesc& g = *c.g;
+  TemperScratch* ts = c.ts;
+  if (ts->err) return;
+  const GroupState* st = g.st;
+  const double delta = ts->beta_next - st->beta, cc = -delta * g.n_data, lse = ts->lse;
+  const double* E = g.E[st->cur];
+  double loc = 0.0;
+  for (int64_t i = c.i0 + threadIdx.x; i < c.i1; i += blockDim.x) {
+    const double w = exp((delta == 0.0 ? 0.0 : cc * E[i]) - lse);
+    g.wbuf[i] = w;
+    loc += w;
+  }
+  const double tot = block_reduce(loc, sh.red, OpAdd(), 0.0);
+  if (threadIdx.x == 0) ts->part[blockIdx.x][0] = tot;
+  if (last_block(&ts->counter, g.nslices) && threadIdx.x == 0) {
+    double o = 0.0;
+    ts->offs[0] = 0.0;
+    for (int s = 0; s < g.nslices; ++s) {
+      o += ts->part[s][0];
+      ts->offs[s + 1] = o;
+    }
+    ts->counter = 0;
+  }
+}
+
+// systematic resampling over the slices, then (last block) the step-size
+// prediction for the level and the state advance
+__global__ void __launch_bounds__(kGridThreads) k_tp_resample(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
+  __shared__ TemperShared sh;
+  SliceCtx c;
+  if (!slice_ctx(gds, list, c)) return;
+  const GroupDesc& g = *c.g;
+  TemperScratch* ts = c.ts;
+  if (ts->err) return;
+  GroupState* st = g.st;
+  const long long S = g.S;
+  const double u = ts->u;
+  const int s = blockIdx.x;
+  const long long lo_b = s == 0 ? 0 : count_le(ts->offs[s], u, S);
+  const long long hi_b = s == g.nslices - 1 ? S : count_le(ts->offs[s + 1], u, S);
+  block_resample_range(g.wbuf + c.i0, c.i1 - c.i0, ts->offs[s], lo_b, hi_b > lo_b ? hi_b : lo_b, S, u, g.anc, c.i0, sh);
+  if (last_block(&ts->counter, g.nslices)) {
+    for (int i = threadIdx.x; i < g.d; i += blockDim.x)
+      g.ls0[i] = predict_log_step(g.hist, st->hist_count, g.d, i, ts->beta_next, g.pkind[i], g.pa[i], g.pb[i]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      st->beta = ts->beta_next;
+      st->level = st->level + 1;
+      ts->counter = 0;
+    }
+  }
+}
+
+// step-size statistics, one CTA per (component, group) (smc.cpp:162-179), then
+// k_stats_final: history entry, level acceptance, buffer flip
+__global__ void __launch_bounds__(256) k_stats_grid(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
+  __shared__ TemperShared sh;
+  const GroupDesc& g = gds[list[blockIdx.y]];
+  const int i = blockIdx.x;
+  if (i >= g.d) return;
+  GroupState* st = g.st;
+  const int d = g.d, S = g.S;
+  double a = 0.0, l = 0.0;
+  for (int c = threadIdx.x; c < S; c += blockDim.x) {
+    a += (double)g.chain_acc[(size_t)i * S + c];
+    l += g.chain_ls[(size_t)i * S + c];
+  }
+  a = block_reduce(a, sh.red, OpAdd(), 0.0);
+  l = block_reduce(l, sh.red, OpAdd(), 0.0);
+  if (threadIdx.x == 0) {
+    double* h = g.hist + (size_t)(st->hist_count % kHist) * (1 + 2 * d);
+    const double prop = (double)S * g.n;
+    h[1 + i] = prop > 0 ? a / prop : 0.0;
+    h[1 + d + i] = exp(l / (double)S);
+    g.stat_acc[i] = a;
+  }
+}
+
+__global__ void k_stats_final(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
+  const GroupDesc& g = gds[list[blockIdx.x]];
+  if (threadIdx.x != 0) return;
+  GroupState* st = g.st;
+  const int d = g.d, S = g.S, H = st->hist_count;
+  double* h = g.hist + (size_t)(H % kHist) * (1 + 2 * d);
+  double acc_all = 0.0;
+  for (int i = 0; i < d; ++i) acc_all += g.stat_acc[i];
+  const double beta = st->beta;
+  h[0] = beta;
+  const double prop_all = (double)S * g.n * d;
+  g.diag[(size_t)(st->level - 1) * 4 + 3] = prop_all > 0 ? acc_all / prop_all : 0.0;
+  st->hist_count = H + 1;
+  st->cur ^= 1;
+  if (beta >= 1.0) st->active = 0;
 }
 
 // ---------------------------------------------------------- unit kernels
@@ -565,6 +881,24 @@ cudaError_t launch_stats(const GroupDesc* gds, const int* list, int n_list, cuda
   k_stats<<<n_list, 256, 0, st>>>(gds, list);
   return cudaGetLastError();
 }
+cudaError_t launch_temper_grid(const GroupDesc* gds, const int* list, int n_list, int max_slices, cudaStream_t st) {
+  const dim3 grid(max_slices, n_list);
+  k_tp_emin<<<grid, kGridThreads, 0, st>>>(gds, list);
+  for (int it = 0; it < 61; ++it) k_tp_ess<<<grid, kGridThreads, 0, st>>>(gds, list);
+  k_tp_wmax<<<grid, kGridThreads, 0, st>>>(gds, list);
+  k_tp_wsum<<<grid, kGridThreads, 0, st>>>(gds, list);
+  k_tp_offsets<<<grid, kGridThreads, 0, st>>>(gds, list);
+  k_tp_resample<<<grid, kGridThreads, 0, st>>>(gds, list);
+  return cudaGetLastError();
+}
+int temper_grid_launches() { return 66; }
+
+cudaError_t launch_stats_grid(const GroupDesc* gds, const int* list, int n_list, int dmax, cudaStream_t st) {
+  k_stats_grid<<<dim3(dmax, n_list), 256, 0, st>>>(gds, list);
+  k_stats_final<<<n_list, 32, 0, st>>>(gds, list);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_unit_ess(const double* lw, int64_t n, double* out, int* err, cudaStream_t st) {
   k_unit_ess<<<1, kTemperThreads, 0, st>>>(lw, n, out, err);
   return cudaGetLastError();

@@ -41,6 +41,12 @@ cudaError_t launch_move(int family, const Shape& s, int dmax, const GroupDesc* d
                         const int* d_cta_prefix, int n_list, int total_ctas, cudaStream_t st);
 // next_beta + weights + evidence + systematic resampling + predict_step_size (one CTA per group)
 cudaError_t launch_temper(const GroupDesc* d_gds, const int* d_list, int n_list, cudaStream_t st);
+// grid-level tempering for large T: emin, 61 bisection steps, weights, CDF scan,
+// resampling + step prediction (66 launches, each over (slices x groups))
+cudaError_t launch_temper_grid(const GroupDesc* d_gds, const int* d_list, int n_list, int max_slices, cudaStream_t st);
+int temper_grid_launches();
+// step-size statistics, one CTA per (component, group), + per-group finalisation
+cudaError_t launch_stats_grid(const GroupDesc* d_gds, const int* d_list, int n_list, int dmax, cudaStream_t st);
 // step-size statistics + history + buffer flip (one CTA per group)
 cudaError_t launch_stats(const GroupDesc* d_gds, const int* d_list, int n_list, cudaStream_t st);
 

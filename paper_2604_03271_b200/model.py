@@ -92,6 +92,20 @@ NoiseSpec = Union[GaussianFixedNoise, PoissonNoise, GaussianApproxPoissonNoise, 
 FAMILY_CODE = {"gm": 0, "xps": 1, "xrd": 2, "offset": 3}
 
 
+@dataclass(frozen=True)
+class Reflection:
+    """model.hpp:25-28"""
+    mu_ref: float         # degrees 2theta
+    rel_intensity: float  # >= 0
+
+
+@dataclass
+class PhaseRef:
+    """model.hpp:29-32"""
+    name: str
+    reflections: List[Reflection]
+
+
 @dataclass
 class Spectrum:
     """proj/include/specmc/spectrum.hpp:16-20"""
@@ -127,6 +141,12 @@ class ModelSpec:
         pb = np.array([c[2] for c in codes], dtype=np.float64)
         return pk, pa, pb
 
+    def reflection_arrays(self):
+        ph = np.array([b for b, p in enumerate(self.phases) for _ in p.reflections], dtype=np.int32)
+        mu = np.array([r.mu_ref for p in self.phases for r in p.reflections], dtype=np.float64)
+        ri = np.array([r.rel_intensity for p in self.phases for r in p.reflections], dtype=np.float64)
+        return ph, mu, ri
+
     def desc(self):
         """Flat C struct; the returned keep-alive tuple must outlive the struct."""
         pk, pa, pb = self.arrays()
@@ -142,9 +162,12 @@ class ModelSpec:
             code, s0, s1, s2, lit = 3, n.s0, n.s1, n.s2, int(n.paper_literal)
         else:
             raise TypeError(f"unknown noise {n!r}")
+        ph, mu, ri = self.reflection_arrays()
         d = _lib.ModelDesc(FAMILY_CODE[self.family], self.K, len(pk), code, sigma, s0, s1, s2, lit,
-                           pk.ctypes.data_as(_lib._ip), pa.ctypes.data_as(_lib._dp), pb.ctypes.data_as(_lib._dp))
-        return d, (pk, pa, pb)
+                           pk.ctypes.data_as(_lib._ip), pa.ctypes.data_as(_lib._dp), pb.ctypes.data_as(_lib._dp),
+                           len(ph), ph.ctypes.data_as(_lib._ip), mu.ctypes.data_as(_lib._dp),
+                           ri.ctypes.data_as(_lib._dp))
+        return d, (pk, pa, pb, ph, mu, ri)
 
 
 def model_dim(spec: ModelSpec) -> int:
@@ -176,6 +199,33 @@ def xps_model(K: int, data: Spectrum, noise: XpsHeteroNoise = XpsHeteroNoise()) 
     layout += [ScalarParam("bg_a", UniformPrior(0.95 * yfirst, 1.01 * yfirst)),
                ScalarParam("bg_b", UniformPrior(0.95 * ylast, 1.01 * ylast))]
     return ModelSpec("xps", K, layout, noise)
+
+
+def xrd_model(phases: List[PhaseRef], data: Spectrum, noise: NoiseSpec = PoissonNoise()) -> ModelSpec:
+    """model.cpp:138-167: K = len(phases) crystalline phases (A, d2t, r, alpha, u, v, w, s, t)
+    then the background (bg_a, bg_sigma, bg_r, bg_b)."""
+    ys = data.ys
+    ymax, ymin = float(ys.max()), float(ys.min())
+    if not ymax > ymin:
+        raise ValueError("xrd model: degenerate intensity range")
+    ymin_pos = ymin if ymin > 0.0 else 0.0
+    layout = []
+    for k in range(1, len(phases) + 1):
+        layout += [ScalarParam(f"A{k}", GammaPrior(4.0, 4.0 / (ymax - ymin))),
+                   ScalarParam(f"d2t{k}", NormalPrior(0.0, 0.05 * 0.05)),
+                   ScalarParam(f"r{k}", UniformPrior(0.0, 1.0)),
+                   ScalarParam(f"alpha{k}", GammaPrior(5.0, 4.0)),
+                   ScalarParam(f"u{k}", GammaPrior(1.0, 10.0)),
+                   ScalarParam(f"v{k}", GammaPrior(1.0, 10.0)),
+                   ScalarParam(f"w{k}", GammaPrior(2.0, 20.0)),
+                   ScalarParam(f"s{k}", GammaPrior(2.0, 20.0)),
+                   ScalarParam(f"t{k}", GammaPrior(1.0, 10.0))]
+    half = float(np.sqrt(ymin_pos))
+    if not half > 0.0:
+        half = 1.0
+    layout += [ScalarParam("bg_a", GammaPrior(2.0, 1.0 / ymax)), ScalarParam("bg_sigma", GammaPrior(2.0, 0.4)),
+               ScalarParam("bg_r", UniformPrior(0.0, 1.0)), ScalarParam("bg_b", UniformPrior(ymin - half, ymin + half))]
+    return ModelSpec("xrd", len(phases), layout, noise, list(phases))
 
 
 def offset_model(sigma: float, m0: float = 0.0, v0: float = 4.0) -> ModelSpec:

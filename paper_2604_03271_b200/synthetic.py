@@ -17,7 +17,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .model import GaussianFixedNoise, ModelSpec, Spectrum, XpsHeteroNoise, gm_model, xps_model
+from .model import (GaussianFixedNoise, ModelSpec, PhaseRef, PoissonNoise, Reflection, Spectrum, XpsHeteroNoise,
+                    gm_model, xps_model)
 
 _M = 0xFFFFFFFFFFFFFFFF
 
@@ -72,6 +73,36 @@ class Rng:
 
     def uniform01(self) -> float:
         return float(self.next_u64() >> 11) * 2.0 ** -53
+
+    def poisson(self, mean: float) -> int:
+        """rng.hpp:95-124 (Knuth inversion below 10, PTRS above)"""
+        if mean <= 0.0:
+            return 0
+        if mean < 10.0:
+            limit = math.exp(-mean)
+            k, p = 0, 1.0
+            while True:
+                k += 1
+                p *= self.uniform01()
+                if not p > limit:
+                    return k - 1
+        slam = math.sqrt(mean)
+        loglam = math.log(mean)
+        b = 0.931 + 2.53 * slam
+        a = -0.059 + 0.02483 * b
+        inv_alpha = 1.1239 + 1.1328 / (b - 3.4)
+        v_r = 0.9277 - 3.6224 / (b - 2.0)
+        while True:
+            u = self.uniform01() - 0.5
+            v = 1.0 - self.uniform01()
+            us = 0.5 - abs(u)
+            kd = math.floor((2.0 * a / us + b) * u + mean + 0.43)
+            if us >= 0.07 and v <= v_r:
+                return int(kd)
+            if kd < 0.0 or (us < 0.013 and v > us):
+                continue
+            if math.log(v * inv_alpha / (a / (us * us) + b)) <= kd * loglam - mean - math.lgamma(kd + 1.0):
+                return int(kd)
 
     def normal(self) -> float:
         if self.has_spare:
@@ -180,6 +211,67 @@ def gen_gm(theta: np.ndarray, seed: int, n: int, x_lo: float, x_hi: float, sigma
         for i in range(n):
             f[i] += sigma * rng.normal()
     return Spectrum(xs, np.array(f) + offset)
+
+
+# proj/data/tio2_synthetic_reflections.csv, xrd_truth_phases.csv, xrd_truth_background.csv
+TIO2_PHASES = [
+    PhaseRef("rutile", [Reflection(27.45, 1.00), Reflection(36.09, 0.50), Reflection(41.26, 0.25),
+                        Reflection(54.32, 0.60), Reflection(56.64, 0.20)]),
+    PhaseRef("anatase", [Reflection(25.28, 1.00), Reflection(37.80, 0.20), Reflection(48.05, 0.35),
+                         Reflection(53.89, 0.20), Reflection(55.06, 0.20)]),
+    PhaseRef("brookite", [Reflection(25.34, 1.00), Reflection(25.69, 0.80), Reflection(30.81, 0.90),
+                          Reflection(42.34, 0.30), Reflection(48.01, 0.30)]),
+]
+# table order (A, d2t, alpha, r, u, v, w, s, t) -> layout order (A, d2t, r, alpha, u, v, w, s, t)
+_XRD_TABLE = [(10000, 0.035, 0.6, 0.50, 0.03, 0.03, 0.06, 0.06, 0.03),
+              (3500, 0.055, 0.9, 0.65, 0.1, 0.1, 0.2, 0.2, 0.1),
+              (1000, 0.04, 1.0, 0.75, 0.1, 0.1, 0.2, 0.2, 0.1)]
+XRD_TRUTH = np.array([v for A, d2t, al, r, u, vv, w, s_, t in _XRD_TABLE for v in (A, d2t, r, al, u, vv, w, s_, t)]
+                     + [60000.0, 10.0, 0.0, 100.0])
+
+
+def xrd_forward_np(theta: np.ndarray, xs: np.ndarray, phases) -> np.ndarray:
+    """model.cpp:222-267 in fp64, the reference's operation order (libm exp/tan/cos)."""
+    K = len(phases)
+    k4 = 2.772588722239781237668928485832706272302
+    n = len(xs)
+    blocks = []
+    for b, ph in enumerate(phases):
+        A, d2t, r, alpha, u, v, w, s_, t = (float(x) for x in theta[9 * b:9 * b + 9])
+        out = [0.0] * n
+        for rf in ph.reflections:
+            c = rf.mu_ref + d2t
+            half = 0.5 * c * (math.pi / 180.0)
+            tn = math.tan(half)
+            disc = u * tn * tn - v * tn + w
+            if not disc > 0.0:
+                raise ValueError(f"Caglioti discriminant non-positive at reflection center {c} deg")
+            sig0 = math.sqrt(disc)
+            om0 = s_ / math.cos(half) + t * tn
+            amp = A * rf.rel_intensity
+            for i in range(n):
+                dx = float(xs[i]) - c
+                wg = dx / (alpha * sig0) if dx >= 0.0 else dx / sig0
+                wl = dx / (alpha * om0) if dx >= 0.0 else dx / om0
+                out[i] += amp * ((1.0 - r) * math.exp((-k4) * (wg * wg)) + r / (1.0 + 4.0 * (wl * wl)))
+        blocks.append(out)
+    a, sbg, rbg, bg = (float(x) for x in theta[9 * K:9 * K + 4])
+    blocks.append([a * ((1.0 - rbg) * math.exp((-k4) * ((float(x) / sbg) ** 2)) + rbg / (1.0 + 4.0 * ((float(x) / sbg)
+                                                                                                    ** 2))) + bg
+                   for x in xs])
+    f = list(blocks[0])
+    for blk in blocks[1:]:
+        f = [f[i] + blk[i] for i in range(n)]
+    return np.array(f)
+
+
+def gen_xrd(n_points: int, seed: int):
+    """gen_xrd (synthetic.cpp:230-268): three TiO2 phases + pV background, Poisson counts on [5, 60]."""
+    xs = linspace(5.0, 60.0, n_points)
+    f = xrd_forward_np(XRD_TRUTH, xs, TIO2_PHASES)
+    rng = Rng(seed)
+    ys = np.array([float(rng.poisson(float(v))) for v in f])
+    return Spectrum(xs, ys), XRD_TRUTH.copy()
 
 
 # ------------------------------------------------------------- BASELINE configs
