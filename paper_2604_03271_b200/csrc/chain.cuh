@@ -43,7 +43,7 @@ struct BlockC {
 
 template <int FAM>
 __device__ __forceinline__ constexpr int block_stride() {
-  return FAM == FAM_GM ? 3 : (FAM == FAM_XPS ? 4 : 1);
+  return FAM == FAM_GM ? 3 : (FAM == FAM_XPS ? 4 : (FAM == FAM_XRD ? 9 : 1));
 }
 
 // gm:  g = A exp(-b/2 (x-mu)^2) = c1 2^(c2 d^2)                   (model.cpp:216-220)
@@ -143,26 +143,115 @@ struct Unit {
   }
 };
 
+// ---- block geometry and block signals -----------------------------------
+// Component i belongs to block b (a peak, an xrd phase, or the xrd background
+// block K), is parameter j of it, and the block's parameters start at off.
+template <int FAM>
+struct BlockIdx {
+  int b, j, off, np;  // np: parameters of the block
+};
+template <int FAM>
+__device__ __forceinline__ BlockIdx<FAM> block_of(const GroupDesc& g, int i) {
+  BlockIdx<FAM> r;
+  if (FAM == FAM_XRD) {
+    if (i < 9 * g.K) {
+      r.b = i / 9;
+      r.off = 9 * r.b;
+      r.np = 9;
+    } else {
+      r.b = g.K;
+      r.off = 9 * g.K;
+      r.np = 4;
+    }
+  } else {
+    constexpr int stride = block_stride<FAM>();
+    r.b = i / stride;
+    r.off = r.b * stride;
+    r.np = stride;
+  }
+  r.j = i - r.off;
+  return r;
+}
+template <int FAM>
+__device__ __forceinline__ int n_blocks(const GroupDesc& g) {
+  return FAM == FAM_OFFSET ? 1 : (FAM == FAM_XRD ? g.K + 1 : g.K);
+}
+template <int FAM>
+__device__ __forceinline__ int block_off(const GroupDesc& g, int b) {
+  return FAM == FAM_XRD ? 9 * b : b * block_stride<FAM>();
+}
+
+// acc_k += sign * g_b(x_k) for block b with (fp32) parameters p.  Returns false
+// on an evaluation fault (model.cpp:226-258, :272-275): the block then adds nothing.
+//   xrd phase b (model.cpp:235-267): sum over its reflections of
+//     A ri [(1-r) 2^(-(2 dx/wg)^2) + r / (1 + (2 dx/wl)^2)],  c = mu_ref + d2t,
+//     wg = sqrt(u tan^2 - v tan + w), wl = s / cos + t tan (theta = c/2), both x alpha for dx >= 0
+//   xrd background (model.cpp:223-234): a [(1-r) 2^(-(2x/s)^2) + r / (1 + (2x/s)^2)] + b
+template <int FAM, int PPL, int W>
+__device__ __forceinline__ bool add_block(const GroupDesc& g, int b, const float* p, const Unit<PPL, W>& u,
+                                          float (&acc)[PPL], float sign) {
+  if (FAM == FAM_XRD) {
+    if (b < g.K) {
+      const float A = p[0], d2t = p[1], r = p[2], alpha = p[3], uu = p[4], vv = p[5], ww = p[6], ss = p[7],
+                  tt = p[8];
+      const int q1 = g.refl_off[b + 1];
+      for (int q = g.refl_off[b]; q < q1; ++q) {
+        const float2 rf = g.refl[q];
+        const float c = rf.x + d2t;
+        float sn, cs;
+        sincosf(0.5f * c * 0.017453292519943295f, &sn, &cs);
+        const float tn = sn / cs;
+        const float disc = fmaf(fmaf(uu, tn, -vv), tn, ww);
+        if (!(disc > 0.f)) return false;
+        const float om0 = ss / cs + tt * tn;
+        if (!(om0 > 0.f)) return false;
+        const float ig_lo = 2.f / sqrtf(disc), ig_hi = ig_lo / alpha;
+        const float il_lo = 2.f / om0, il_hi = il_lo / alpha;
+        const float amp = sign * A * rf.y;
+        const float ag = amp * (1.f - r), al = amp * r;
+#pragma unroll
+        for (int k = 0; k < PPL; ++k) {
+          const float dx = u.x(k) - c;
+          const bool pos = dx >= 0.f;
+          const float tg = dx * (pos ? ig_hi : ig_lo);
+          const float tl = dx * (pos ? il_hi : il_lo);
+          acc[k] += fmaf(ag, ex2f(-(tg * tg)), al * rcpf(fmaf(tl, tl, 1.f)));
+        }
+      }
+      return true;
+    }
+    if (!(p[1] > 0.f)) return false;
+    const float is = 2.f / p[1];
+    const float ag = sign * p[0] * (1.f - p[2]), al = sign * p[0] * p[2], off = sign * p[3];
+#pragma unroll
+    for (int k = 0; k < PPL; ++k) {
+      const float t = u.x(k) * is;
+      acc[k] += fmaf(ag, ex2f(-(t * t)), fmaf(al, rcpf(fmaf(t, t, 1.f)), off));
+    }
+    return true;
+  } else {
+    BlockC c = block_consts<FAM>(p);
+    if (!c.ok) return false;
+    c.c1 *= sign;                      // amplitudes: gm c1; xps c1, c2 (gm c2 is the exponent)
+    if (FAM == FAM_XPS) c.c2 *= sign;
+#pragma unroll
+    for (int k = 0; k < PPL; ++k) acc[k] += shape<FAM>(c, u.x(k));
+    return true;
+  }
+}
+
 // P_k = sum over non-faulty blocks of g_b(x_k), in layout order (combine,
 // model.cpp:287-288).  Returns the bit mask of faulty blocks (eval_block
 // returning false, model.cpp:272-275): any set bit means E = +inf.
 template <int FAM, int PPL, int W>
 __device__ __forceinline__ unsigned long long full_signal(const GroupDesc& g, const float* th,
                                                           const Unit<PPL, W>& u, float (&P)[PPL]) {
-  constexpr int stride = block_stride<FAM>();
 #pragma unroll
   for (int k = 0; k < PPL; ++k) P[k] = 0.f;
-  const int nb = FAM == FAM_OFFSET ? 1 : g.K;
+  const int nb = n_blocks<FAM>(g);
   unsigned long long fmask = 0ull;
-  for (int b = 0; b < nb; ++b) {
-    const BlockC c = block_consts<FAM>(th + b * stride);
-    if (!c.ok) {
-      fmask |= 1ull << b;
-      continue;
-    }
-#pragma unroll
-    for (int k = 0; k < PPL; ++k) P[k] += shape<FAM>(c, u.x(k));
-  }
+  for (int b = 0; b < nb; ++b)
+    if (!add_block<FAM, PPL, W>(g, b, th + block_off<FAM>(g, b), u, P, 1.f)) fmask |= 1ull << b;
   return fmask;
 }
 
@@ -498,7 +587,8 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   const uint32_t cg = g.chain_base + (uint32_t)c;
   double* thn = g.theta[cur ^ 1];
   double* En = g.E[cur ^ 1];
-  const int npeak = FAM == FAM_OFFSET ? 0 : stride * g.K;
+  // components inside a block (everything but the xps Shirley endpoints and the offset family)
+  const int npeak = FAM == FAM_OFFSET ? 0 : (FAM == FAM_XRD ? g.d : stride * g.K);
   unsigned long long trials = 0;
   // Q[k] at Qs[k * L]: signal of every block except the one being swept (P - g_b)
   float* Qs = gcache + (size_t)unit * SM::NPT + u.lg;
@@ -535,17 +625,16 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
     __syncwarp();
     asum = amp_sum<FAM>(g, thf);
     for (int i = 0; i < d; ++i) {
-      const int b = i / stride, j = i - b * stride;
+      const BlockIdx<FAM> bi = block_of<FAM>(g, i);
+      const int b = bi.b, j = bi.j;
       const bool peak = i < npeak;
       if (FAM != FAM_OFFSET && peak && j == 0) {  // entering block b: Q = P - g_b(x)
-        const BlockC cb = block_consts<FAM>(thf + b * stride);
-        if (cb.ok) {
+        float Qn[PPL];
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) Qs[k * L] = SMC_P(k) - shape<FAM>(cb, u.x(k));
-        } else {
+        for (int k = 0; k < PPL; ++k) Qn[k] = SMC_P(k);
+        if (!((fmask >> b) & 1ull)) add_block<FAM, PPL, W>(g, b, thf + bi.off, u, Qn, -1.f);
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) Qs[k * L] = SMC_P(k);
-        }
+        for (int k = 0; k < PPL; ++k) Qs[k * L] = Qn[k];
       }
       if (!(flg[i] & 1)) continue;  // outside the prior support: no trial (mcmc.cpp:68)
       const float oldf = thf[i], newf = nvf[i];
@@ -560,7 +649,8 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
       } else if (!peak) {  // Shirley endpoint: enters combine() only (block -1)
 #pragma unroll
         for (int k = 0; k < PPL; ++k) Pn[k] = SMC_P(k);
-      } else if (j == 0 && oldf != 0.f && !((fmask >> b) & 1ull)) {  // amplitude: g' = (A'/A) g
+      } else if (j == 0 && oldf != 0.f && !((fmask >> b) & 1ull) &&
+                 (FAM != FAM_XRD || b < g.K)) {  // amplitude: g' = (A'/A) g
         const float r = (newf - oldf) * rcpf(oldf);
 #pragma unroll
         for (int k = 0; k < PPL; ++k) {
@@ -569,19 +659,16 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
         }
         dA = fabsf(newf) - fabsf(oldf);
       } else {
-        float pn[stride];
+        constexpr int kMaxNp = FAM == FAM_XRD ? 9 : block_stride<FAM>();
+        float pn[kMaxNp];
 #pragma unroll
-        for (int q = 0; q < stride; ++q) pn[q] = (q == j) ? newf : thf[b * stride + q];
-        const BlockC cn = block_consts<FAM>(pn);
-        if (cn.ok) {
+        for (int q = 0; q < kMaxNp; ++q) pn[q] = (q == j) ? newf : (q < bi.np ? thf[bi.off + q] : 0.f);
+#pragma unroll
+        for (int k = 0; k < PPL; ++k) Pn[k] = Qs[k * L];
+        if (add_block<FAM, PPL, W>(g, b, pn, u, Pn, 1.f))
           fnew &= ~(1ull << b);
-#pragma unroll
-          for (int k = 0; k < PPL; ++k) Pn[k] = Qs[k * L] + shape<FAM>(cn, u.x(k));
-        } else {
+        else
           fnew |= 1ull << b;
-#pragma unroll
-          for (int k = 0; k < PPL; ++k) Pn[k] = Qs[k * L];
-        }
         if (j == 0) dA = fabsf(newf) - fabsf(oldf);
       }
       float bga = 0.f, bgb = 0.f;

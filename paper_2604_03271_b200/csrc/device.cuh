@@ -73,6 +73,9 @@ struct GroupDesc {  // immutable per group
   const float* spec_x;   // shifted abscissa x' = x - x_shift
   const float2* spec_c;  // (c_k, h_{k+1}): trapezoid weights of the Shirley scan
   const float2* spec_y;  // (y_k, 1/s_k): observation and inverse noise scale
+  // xrd reflections (mu_ref, rel_intensity) grouped by phase: phase b owns [refl_off[b], refl_off[b+1])
+  const float2* refl;
+  const int* refl_off;
   // priors (layout order, location components already shifted)
   const int* pkind;
   const double* pa;

@@ -72,11 +72,25 @@ int model_dim(const specmc_model_desc& m) {  // model.cpp:86-93
 }
 
 void validate_model(const specmc_model_desc& m) {
-  if (m.family == SPECMC_FAMILY_XRD)
-    throw Error(SPECMC_EINVAL, "xrd family is not implemented on the device path yet");
-  if (m.family != SPECMC_FAMILY_GM && m.family != SPECMC_FAMILY_XPS && m.family != SPECMC_FAMILY_OFFSET)
+  if (m.family != SPECMC_FAMILY_GM && m.family != SPECMC_FAMILY_XPS && m.family != SPECMC_FAMILY_OFFSET &&
+      m.family != SPECMC_FAMILY_XRD)
     throw Error(SPECMC_EINVAL, "unknown model family");
   if (m.K < 1) throw Error(SPECMC_EINVAL, "model needs K >= 1");
+  if (m.family == SPECMC_FAMILY_XRD) {  // model.cpp:99-105, :62-72
+    if (m.n_refl < 1 || !m.refl_phase || !m.refl_mu || !m.refl_int)
+      throw Error(SPECMC_EINVAL, "xrd model: phases count must equal K");
+    std::vector<int> cnt(m.K, 0);
+    for (int q = 0; q < m.n_refl; ++q) {
+      const int ph = m.refl_phase[q];
+      if (ph < 0 || ph >= m.K) throw Error(SPECMC_EINVAL, "xrd model: phases count must equal K");
+      if (q > 0 && ph < m.refl_phase[q - 1]) throw Error(SPECMC_EINVAL, "xrd model: reflections must be grouped by phase");
+      if (m.refl_int[q] < 0.0) throw Error(SPECMC_EINVAL, "negative reflection intensity");
+      ++cnt[ph];
+    }
+    for (int b = 0; b < m.K; ++b)
+      if (!cnt[b]) throw Error(SPECMC_EINVAL, "xrd phase has no reflections");
+  }
+  if (m.K > 64 && m.family != SPECMC_FAMILY_OFFSET) throw Error(SPECMC_EINVAL, "device path supports K <= 64");
   if (m.d != model_dim(m)) throw Error(SPECMC_EINVAL, "model layout length mismatch");
   if (!m.prior_kind || !m.prior_a || !m.prior_b) throw Error(SPECMC_EINVAL, "model priors missing");
   for (int i = 0; i < m.d; ++i) {  // priors.cpp:9-20
@@ -287,6 +301,8 @@ struct RunSpec {
   specmc_model_desc m;
   std::vector<int32_t> pk;
   std::vector<double> pa, pb;  // shifted
+  std::vector<float> refl;     // xrd: (mu_ref, rel_intensity) pairs grouped by phase
+  std::vector<int> refl_off;   // xrd: K + 1 phase offsets
   int spectrum;
   specmc_smc_config cfg;
   double x_shift;
@@ -397,6 +413,7 @@ struct ClassRun {
       bytes += Arena::al(T * 8) + Arena::al(kHist * (1 + 2 * d) * 8);
       bytes += Arena::al((size_t)R.cfg.max_levels * 4 * 8);
       bytes += Arena::al(d * 8);                                                // stat_acc
+      bytes += Arena::al(R.refl.size() * 4 + 8) + Arena::al(R.refl_off.size() * 4 + 4);  // xrd reflections
       if (T > kGridTemperT) bytes += Arena::al(sizeof(TemperScratch));         // grid tempering
     }
     ar.reserve(bytes);
@@ -479,6 +496,14 @@ struct ClassRun {
       g.diag = ar.take<double>((size_t)R.cfg.max_levels * 4);
       g.st = d_st + gi;
       g.stat_acc = ar.take<double>(d);
+      if (!R.refl.empty()) {
+        float2* rf = ar.take<float2>(R.refl.size() / 2);
+        int* ro = ar.take<int>(R.refl_off.size());
+        h2d(reinterpret_cast<float*>(rf), R.refl.data(), R.refl.size(), st);
+        h2d(ro, R.refl_off.data(), R.refl_off.size(), st);
+        g.refl = rf;
+        g.refl_off = ro;
+      }
       if (T > kGridTemperT) {  // grid-level tempering: slices of <= 512 x slice_len particles
         g.ts = ar.take<TemperScratch>(1);
         size_t sl = std::max<size_t>(32768, (T + kMaxSlices - 1) / kMaxSlices);
@@ -663,9 +688,21 @@ RunSpec make_runspec(const specmc_model_desc& m, int spectrum, const specmc_smc_
         R.pb[i] -= R.x_shift;
       }
     }
+  if (m.family == SPECMC_FAMILY_XRD) {
+    R.refl_off.assign(m.K + 1, 0);
+    for (int q = 0; q < m.n_refl; ++q) {
+      R.refl.push_back((float)m.refl_mu[q]);
+      R.refl.push_back((float)m.refl_int[q]);
+      ++R.refl_off[m.refl_phase[q] + 1];
+    }
+    for (int b = 0; b < m.K; ++b) R.refl_off[b + 1] += R.refl_off[b];
+  }
   R.m.prior_kind = nullptr;  // owned copies live in R
   R.m.prior_a = nullptr;
   R.m.prior_b = nullptr;
+  R.m.refl_phase = nullptr;
+  R.m.refl_mu = nullptr;
+  R.m.refl_int = nullptr;
   return R;
 }
 
@@ -885,6 +922,8 @@ int specmc_energy_batch(const specmc_model_desc* model, const double* xs, const 
     double* pb = sc.alloc<double>(d);
     double* th = sc.alloc<double>((size_t)d * T);
     double* E = sc.alloc<double>(T);
+    float2* rf = sc.alloc<float2>(std::max<size_t>(R.refl.size() / 2, 1));
+    int* ro = sc.alloc<int>(std::max<size_t>(R.refl_off.size(), 1));
     GroupState* gst = sc.alloc<GroupState>(1);
     GroupDesc* gd = sc.alloc<GroupDesc>(1);
     int* lst = sc.alloc<int>(2);
@@ -896,6 +935,8 @@ int specmc_energy_batch(const specmc_model_desc* model, const double* xs, const 
     h2d(pk, R.pk.data(), d, st);
     h2d(pa, R.pa.data(), d, st);
     h2d(pb, R.pb.data(), d, st);
+    h2d(reinterpret_cast<float*>(rf), R.refl.data(), R.refl.size(), st);
+    h2d(ro, R.refl_off.data(), R.refl_off.size(), st);
     std::vector<double> soa((size_t)d * T);
     for (int64_t c = 0; c < T; ++c)
       for (int i = 0; i < d; ++i) {
@@ -934,6 +975,8 @@ int specmc_energy_batch(const specmc_model_desc* model, const double* xs, const 
     g.theta[0] = g.theta[1] = th;
     g.E[0] = g.E[1] = E;
     g.st = gst;
+    g.refl = rf;
+    g.refl_off = ro;
     GroupState s;
     std::memset(&s, 0, sizeof(s));
     h2d(gd, &g, 1, st);

@@ -837,6 +837,7 @@ cudaError_t launch_energy(int family, const Shape& s, int dmax, const GroupDesc*
     case FAM_GM: return launch_chain_gm_energy(s, dmax, gds, list, prefix, n_list, total_ctas, st);
     case FAM_XPS: return launch_chain_xps_energy(s, dmax, gds, list, prefix, n_list, total_ctas, st);
     case FAM_OFFSET: return launch_chain_offset_energy(s, dmax, gds, list, prefix, n_list, total_ctas, st);
+    case FAM_XRD: return launch_chain_xrd_energy(s, dmax, gds, list, prefix, n_list, total_ctas, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -846,6 +847,7 @@ cudaError_t launch_move(int family, const Shape& s, int dmax, const GroupDesc* g
     case FAM_GM: return launch_chain_gm_move(s, dmax, gds, list, prefix, n_list, total_ctas, st);
     case FAM_XPS: return launch_chain_xps_move(s, dmax, gds, list, prefix, n_list, total_ctas, st);
     case FAM_OFFSET: return launch_chain_offset_move(s, dmax, gds, list, prefix, n_list, total_ctas, st);
+    case FAM_XRD: return launch_chain_xrd_move(s, dmax, gds, list, prefix, n_list, total_ctas, st);
   }
   return cudaErrorInvalidValue;
 }

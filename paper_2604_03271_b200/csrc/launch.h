@@ -35,6 +35,8 @@ SMC_DECL_CHAIN(launch_chain_xps_energy)
 SMC_DECL_CHAIN(launch_chain_xps_move)
 SMC_DECL_CHAIN(launch_chain_offset_energy)
 SMC_DECL_CHAIN(launch_chain_offset_move)
+SMC_DECL_CHAIN(launch_chain_xrd_energy)
+SMC_DECL_CHAIN(launch_chain_xrd_move)
 #undef SMC_DECL_CHAIN
 // fused waste-free chain move (wastefree_level chain loop x cw_mh_sweep, smc.cpp:142-156, mcmc.cpp:55-96)
 cudaError_t launch_move(int family, const Shape& s, int dmax, const GroupDesc* d_gds, const int* d_list,

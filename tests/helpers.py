@@ -19,6 +19,9 @@ def oracle_model(spec: M.ModelSpec, data: M.Spectrum) -> OracleModel:
         kw = dict(noise="gauss_approx")
     else:
         kw = dict(noise="xps_hetero", s0=n.s0, s1=n.s1, s2=n.s2, paper_literal=n.paper_literal)
+    if spec.family == "xrd":
+        ph, mu, ri = spec.reflection_arrays()
+        kw.update(refl_phase=ph, refl_mu=mu, refl_int=ri)
     return OracleModel(spec.family, spec.K, pk, pa, pb, data.xs, data.ys, **kw)
 
 

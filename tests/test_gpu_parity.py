@@ -40,6 +40,9 @@ def _cases():
     cases.append(("c2_xps6", w.spec(6), w.data))
     w1 = syn.config("C1")
     cases.append(("c1_gm3", w1.spec(3), w1.data))
+    xr, _ = syn.gen_xrd(600, 5)
+    cases.append(("xrd3_poisson", M.xrd_model(syn.TIO2_PHASES, xr), xr))
+    cases.append(("xrd3_gapprox", M.xrd_model(syn.TIO2_PHASES, xr, M.GaussianApproxPoissonNoise()), xr))
     return cases
 
 
@@ -63,6 +66,18 @@ def test_energy_at_truth_xps(smc, port):
     e_ref = port.energy(om, th)
     e_gpu = smc.energy(spec, th, sp)
     assert abs(e_gpu - e_ref) <= _energy_tol(e_ref, 840)
+
+
+def test_energy_at_truth_xrd(smc, port):
+    sp, th = syn.gen_xrd(1000, 7)
+    spec = M.xrd_model(syn.TIO2_PHASES, sp)
+    om = oracle_model(spec, sp)
+    e_ref = port.energy(om, th)
+    assert abs(smc.energy(spec, th, sp) - e_ref) <= _energy_tol(e_ref, 1000)
+    # Caglioti fault (discriminant <= 0) is the +inf sentinel (model.cpp:243-249)
+    bad = th.copy()
+    bad[4], bad[5], bad[6] = 0.0, 1.0, 0.0
+    assert smc.energy(spec, bad, sp) == math.inf and port.energy(om, bad) == math.inf
 
 
 def test_energy_sentinels(smc):

@@ -155,3 +155,11 @@ def test_grid_and_block_tempering_agree(smc, port):
     big = smc.smc_run_batch([(spec, 0, smc.SmcConfig(T=(1 << 17) + 1024, n=8, seed=s)) for s in (1, 2, 3)], [w.data])
     fs, fb = np.array([r.F for r in small]), np.array([r.F for r in big])
     assert abs(fs.mean() - fb.mean()) < 0.5, (fs, fb)
+
+
+def test_free_energy_matches_oracle_xrd(smc, port):
+    data, _ = syn.gen_xrd(160, 5)
+    phases = syn.TIO2_PHASES[:1]
+    spec = M.xrd_model(phases, data)
+    f_gpu, f_cpu, se = _compare_F(smc, port, spec, data, 200, 5, range(100, 132), range(4))
+    assert abs(f_gpu.mean() - f_cpu.mean()) <= 4 * se + 0.1, (f_gpu.mean(), f_cpu.mean(), se)

@@ -43,3 +43,18 @@ def test_config_shapes():
         w = syn.config(name)
         assert len(w.data.xs) == N and w.k_range[1] == kmax and w.T % w.n == 0
         assert np.all(np.diff(w.data.xs) > 0) and np.all(np.isfinite(w.data.ys))
+
+
+def test_gen_xrd_bitwise(ref):  # synthetic.cpp:230-268 (Poisson counts, PTRS)
+    xs, ys = ref.gen_xrd(1000, 5)
+    sp, _ = syn.gen_xrd(1000, 5)
+    assert np.array_equal(xs, sp.xs) and np.array_equal(ys, sp.ys)
+
+
+def test_xrd_model_priors(ref):  # model.cpp:138-167
+    sp, _ = syn.gen_xrd(500, 2)
+    spec = M.xrd_model(syn.TIO2_PHASES, sp)
+    ph, mu, ri = spec.reflection_arrays()
+    rk, ra, rb = ref.xrd_model_priors(3, ph, mu, ri, sp.xs, sp.ys)
+    pk, pa, pb = spec.arrays()
+    assert np.array_equal(pk, rk) and np.array_equal(pa, ra) and np.array_equal(pb, rb)
