@@ -317,6 +317,55 @@ __device__ __forceinline__ float noise_term(const GroupDesc& g, float f, float2 
   }
 }
 
+// Hetero terms of two points share one rcp and one lg2 (3 instead of 4 MUFU
+// ops per point with the peak shape):
+//   lg2(va/sa) + lg2(vb/sb) = lg2((va/sa)(vb/sb)),
+//   ra^2/va + rb^2/vb = (ra^2 vb + rb^2 va) / (va vb).
+// The var <= 0 sentinel survives: the lg2 argument takes the sign of min(va, vb)
+// (NaN for a negative variance, energy.cpp:20), va vb = 0 gives inf.  Products
+// leave the fp32 range only for states whose per-point fp32 terms already
+// overflow (E >~ 1e19): those read as +inf as before.
+template <int NZ>
+__host__ __device__ constexpr bool nz_pairs() { return NZ == NZ_HETERO || NZ == NZ_HLIN || NZ == NZ_HPROP; }
+template <int NZ>
+__device__ __forceinline__ float nz_var(const GroupDesc& g, float f) {
+  if (NZ == NZ_HETERO) return fmaf(fmaf(g.nz_a1, f, g.nz_a0), f, g.nz_a2);
+  if (NZ == NZ_HLIN) return fmaf(g.nz_a0, f, g.nz_a2);
+  return f;  // NZ_HPROP
+}
+template <int NZ>
+__device__ __forceinline__ float noise_pair(const GroupDesc& g, float fa, float fb, float2 ya, float2 yb) {
+  const float ra = ya.x - fa, rb = yb.x - fb;
+  const float va = nz_var<NZ>(g, fa), vb = nz_var<NZ>(g, fb);
+  const float num = fmaf(ra * ra, vb, (rb * rb) * va);
+  const float la = copysignf((va * ya.y) * (vb * yb.y), fminf(va, vb));
+  return fmaf(g.nz_q, num * rcpf(va * vb), lg2f(la));
+}
+// f(k) -> sum of the noise terms of this lane's PPL points, and the padding
+// correction: padding points (k >= nv) replicate the lane's last point, so
+// npad copies of its term are removed at once
+template <int NZ, int PPL, int W, class F>
+__device__ __forceinline__ float lane_noise_sum(const GroupDesc& g, const Unit<PPL, W>& u, F&& fk) {
+  float acc = 0.f, tl = 0.f, fprev = 0.f, flast = 0.f;
+#pragma unroll
+  for (int k = 0; k < PPL; ++k) {
+    const float f = fk(k);
+    if (nz_pairs<NZ>()) {
+      if (k & 1)
+        acc += noise_pair<NZ>(g, fprev, f, u.y(k - 1), u.y(k));
+      else
+        fprev = f;
+      flast = f;
+    } else {
+      tl = noise_term<NZ>(g, f, u.y(k));
+      acc += tl;
+    }
+  }
+  if (!nz_pairs<NZ>()) return fmaf(-u.npad, tl, acc);
+  if (u.npad > 0.f) acc = fmaf(-u.npad, noise_term<NZ>(g, flast, u.y(PPL - 1)), acc);
+  return acc;
+}
+
 template <int NZ>
 __device__ __forceinline__ double finish_energy(const GroupDesc& g, double s) {
   if (!isfinite(s)) return dinf();  // var <= 0 / f <= 0 sentinel (energy.cpp:16, :20, :25)
@@ -325,14 +374,8 @@ __device__ __forceinline__ double finish_energy(const GroupDesc& g, double s) {
 
 template <int PPL, int W, int NZ>
 __device__ __forceinline__ double eval_plain_nz(const GroupDesc& g, Unit<PPL, W>& u, const float (&Pn)[PPL]) {
-  float acc = 0.f, tl = 0.f;
-#pragma unroll
-  for (int k = 0; k < PPL; ++k) {
-    tl = noise_term<NZ>(g, Pn[k], u.y(k));
-    acc += tl;
-  }
-  // padding points (k >= nv) replicate the lane's last point: remove them at once
-  return finish_energy<NZ>(g, unit_sum(u, fmaf(-u.npad, tl, acc)));
+  const float acc = lane_noise_sum<NZ>(g, u, [&](int k) { return Pn[k]; });
+  return finish_energy<NZ>(g, unit_sum(u, acc));
 }
 
 // Shirley background + energy (lineshapes.hpp:65-83, model.cpp:289-292).
@@ -385,60 +428,46 @@ __device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, 
     }
     degen = !(total > 1e-12f * mx * g.range);
   }
-  float acc = 0.f, tl = 0.f;
+  float acc;
   if (!degen) {
     const float scale = ba * rcpf(total);
     const float base = fmaf(scale, prefix, bga);
     float run2 = 0.f;
-#pragma unroll
-    for (int k = 0; k < PPL; ++k) {
+    acc = lane_noise_sum<NZ>(g, u, [&](int k) {
       float Ck;  // C_k = sum_{j<=k} c_j Pn_j - h_{k+1} Pn_k (lane-local part)
       if (kKeepC) {
-        Ck = Cn[k];
+        Ck = Cn[kKeepC ? k : 0];
       } else {
         const float2 c = u.c(k);
         run2 = fmaf(c.x, Pn[k], run2);
         Ck = fmaf(-c.y, Pn[k], run2);
       }
-      const float B = fmaf(scale, Ck, base);
-      tl = noise_term<NZ>(g, Pn[k] + B, u.y(k));
-      acc += tl;
-    }
+      return Pn[k] + fmaf(scale, Ck, base);
+    });
   } else {  // linear ramp a -> b
-#pragma unroll
-    for (int k = 0; k < PPL; ++k) {
-      const float B = fmaf(ba, (u.x(k) - g.x0s) * g.inv_range, bga);
-      tl = noise_term<NZ>(g, Pn[k] + B, u.y(k));
-      acc += tl;
-    }
+    acc = lane_noise_sum<NZ>(g, u, [&](int k) { return Pn[k] + fmaf(ba, (u.x(k) - g.x0s) * g.inv_range, bga); });
   }
   // padding points (k >= nv, c = h = 0) replicate the lane's last point exactly
-  return finish_energy<NZ>(g, unit_sum(u, fmaf(-u.npad, tl, acc)));
+  return finish_energy<NZ>(g, unit_sum(u, acc));
 }
 
-template <int FAM, int PPL, int W>
-__device__ __forceinline__ double evaluate(const GroupDesc& g, Unit<PPL, W>& u, const float (&Pn)[PPL], float bga,
-                                           float bgb, float amp_bound) {
-#ifdef SMC_FORCE_NZ
-  if (FAM == FAM_XPS) return eval_shirley_nz<PPL, W, SMC_FORCE_NZ>(g, u, Pn, bga, bgb, amp_bound);
-#endif
-  if (FAM == FAM_XPS) {
+// NZ is the device noise model, or NZ_DYN to switch on g.noise per evaluation
+// (energy kernels and the offset test family: one instantiation for all noises)
+template <int FAM, int PPL, int W, int NZ>
+__device__ __forceinline__ double evaluate_nz(const GroupDesc& g, Unit<PPL, W>& u, const float (&Pn)[PPL], float bga,
+                                              float bgb, float amp_bound) {
+  if (NZ == NZ_DYN) {
     switch (g.noise) {
-      case NZ_GAUSS: return eval_shirley_nz<PPL, W, NZ_GAUSS>(g, u, Pn, bga, bgb, amp_bound);
-      case NZ_HETERO: return eval_shirley_nz<PPL, W, NZ_HETERO>(g, u, Pn, bga, bgb, amp_bound);
-      case NZ_HLIN: return eval_shirley_nz<PPL, W, NZ_HLIN>(g, u, Pn, bga, bgb, amp_bound);
-      case NZ_HPROP: return eval_shirley_nz<PPL, W, NZ_HPROP>(g, u, Pn, bga, bgb, amp_bound);
-      default: return eval_shirley_nz<PPL, W, NZ_POISSON>(g, u, Pn, bga, bgb, amp_bound);
-    }
-  } else {
-    switch (g.noise) {
-      case NZ_GAUSS: return eval_plain_nz<PPL, W, NZ_GAUSS>(g, u, Pn);
-      case NZ_HETERO: return eval_plain_nz<PPL, W, NZ_HETERO>(g, u, Pn);
-      case NZ_HLIN: return eval_plain_nz<PPL, W, NZ_HLIN>(g, u, Pn);
-      case NZ_HPROP: return eval_plain_nz<PPL, W, NZ_HPROP>(g, u, Pn);
-      default: return eval_plain_nz<PPL, W, NZ_POISSON>(g, u, Pn);
+      case NZ_GAUSS: return evaluate_nz<FAM, PPL, W, NZ_GAUSS>(g, u, Pn, bga, bgb, amp_bound);
+      case NZ_HETERO: return evaluate_nz<FAM, PPL, W, NZ_HETERO>(g, u, Pn, bga, bgb, amp_bound);
+      case NZ_HLIN: return evaluate_nz<FAM, PPL, W, NZ_HLIN>(g, u, Pn, bga, bgb, amp_bound);
+      case NZ_HPROP: return evaluate_nz<FAM, PPL, W, NZ_HPROP>(g, u, Pn, bga, bgb, amp_bound);
+      default: return evaluate_nz<FAM, PPL, W, NZ_POISSON>(g, u, Pn, bga, bgb, amp_bound);
     }
   }
+  constexpr int nz = NZ == NZ_DYN ? NZ_GAUSS : NZ;  // (the NZ_DYN branch above returned)
+  if (FAM == FAM_XPS) return eval_shirley_nz<PPL, W, nz>(g, u, Pn, bga, bgb, amp_bound);
+  return eval_plain_nz<PPL, W, nz>(g, u, Pn);
 }
 
 // lp_new - lp_old for one component (priors.cpp:22-35); false = -inf (reject)
@@ -490,88 +519,23 @@ struct Bounds {
   // (PPL = 32: 2 x 256 threads at <= 128 registers as well)
 };
 
-template <int FAM, int PPL, int W, bool ENERGY>
-__global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_blocks)
-    k_chain(const GroupDesc* __restrict__ gds, const int* __restrict__ list, const int* __restrict__ cta_prefix,
-            int n_list, int U, int dpad) {
+// The level's work for one chain unit (initial energy, then the move kernel's
+// n sweeps), with the noise model NZ fixed at compile time for the move
+// kernels: the sweep loop holds a single evaluation variant.
+template <int FAM, int PPL, int W, bool ENERGY, int NZ>
+__device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, const int c, const int unit,
+                                           const int wiu, const int lane, const GroupState* st, const int cur,
+                                           const int d, const int T, double* th, double* lsv, int* acc, double* nvb,
+                                           double* dlpb, float* lub, int* flg, float* thf, float* nvf,
+                                           float* gcache, float* pcache) {
   using SM = Smem<PPL, W>;
   constexpr int stride = block_stride<FAM>();
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int gi = find_group(cta_prefix, n_list, blockIdx.x);
-  const GroupDesc& g = gds[list[gi]];
-  const int cta_in_group = blockIdx.x - cta_prefix[gi];
-
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  float* sx = reinterpret_cast<float*>(smem + SM::off_x);
-  float2* sc = reinterpret_cast<float2*>(smem + SM::off_c);
-  float2* sy = reinterpret_cast<float2*>(smem + SM::off_y);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int unit = warp / W, wiu = warp - unit * W;
-  unsigned char* wb = smem + SM::off_w + (size_t)unit * SM::per_unit(dpad);
-  double* th = reinterpret_cast<double*>(wb);
-  double* lsv = th + dpad;
-  int* acc = reinterpret_cast<int*>(lsv + dpad);
-  double* nvb = reinterpret_cast<double*>(acc + dpad);  // dpad is even: 8-byte aligned
-  double* dlpb = nvb + dpad;
-  float* lub = reinterpret_cast<float*>(dlpb + dpad);
-  int* flg = reinterpret_cast<int*>(lub + dpad);
-  float* thf = reinterpret_cast<float*>(flg + dpad);  // fp32 shadow of th (block constants)
-  float* nvf = thf + dpad;                            // fp32 shadow of the proposals
-  const size_t xoff = ((SM::off_w + (size_t)U * SM::per_unit(dpad)) + 15) & ~(size_t)15;
-  Xch* xcs = reinterpret_cast<Xch*>(smem + xoff);
-  float* gcache = reinterpret_cast<float*>(smem + xoff + (size_t)U * sizeof(Xch));
-  float* pcache = gcache + (size_t)U * SM::NPT;
-
-  // ---- stage the spectrum: cp.async.bulk (UBLKCP) completing on an mbarrier
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    constexpr uint32_t bx = SM::NPT * 4u, bc = SM::NPT * 8u, by = SM::NPT * 8u;
-    mbar_expect_tx(bar, bx + (FAM == FAM_XPS ? bc : 0u) + by);
-    bulk_g2s(sx, g.spec_x, bx, bar);
-    if (FAM == FAM_XPS) bulk_g2s(sc, g.spec_c, bc, bar);
-    bulk_g2s(sy, g.spec_y, by, bar);
-  }
-  __syncthreads();
-  mbar_wait(bar, 0);
-
-  const int c = cta_in_group * U + unit;
-  const int units = ENERGY ? g.T : g.S;
-  if (c >= units) return;  // the whole unit leaves; no CTA-wide barrier follows
-
-  Unit<PPL, W> u;
-  u.sx = sx;
-  u.sc = sc;
-  u.sy = sy;
-  u.xc = xcs + unit;
-  u.lg = wiu * 32 + lane;
-  u.wiu = wiu;
-  u.lane = lane;
-  u.bar_id = 1 + unit;
-  u.par = 0;
-  u.nv = min(max(g.N - u.lg * PPL, 0), PPL);
-  u.npad = (float)(PPL - u.nv);
-
-  const GroupState* st = g.st;
-  const int cur = st->cur;
-  const int d = g.d, T = g.T;
-  const double* thc = g.theta[cur];
-  const int src = ENERGY ? c : g.anc[c];
-  for (int i = lane; i < d; i += 32) {
-    th[i] = thc[(size_t)i * T + src];
-    thf[i] = (float)th[i];
-    if (!ENERGY) {
-      lsv[i] = g.ls0[i];
-      acc[i] = 0;
-    }
-  }
-  __syncwarp();
-
   const int ibg = 4 * g.K;  // xps Shirley endpoints (a, b) at ibg, ibg + 1
   float P[PPL];
   unsigned long long fmask = full_signal<FAM, PPL, W>(g, thf, u, P);
   float asum = amp_sum<FAM>(g, thf);
   double e = fmask ? dinf()
-                   : evaluate<FAM, PPL, W>(g, u, P, FAM == FAM_XPS ? thf[ibg] : 0.f,
+                   : evaluate_nz<FAM, PPL, W, NZ>(g, u, P, FAM == FAM_XPS ? thf[ibg] : 0.f,
                                            FAM == FAM_XPS ? thf[ibg + 1] : 0.f, asum);
   if (ENERGY) {
     if (wiu == 0 && lane == 0) g.E[cur][c] = e;
@@ -676,7 +640,7 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
         bga = i == ibg ? newf : thf[ibg];
         bgb = i == ibg + 1 ? newf : thf[ibg + 1];
       }
-      const double e_new = fnew ? dinf() : evaluate<FAM, PPL, W>(g, u, Pn, bga, bgb, asum + dA);
+      const double e_new = fnew ? dinf() : evaluate_nz<FAM, PPL, W, NZ>(g, u, Pn, bga, bgb, asum + dA);
       // mcmc.cpp:72-80
       const double dlp = dlpb[i];
       double lr;
@@ -715,27 +679,31 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
     }
     __syncwarp();
     // ---- sweep epilogue: tallies and Robbins-Monro in log space (mcmc.cpp:14-18, :89-93);
-    // step i is only read by component i's next proposal, so the update can wait until here
-    const float gam = (t <= adapt_sweeps) ? exp2f(-0.6f * log2f((float)t)) : 0.f;  // t^-0.6
-    for (int i = lane; i < d; i += 32) {
-      const int a = flg[i] >> 1;
-      acc[i] += a;
-      if (t <= adapt_sweeps) {
-        const double ls = lsv[i] + (double)gam * ((double)a - 0.5);
-        lsv[i] = fmin(fmax(ls, kLogStepMin), kLogStepMax);
+    // step i is only read by component i's next proposal, so the update can wait until here.
+    // These are read-modify-writes of the unit's shared state: warp 0 alone does them
+    // (the other warps read lsv after the unit barrier that opens the next sweep).
+    if (wiu == 0) {
+      const float gam = (t <= adapt_sweeps) ? exp2f(-0.6f * log2f((float)t)) : 0.f;  // t^-0.6
+      for (int i = lane; i < d; i += 32) {
+        const int a = flg[i] >> 1;
+        acc[i] += a;
+        if (t <= adapt_sweeps) {
+          const double ls = lsv[i] + (double)gam * ((double)a - 0.5);
+          lsv[i] = fmin(fmax(ls, kLogStepMin), kLogStepMax);
+        }
       }
     }
     __syncwarp();
     const size_t slot = (size_t)c * n + (t - 1);  // smc.cpp:151
     if (wiu == 0) {
-      for (int i = lane; i < d; i += 32) thn[(size_t)i * T + slot] = th[i];
+      for (int i = lane; i < d; i += 32) thn[(size_t)i * g.tp + slot] = th[i];
       if (lane == 0) En[slot] = e;
     }
   }
   if (wiu == 0) {
     for (int i = lane; i < d; i += 32) {
-      g.chain_acc[(size_t)i * S + c] = acc[i];
-      g.chain_ls[(size_t)i * S + c] = lsv[i];
+      g.chain_acc[(size_t)i * g.sp + c] = acc[i];
+      g.chain_ls[(size_t)i * g.sp + c] = lsv[i];
     }
   }
 #undef SMC_P
@@ -743,17 +711,97 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   if (wiu == 0 && lane == 0) atomicAdd(&g.st->trials, trials);
 }
 
+template <int FAM, int PPL, int W, bool ENERGY, int NZ>
+__global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_blocks)
+    k_chain(const GroupDesc* __restrict__ gds, const int* __restrict__ list, const int* __restrict__ cta_prefix,
+            int n_list, int U, int dpad) {
+  using SM = Smem<PPL, W>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int gi = find_group(cta_prefix, n_list, blockIdx.x);
+  const GroupDesc& g = gds[list[gi]];
+  const int cta_in_group = blockIdx.x - cta_prefix[gi];
+
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  float* sx = reinterpret_cast<float*>(smem + SM::off_x);
+  float2* sc = reinterpret_cast<float2*>(smem + SM::off_c);
+  float2* sy = reinterpret_cast<float2*>(smem + SM::off_y);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int unit = warp / W, wiu = warp - unit * W;
+  unsigned char* wb = smem + SM::off_w + (size_t)unit * SM::per_unit(dpad);
+  double* th = reinterpret_cast<double*>(wb);
+  double* lsv = th + dpad;
+  int* acc = reinterpret_cast<int*>(lsv + dpad);
+  double* nvb = reinterpret_cast<double*>(acc + dpad);  // dpad is even: 8-byte aligned
+  double* dlpb = nvb + dpad;
+  float* lub = reinterpret_cast<float*>(dlpb + dpad);
+  int* flg = reinterpret_cast<int*>(lub + dpad);
+  float* thf = reinterpret_cast<float*>(flg + dpad);  // fp32 shadow of th (block constants)
+  float* nvf = thf + dpad;                            // fp32 shadow of the proposals
+  const size_t xoff = ((SM::off_w + (size_t)U * SM::per_unit(dpad)) + 15) & ~(size_t)15;
+  Xch* xcs = reinterpret_cast<Xch*>(smem + xoff);
+  float* gcache = reinterpret_cast<float*>(smem + xoff + (size_t)U * sizeof(Xch));
+  float* pcache = gcache + (size_t)U * SM::NPT;
+
+  // ---- stage the spectrum: cp.async.bulk (UBLKCP) completing on an mbarrier
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    constexpr uint32_t bx = SM::NPT * 4u, bc = SM::NPT * 8u, by = SM::NPT * 8u;
+    mbar_expect_tx(bar, bx + (FAM == FAM_XPS ? bc : 0u) + by);
+    bulk_g2s(sx, g.spec_x, bx, bar);
+    if (FAM == FAM_XPS) bulk_g2s(sc, g.spec_c, bc, bar);
+    bulk_g2s(sy, g.spec_y, by, bar);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+
+  const int c = cta_in_group * U + unit;
+  const int units = ENERGY ? g.T : g.S;
+  if (c >= units) return;  // the whole unit leaves; no CTA-wide barrier follows
+
+  Unit<PPL, W> u;
+  u.sx = sx;
+  u.sc = sc;
+  u.sy = sy;
+  u.xc = xcs + unit;
+  u.lg = wiu * 32 + lane;
+  u.wiu = wiu;
+  u.lane = lane;
+  u.bar_id = 1 + unit;
+  u.par = 0;
+  u.nv = min(max(g.N - u.lg * PPL, 0), PPL);
+  u.npad = (float)(PPL - u.nv);
+
+  const GroupState* st = g.st;
+  const int cur = st->cur;
+  const int d = g.d, T = g.T;
+  const double* thc = g.theta[cur];
+  const int src = ENERGY ? c : g.anc[c];
+  for (int i = lane; i < d; i += 32) {
+    th[i] = thc[(size_t)i * g.tp + src];
+    thf[i] = (float)th[i];
+    if (!ENERGY) {
+      lsv[i] = g.ls0[i];
+      acc[i] = 0;
+    }
+  }
+  __syncwarp();
+
+  chain_body<FAM, PPL, W, ENERGY, NZ>(g, u, c, unit, wiu, lane, st, cur, d, T, th, lsv, acc, nvb, dlpb, lub, flg, thf,
+                                      nvf, gcache, pcache);
+}
+
 // ------------------------------------------------------------------ launch
-template <int FAM, int PPL, int W, bool ENERGY>
+template <int FAM, int PPL, int W, bool ENERGY, int NZ>
 cudaError_t launch_chain_t(int U, int dmax, const GroupDesc* gds, const int* list, const int* prefix, int n_list,
                            int total_ctas, cudaStream_t st) {
   const int dpad = (dmax + 1) & ~1;
   const size_t smem = Smem<PPL, W>::bytes(U, dpad);
-  auto kern = k_chain<FAM, PPL, W, ENERGY>;
+  auto kern = k_chain<FAM, PPL, W, ENERGY, NZ>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
+  if (total_ctas <= 0) return cudaSuccess;  // prime only (module load + attributes, see prime_level_kernels)
   kern<<<total_ctas, Bounds<W, PPL>::threads, smem, st>>>(gds, list, prefix, n_list, U, dpad);
   return cudaGetLastError();
 }
@@ -765,11 +813,11 @@ cudaError_t launch_chain_t(int U, int dmax, const GroupDesc* gds, const int* lis
   X(2, 10) X(2, 12) X(2, 14) X(2, 16) X(2, 20) X(2, 24) X(2, 28) X(2, 32)                             \
   X(4, 20) X(4, 24) X(4, 28) X(4, 32) X(8, 20) X(8, 24) X(8, 28) X(8, 32)
 
-template <int FAM, bool ENERGY>
+template <int FAM, bool ENERGY, int NZ>
 cudaError_t launch_chain_fam(const Shape& s, int dmax, const GroupDesc* gds, const int* list, const int* prefix,
                              int n_list, int total_ctas, cudaStream_t st) {
 #define SMC_CASE(WW, PP) \
-  if (s.W == WW && s.PPL == PP) return launch_chain_t<FAM, PP, WW, ENERGY>(s.U, dmax, gds, list, prefix, n_list, total_ctas, st);
+  if (s.W == WW && s.PPL == PP) return launch_chain_t<FAM, PP, WW, ENERGY, NZ>(s.U, dmax, gds, list, prefix, n_list, total_ctas, st);
   SMC_FOR_EACH_SHAPE(SMC_CASE)
 #undef SMC_CASE
   return cudaErrorInvalidValue;

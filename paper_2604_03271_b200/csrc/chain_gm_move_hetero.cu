@@ -1,0 +1,9 @@
+// chain_gm_move_hetero.cu -- instantiates k_chain<FAM_GM, *, *, false, NZ_HETERO> (see chain.cuh).
+#include "chain.cuh"
+
+namespace smc {
+cudaError_t launch_chain_gm_move_hetero(const Shape& s, int dmax, const GroupDesc* gds, const int* list, const int* prefix,
+                                        int n_list, int total_ctas, cudaStream_t st) {
+  return launch_chain_fam<FAM_GM, false, NZ_HETERO>(s, dmax, gds, list, prefix, n_list, total_ctas, st);
+}
+}  // namespace smc

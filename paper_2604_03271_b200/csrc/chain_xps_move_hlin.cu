@@ -1,0 +1,9 @@
+// chain_xps_move_hlin.cu -- instantiates k_chain<FAM_XPS, *, *, false, NZ_HLIN> (see chain.cuh).
+#include "chain.cuh"
+
+namespace smc {
+cudaError_t launch_chain_xps_move_hlin(const Shape& s, int dmax, const GroupDesc* gds, const int* list, const int* prefix,
+                                       int n_list, int total_ctas, cudaStream_t st) {
+  return launch_chain_fam<FAM_XPS, false, NZ_HLIN>(s, dmax, gds, list, prefix, n_list, total_ctas, st);
+}
+}  // namespace smc

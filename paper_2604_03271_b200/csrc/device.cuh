@@ -21,7 +21,7 @@
 namespace smc {
 
 enum Family : int { FAM_GM = 0, FAM_XPS = 1, FAM_XRD = 2, FAM_OFFSET = 3 };
-enum NoiseDev : int { NZ_GAUSS = 0, NZ_HETERO = 1, NZ_POISSON = 2, NZ_HLIN = 3, NZ_HPROP = 4 };
+enum NoiseDev : int { NZ_DYN = -1, NZ_GAUSS = 0, NZ_HETERO = 1, NZ_POISSON = 2, NZ_HLIN = 3, NZ_HPROP = 4 };
 enum PriorKind : int { PR_NORMAL = 0, PR_GAMMA = 1, PR_UNIFORM = 2 };
 enum Role : uint32_t { ROLE_INIT = 1, ROLE_CHAIN = 2, ROLE_RESAMPLE = 3 };
 enum GroupError : int { GE_NONE = 0, GE_MAX_LEVELS = 1, GE_ZERO_WEIGHT = 2 };
@@ -80,7 +80,11 @@ struct GroupDesc {  // immutable per group
   const int* pkind;
   const double* pa;
   const double* pb;
-  // buffers
+  // buffers.  [d][*] arrays use a padded row pitch (tp for T columns, sp for
+  // S): pitch * 8 bytes is an odd multiple of 256 B, so the d rows of one
+  // particle (read/written lane-parallel over components by the chain kernel)
+  // spread over L2 slices instead of aliasing at a power-of-two stride
+  int tp, sp;
   double* theta[2];
   double* E[2];
   int* anc;

@@ -23,6 +23,7 @@
 #include <numeric>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/specmc_b200.h"
@@ -180,18 +181,110 @@ struct DevBuf {
 };
 
 // bump allocator over one cudaMalloc (256-byte aligned slices)
+// Process-wide cache of session arenas.  Large cudaMalloc/cudaFree pairs cost
+// up to ~1 s per call at C2 sizes (cudaFree synchronises and unmaps), and
+// stream-ordered pool memory measured ~16% slower in the move kernel than
+// cudaMalloc'd memory, so freed arenas are kept (per device, up to kMaxCached
+// bytes) and handed to later sessions of similar size.
+struct ArenaCache {
+  static constexpr size_t kMaxCached = size_t(16) << 30;
+  std::mutex mu;
+  std::multimap<size_t, std::pair<int, void*>> free_;  // bytes -> (device, ptr)
+  size_t cached = 0;
+  void* get(int dev, size_t b, size_t& got) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      for (auto it = free_.lower_bound(b); it != free_.end() && it->first <= 2 * b + (size_t(64) << 20); ++it)
+        if (it->second.first == dev) {
+          void* p = it->second.second;
+          got = it->first;
+          cached -= it->first;
+          free_.erase(it);
+          return p;
+        }
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, b) != cudaSuccess) {  // retry once with the cache released
+      cudaGetLastError();
+      release(dev);
+      cuda_check(cudaMalloc(&p, b), "cudaMalloc");
+    }
+    got = b;
+    return p;
+  }
+  void put(int dev, void* p, size_t b) {
+    std::lock_guard<std::mutex> lk(mu);
+    free_.emplace(b, std::make_pair(dev, p));
+    cached += b;
+    while (cached > kMaxCached && !free_.empty()) {  // drop the smallest
+      auto it = free_.begin();
+      free_on(it->second.first, it->second.second);
+      cached -= it->first;
+      free_.erase(it);
+    }
+  }
+  void release(int dev) {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto it = free_.begin(); it != free_.end();)
+      if (it->second.first == dev) {
+        free_on(dev, it->second.second);
+        cached -= it->first;
+        it = free_.erase(it);
+      } else {
+        ++it;
+      }
+  }
+  static void free_on(int dev, void* p) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(dev);
+    cudaFree(p);
+    cudaSetDevice(cur);
+  }
+};
+ArenaCache& arena_cache() {
+  static ArenaCache* c = new ArenaCache();  // never destroyed: the CUDA context may be gone at exit
+  return *c;
+}
+
+// Row pitch (elements) of the [d][n] device arrays: a multiple of 32 doubles
+// with pitch / 32 odd (GroupDesc::tp, device.cuh)
+inline size_t row_pitch(size_t n) {
+  size_t p = (n + 31) & ~(size_t)31;
+  if (((p / 32) & 1) == 0) p += 32;
+  return p;
+}
+
+// One device allocation per class of runs, carved by take().
 struct Arena {
-  DevBuf buf;
-  size_t off = 0;
+  void* p = nullptr;
+  size_t bytes = 0, off = 0;
+  int dev = 0;
+  cudaStream_t st = nullptr;
   static size_t al(size_t b) { return (b + 255) & ~(size_t)255; }
-  void reserve(size_t b) { buf = DevBuf(b); }
+  void reserve(size_t b, int device, cudaStream_t s) {
+    dev = device;
+    st = s;
+    if (b) p = arena_cache().get(dev, b, bytes);
+    if (const char* poison = std::getenv("SPECMC_POISON"))  // debug: fill with a byte pattern (uninitialised-read hunt)
+      if (p) cuda_check(cudaMemsetAsync(p, std::atoi(poison), bytes, st), "poison");
+  }
+  Arena() = default;
+  Arena(const Arena&) = delete;
+  ~Arena() {
+    if (!p) return;
+    if (cudaStreamSynchronize(st) == cudaSuccess)
+      arena_cache().put(dev, p, bytes);
+    else
+      cudaFree(p);  // the context is in an error state: do not recycle
+  }
   template <typename T>
   T* take(size_t count) {
     const size_t b = al(sizeof(T) * std::max<size_t>(count, 1));
-    if (off + b > buf.bytes) throw Error(SPECMC_ECUDA, "arena overflow");
-    T* p = reinterpret_cast<T*>(static_cast<char*>(buf.p) + off);
+    if (off + b > bytes) throw Error(SPECMC_ECUDA, "arena overflow");
+    T* q = reinterpret_cast<T*>(static_cast<char*>(p) + off);
     off += b;
-    return p;
+    return q;
   }
 };
 
@@ -209,6 +302,19 @@ struct PreparedSpectrum {
 
 // Lane-transposed spectrum arrays for one launch shape (see device.cuh) and the
 // noise constants of E = e_a0 + e_a1 * sum_k l_k (kernels.cu noise_term).
+// device noise model of a model description (NoiseDev, device.cuh); the move
+// kernel is instantiated per model
+int dev_noise(const specmc_model_desc& m) {
+  switch (m.noise) {
+    case SPECMC_NOISE_GAUSSIAN: return NZ_GAUSS;
+    case SPECMC_NOISE_POISSON: return NZ_POISSON;
+    case SPECMC_NOISE_XPS_HETERO:
+      if (m.s1 == 0.0 && m.s2 == 0.0) return NZ_HPROP;
+      return m.s1 == 0.0 ? NZ_HLIN : NZ_HETERO;
+    default: return NZ_HPROP;  // GaussianApproxPoisson: var = f
+  }
+}
+
 PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, const double* ys, int64_t N,
                                   const Shape& s, double x_shift) {
   PreparedSpectrum ps;
@@ -256,6 +362,7 @@ PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, 
       // s1 = s2 = 0 (var = s0^2 f) the s0^2 factor moves into 1/s and q'
       const bool prop = h1 == 0.0 && h2 == 0.0;
       ps.nz = prop ? NZ_HPROP : (h1 == 0.0 ? NZ_HLIN : NZ_HETERO);
+      if (ps.nz != dev_noise(m)) throw Error(SPECMC_ERUNTIME, "internal: noise model code mismatch");
       ps.a0 = (float)h0;
       ps.a1 = (float)h1;
       ps.a2 = (float)h2;
@@ -357,7 +464,7 @@ struct Timer {
 struct ClassRun {
   std::vector<int> idx;  // indices into the session's runs
   Shape shape{};
-  int dmax = 1, Tmax = 0, family = 0, G = 0;
+  int dmax = 1, Tmax = 0, family = 0, noise = 0, G = 0;
   Arena ar;
   GroupDesc* d_gds = nullptr;
   GroupState* d_st = nullptr;
@@ -381,6 +488,7 @@ struct ClassRun {
   void prepare(Device& dev, const std::vector<RunSpec>& runs, const std::vector<specmc_spectrum>& spectra) {
     G = (int)idx.size();
     family = runs[idx[0]].m.family;
+    noise = dev_noise(runs[idx[0]].m);
     int64_t Nmax = 0;
     for (int r : idx) {
       Nmax = std::max(Nmax, runs[r].N);
@@ -390,6 +498,8 @@ struct ClassRun {
     shape = pick_shape(Nmax);
     if ((int64_t)32 * shape.W * shape.PPL < Nmax)
       throw Error(SPECMC_EINVAL, "spectrum has more points than the device path supports (8192)");
+    // module load of this class's kernels happens here, outside the timed level loop
+    cuda_check(prime_level_kernels(family, noise, shape, dmax), "loading the level kernels");
     if (chain_smem_bytes(shape, dmax) > 227 * 1024)
       throw Error(SPECMC_EINVAL, "model too large for the device path (shared memory)");
 
@@ -407,16 +517,17 @@ struct ClassRun {
     for (int r : idx) {
       const auto& R = runs[r];
       const size_t T = R.cfg.T, d = R.m.d, S = T / R.cfg.n;
+      const size_t tp = row_pitch(T), sp = row_pitch(S);
       bytes += 3 * Arena::al(d * 8) + Arena::al(d * 4);
-      bytes += 2 * Arena::al(d * T * 8) + 2 * Arena::al(T * 8);
-      bytes += Arena::al(S * 4) + Arena::al(d * S * 4) + Arena::al(d * S * 8);
+      bytes += 2 * Arena::al(d * tp * 8) + 2 * Arena::al(T * 8);
+      bytes += Arena::al(S * 4) + Arena::al(d * sp * 4) + Arena::al(d * sp * 8);
       bytes += Arena::al(T * 8) + Arena::al(kHist * (1 + 2 * d) * 8);
       bytes += Arena::al((size_t)R.cfg.max_levels * 4 * 8);
       bytes += Arena::al(d * 8);                                                // stat_acc
       bytes += Arena::al(R.refl.size() * 4 + 8) + Arena::al(R.refl_off.size() * 4 + 4);  // xrd reflections
       if (T > kGridTemperT) bytes += Arena::al(sizeof(TemperScratch));         // grid tempering
     }
-    ar.reserve(bytes);
+    ar.reserve(bytes, dev.ordinal, dev.stream);
     d_gds = ar.take<GroupDesc>(G);
     d_st = ar.take<GroupState>(G);
     d_list = ar.take<int>(G + 1);
@@ -483,14 +594,16 @@ struct ClassRun {
       g.pkind = pk;
       g.pa = pa;
       g.pb = pb;
-      g.theta[0] = ar.take<double>(d * T);
-      g.theta[1] = ar.take<double>(d * T);
+      g.tp = (int)row_pitch(T);
+      g.sp = (int)row_pitch(S);
+      g.theta[0] = ar.take<double>(d * g.tp);
+      g.theta[1] = ar.take<double>(d * g.tp);
       g.E[0] = ar.take<double>(T);
       g.E[1] = ar.take<double>(T);
       g.anc = ar.take<int>(S);
       g.ls0 = ar.take<double>(d);
-      g.chain_acc = ar.take<int>(d * S);
-      g.chain_ls = ar.take<double>(d * S);
+      g.chain_acc = ar.take<int>(d * g.sp);
+      g.chain_ls = ar.take<double>(d * g.sp);
       g.wbuf = ar.take<double>(T);
       g.hist = ar.take<double>(kHist * (1 + 2 * d));
       g.diag = ar.take<double>((size_t)R.cfg.max_levels * 4);
@@ -584,7 +697,7 @@ struct ClassRun {
         count_launch(temper_grid_launches());
       }
       cuda_check(cudaEventRecord(mv.a, st), "event");
-      cuda_check(launch_move(family, shape, dmax, d_gds, d_list, d_prefix, na, total, st), "k_chain<move>");
+      cuda_check(launch_move(family, noise, shape, dmax, d_gds, d_list, d_prefix, na, total, st), "k_chain<move>");
       cuda_check(cudaEventRecord(mv.b, st), "event");
       cuda_check(launch_stats_grid(d_gds, d_list, na, dmax, st), "k_stats_grid");
       count_launch(3);
@@ -633,7 +746,10 @@ struct ClassRun {
       std::vector<double> diag((size_t)Lv * 4);
       d2h(diag.data(), gds[gi].diag, diag.size(), st);
       std::vector<double> th(d * T);
-      d2h(th.data(), gds[gi].theta[s.cur], th.size(), st);
+      cuda_check(cudaMemcpy2DAsync(th.data(), T * sizeof(double), gds[gi].theta[s.cur],
+                                   (size_t)gds[gi].tp * sizeof(double), T * sizeof(double), d,
+                                   cudaMemcpyDeviceToHost, st),
+                 "D2H theta");
       o.energies = static_cast<double*>(std::malloc(sizeof(double) * T));
       d2h(o.energies, gds[gi].E[s.cur], T, st);
       dev.sync();
@@ -729,10 +845,11 @@ struct Session {
     for (auto& r : runs)
       if (r.cfg.device != device) throw Error(SPECMC_EINVAL, "batch: all problems must target the same device");
     dev = std::make_unique<Device>(device);
-    std::map<std::pair<int, int>, std::vector<int>> cls;
+    // one class per (family, noise model, launch shape): each has its own move kernel
+    std::map<std::tuple<int, int, int>, std::vector<int>> cls;
     for (int i = 0; i < n_problems; ++i) {
       const Shape s = pick_shape(runs[i].N);
-      cls[{runs[i].m.family, s.W * 100 + s.PPL}].push_back(i);
+      cls[{runs[i].m.family, dev_noise(runs[i].m), s.W * 100 + s.PPL}].push_back(i);
     }
     for (auto& kv : cls) {
       classes.push_back(std::make_unique<ClassRun>());
@@ -954,6 +1071,8 @@ int specmc_energy_batch(const specmc_model_desc* model, const double* xs, const 
     g.T = (int)T;
     g.n = 1;
     g.S = (int)T;
+    g.tp = (int)T;  // SoA uploaded with pitch T
+    g.sp = (int)T;
     g.max_levels = 1;
     g.n_data = (double)n_points;
     g.N = (int)n_points;

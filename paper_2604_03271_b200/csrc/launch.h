@@ -30,16 +30,24 @@ cudaError_t launch_energy(int family, const Shape& s, int dmax, const GroupDesc*
   cudaError_t NAME(const Shape& s, int dmax, const GroupDesc* d_gds, const int* d_list, const int* d_cta_prefix, \
                    int n_list, int total_ctas, cudaStream_t st);
 SMC_DECL_CHAIN(launch_chain_gm_energy)
-SMC_DECL_CHAIN(launch_chain_gm_move)
 SMC_DECL_CHAIN(launch_chain_xps_energy)
-SMC_DECL_CHAIN(launch_chain_xps_move)
-SMC_DECL_CHAIN(launch_chain_offset_energy)
-SMC_DECL_CHAIN(launch_chain_offset_move)
 SMC_DECL_CHAIN(launch_chain_xrd_energy)
-SMC_DECL_CHAIN(launch_chain_xrd_move)
+SMC_DECL_CHAIN(launch_chain_offset_energy)
+SMC_DECL_CHAIN(launch_chain_offset_move_dyn)
+#define SMC_DECL_MOVE(FAM) \
+  SMC_DECL_CHAIN(launch_chain_##FAM##_move_gauss)  \
+  SMC_DECL_CHAIN(launch_chain_##FAM##_move_hetero) \
+  SMC_DECL_CHAIN(launch_chain_##FAM##_move_poisson) \
+  SMC_DECL_CHAIN(launch_chain_##FAM##_move_hlin)   \
+  SMC_DECL_CHAIN(launch_chain_##FAM##_move_hprop)
+SMC_DECL_MOVE(gm)
+SMC_DECL_MOVE(xps)
+SMC_DECL_MOVE(xrd)
+#undef SMC_DECL_MOVE
 #undef SMC_DECL_CHAIN
 // fused waste-free chain move (wastefree_level chain loop x cw_mh_sweep, smc.cpp:142-156, mcmc.cpp:55-96)
-cudaError_t launch_move(int family, const Shape& s, int dmax, const GroupDesc* d_gds, const int* d_list,
+// (one instantiation per family x device noise model, NoiseDev in device.cuh)
+cudaError_t launch_move(int family, int noise, const Shape& s, int dmax, const GroupDesc* d_gds, const int* d_list,
                         const int* d_cta_prefix, int n_list, int total_ctas, cudaStream_t st);
 // next_beta + weights + evidence + systematic resampling + predict_step_size (one CTA per group)
 cudaError_t launch_temper(const GroupDesc* d_gds, const int* d_list, int n_list, cudaStream_t st);
@@ -51,6 +59,9 @@ int temper_grid_launches();
 cudaError_t launch_stats_grid(const GroupDesc* d_gds, const int* d_list, int n_list, int dmax, cudaStream_t st);
 // step-size statistics + history + buffer flip (one CTA per group)
 cudaError_t launch_stats(const GroupDesc* d_gds, const int* d_list, int n_list, cudaStream_t st);
+
+// load every kernel of one class (family, noise, shape) before its timed run
+cudaError_t prime_level_kernels(int family, int noise, const Shape& s, int dmax);
 
 cudaError_t launch_probe_mufu(float* d_out, int blocks, int iters, cudaStream_t st);
 

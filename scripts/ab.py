@@ -8,7 +8,10 @@ res = {}
 for r in range(reps):
     for lib in libs:
         env = dict(os.environ, SPECMC_LIB=str((root / lib).resolve()))
-        out = subprocess.run([sys.executable, str(root / "scripts" / "probe.py"), *cfgs], env=env, capture_output=True, text=True).stdout
+        cp = subprocess.run([sys.executable, str(root / "scripts" / "probe.py"), *cfgs], env=env, capture_output=True, text=True)
+        out = cp.stdout
+        if cp.returncode:
+            print(lib, "probe failed:", cp.stderr[-2000:], flush=True)
         for line in out.splitlines():
             if line.startswith("{"):
                 d = json.loads(line)
@@ -17,4 +20,5 @@ for r in range(reps):
                 print(lib, line, flush=True)
 for (lib, cfg), v in sorted(res.items(), key=lambda kv: (kv[0][1], kv[0][0])):
     devs = sorted(x[0] for x in v); pe = sorted(x[1] for x in v)
-    print(f"{cfg:4s} {lib:45s} dev_med={devs[len(devs)//2]:.3f} dev_min={devs[0]:.3f}  Gpe/s_med={pe[len(pe)//2]:.1f} max={pe[-1]:.1f}")
+    print(f"{cfg:4s} {lib:45s} dev_med={devs[len(devs)//2]:.3f} dev_min={devs[0]:.3f}  Gpe/s_med={pe[len(pe)//2]:.1f} max={pe[-1]:.1f}"
+          f"  reps={[round(x[1] / 1e0, 1) for x in v]}")

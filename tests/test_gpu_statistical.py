@@ -126,6 +126,20 @@ def test_seed_replay_is_bitwise(smc):
     assert a.F == b.F and np.array_equal(a.posterior, b.posterior)
 
 
+@pytest.mark.parametrize("n_points,shape", [(1200, (2, 20)), (3000, (4, 24)), (6000, (8, 24))])
+def test_seed_replay_multiwarp_units(smc, n_points, shape):
+    # W > 1 warps per chain share the unit state in shared memory: a replay must be
+    # bitwise identical (guards against cross-warp races in the move kernel)
+    assert smc.launch_shape(n_points)[:2] == shape
+    sp, _ = syn.gen_xps_grid(4, 11, n_points, 840.0, 900.0)
+    spec = M.xps_model(4, sp)
+    cfg = smc.SmcConfig(T=512, n=8, seed=21)
+    a = smc.smc_run(spec, sp, cfg)
+    b = smc.smc_run(spec, sp, cfg)
+    assert a.F == b.F and np.array_equal(a.posterior, b.posterior)
+    assert np.array_equal(a.arrays["level_acc_rate"], b.arrays["level_acc_rate"])
+
+
 def test_batch_equals_single_runs(smc):
     # a run's result does not depend on what else shares the batch
     w = syn.config("C1")
