@@ -53,9 +53,19 @@ using NoiseSpec = std::variant<GaussianFixedNoise, PoissonNoise, GaussianApproxP
 
 enum class Family { GaussianMixture, XrdPseudoVoigt, XpsShirley, ConjugateOffset };
 
-struct ModelSpec {
+struct Reflection {  // model.hpp:28-31
+  double mu_ref;         // degrees 2theta
+  double rel_intensity;  // >= 0
+};
+struct PhaseRef {  // model.hpp:32-35
+  std::string name;
+  std::vector<Reflection> reflections;
+};
+
+struct ModelSpec {  // model.hpp:50-56
   Family family = Family::GaussianMixture;
-  int K = 0;
+  int K = 0;  // peaks (gm, xps) or phases (xrd)
+  std::vector<PhaseRef> phases;
   std::vector<ScalarParam> layout;
   NoiseSpec noise = GaussianFixedNoise{1.0};
 };
@@ -128,12 +138,51 @@ inline ModelSpec xps_model(int K, const Spectrum& data, XpsHeteroNoise noise = {
   return s;
 }
 
+// model.cpp:138-167: K = phases.size() phases (A, d2t, r, alpha, u, v, w, s, t),
+// then the background block (bg_a, bg_sigma, bg_r, bg_b)
+inline ModelSpec xrd_model(std::vector<PhaseRef> phases, const Spectrum& data, NoiseSpec noise = PoissonNoise{}) {
+  if (data.ys.empty()) throw std::invalid_argument("xrd_model: empty spectrum");
+  ModelSpec s;
+  s.family = Family::XrdPseudoVoigt;
+  s.K = static_cast<int>(phases.size());
+  s.phases = std::move(phases);
+  s.noise = noise;
+  double ymax = data.ys[0], ymin = data.ys[0];
+  for (double y : data.ys) {
+    ymax = y > ymax ? y : ymax;
+    ymin = y < ymin ? y : ymin;
+  }
+  if (!(ymax > ymin)) throw std::invalid_argument("xrd model: degenerate intensity range");
+  const double ymin_pos = ymin > 0.0 ? ymin : 0.0;
+  for (int k = 1; k <= s.K; ++k) {
+    const std::string i = std::to_string(k);
+    s.layout.push_back({"A" + i, GammaPrior{4.0, 4.0 / (ymax - ymin)}});
+    s.layout.push_back({"d2t" + i, NormalPrior{0.0, 0.05 * 0.05}});
+    s.layout.push_back({"r" + i, UniformPrior{0.0, 1.0}});
+    s.layout.push_back({"alpha" + i, GammaPrior{5.0, 4.0}});
+    s.layout.push_back({"u" + i, GammaPrior{1.0, 10.0}});
+    s.layout.push_back({"v" + i, GammaPrior{1.0, 10.0}});
+    s.layout.push_back({"w" + i, GammaPrior{2.0, 20.0}});
+    s.layout.push_back({"s" + i, GammaPrior{2.0, 20.0}});
+    s.layout.push_back({"t" + i, GammaPrior{1.0, 10.0}});
+  }
+  double half = std::sqrt(ymin_pos);
+  if (!(half > 0.0)) half = 1.0;
+  s.layout.push_back({"bg_a", GammaPrior{2.0, 1.0 / ymax}});
+  s.layout.push_back({"bg_sigma", GammaPrior{2.0, 0.4}});
+  s.layout.push_back({"bg_r", UniformPrior{0.0, 1.0}});
+  s.layout.push_back({"bg_b", UniformPrior{ymin - half, ymin + half}});
+  return s;
+}
+
 namespace detail {
 
 struct Desc {
   specmc_model_desc d{};
   std::vector<std::int32_t> k;
   std::vector<double> a, b;
+  std::vector<std::int32_t> refl_phase;  // xrd reflections, flattened in phase order
+  std::vector<double> refl_mu, refl_int;
 };
 
 inline Desc to_desc(const ModelSpec& spec) {
@@ -181,6 +230,16 @@ inline Desc to_desc(const ModelSpec& spec) {
   d.prior_kind = D.k.data();
   d.prior_a = D.a.data();
   d.prior_b = D.b.data();
+  for (std::size_t b = 0; b < spec.phases.size(); ++b)
+    for (const auto& r : spec.phases[b].reflections) {
+      D.refl_phase.push_back(static_cast<std::int32_t>(b));
+      D.refl_mu.push_back(r.mu_ref);
+      D.refl_int.push_back(r.rel_intensity);
+    }
+  d.n_refl = static_cast<std::int32_t>(D.refl_phase.size());
+  d.refl_phase = D.refl_phase.empty() ? nullptr : D.refl_phase.data();
+  d.refl_mu = D.refl_mu.empty() ? nullptr : D.refl_mu.data();
+  d.refl_int = D.refl_int.empty() ? nullptr : D.refl_int.data();
   return D;
 }
 

@@ -71,6 +71,34 @@ int main(int argc, char** argv) {
     CHECK(reps[2].arrays.at("ladder").back() == 1.0);
     std::printf("F = %.4f %.4f %.4f\n", reps[0].F, reps[1].F, reps[2].F);
   }
+  // xrd family (model.cpp:138-167): one phase with three reflections on a counts spectrum
+  Spectrum xr;
+  const double refl[3][2] = {{25.3, 100.0}, {37.8, 20.0}, {48.0, 35.0}};
+  for (int i = 0; i < 700; ++i) {
+    const double x = 20.0 + 40.0 * i / 699.0;
+    double y = 30.0;
+    for (const auto& r : refl) y += 400.0 * r[1] / 100.0 / (1.0 + ((x - r[0]) / 0.15) * ((x - r[0]) / 0.15));
+    xr.xs.push_back(x);
+    xr.ys.push_back(std::floor(y + 3.0 * std::sin(11.0 * i)));
+  }
+  PhaseRef ph{"anatase", {{25.3, 100.0}, {37.8, 20.0}, {48.0, 35.0}}};
+  const ModelSpec xs = xrd_model({ph}, xr);
+  CHECK(xs.K == 1 && xs.layout.size() == 13 && xs.phases.size() == 1);
+  Spectrum flat = xr;
+  for (auto& y : flat.ys) y = 5.0;
+  CHECK(throws<std::invalid_argument>([&] { xrd_model({ph}, flat); }));
+  SmcConfig cx;
+  cx.T = 1024;
+  cx.n = 8;
+  cx.seed = 5;
+  if (!gpu) {
+    CHECK(throws<std::runtime_error>([&] { smc_run(xs, xr, cx); }));
+  } else {
+    const RunReport r = smc_run(xs, xr, cx);
+    CHECK(std::isfinite(r.F) && !r.diverged);
+    CHECK(r.posterior.size() == static_cast<size_t>(13 * 1024));
+    std::printf("xrd F = %.4f\n", r.F);
+  }
   std::printf("%s (%d failures)\n", fails ? "FAILED" : "OK", fails);
   return fails ? 1 : 0;
 }
