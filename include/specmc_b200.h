@@ -147,6 +147,31 @@ int specmc_session_run(specmc_session* s, double* device_seconds, char* err, siz
 int specmc_session_fetch(specmc_session* s, specmc_smc_result* out, char* err, size_t errlen);
 void specmc_session_destroy(specmc_session* s);
 
+/* ---- particle-sharded runs (multi-GPU) -----------------
+ * One run's T particles split over shards that exchange a few scalars per
+ * tempering phase (ESS bisection sums, weight max / sums, per-shard weight
+ * totals for the global systematic resampling, step statistics).  The
+ * reference runs these as one process (smc.cpp:55-183); the split keeps its
+ * arithmetic: global ESS / evidence / resampling positions, Philox streams
+ * keyed by global particle and chain ids (F is GPU-count invariant up to the
+ * order of fp64 sums).
+ *   comm == NULL: n_virtual shards on cfg.device in this process (protocol
+ *                 check on one GPU); out holds every particle.
+ *   comm != NULL: this process is shard `rank` of `world` (one GPU each,
+ *                 NCCL collectives); out holds this shard's particles, F and
+ *                 the level diagnostics are global.  T % shards == 0. */
+typedef struct specmc_comm specmc_comm;
+#define SPECMC_COMM_ID_BYTES 128
+int specmc_smc_run_sharded(const specmc_model_desc* model, const double* xs, const double* ys, int64_t n_points,
+                           const specmc_smc_config* cfg, int32_t n_virtual, specmc_comm* comm,
+                           specmc_smc_result* out, char* err, size_t errlen);
+/* NCCL bootstrap: rank 0 creates the id, the host framework broadcasts it
+ * (e.g. torch.distributed), every rank then creates its communicator. */
+int specmc_nccl_unique_id(uint8_t* out /* SPECMC_COMM_ID_BYTES */, char* err, size_t errlen);
+int specmc_comm_init_nccl(int32_t rank, int32_t world, const uint8_t* id, int32_t device, specmc_comm** out,
+                          char* err, size_t errlen);
+void specmc_comm_destroy(specmc_comm* c);
+
 /* ---- parity units (each runs the same device code as the sampler) ------ */
 
 /* Batched full energies E(theta) for fixed parameters: the K2 kernel.

@@ -7,14 +7,14 @@ hand-written sm_100a CUDA kernels behind the C ABI of include/specmc_b200.h.
 from .model import (GammaPrior, GaussianApproxPoissonNoise, GaussianFixedNoise, ModelSpec, NormalPrior, PhaseRef,
                     PoissonNoise, Reflection, ScalarParam, Spectrum, UniformPrior, XpsHeteroNoise, gm_model,
                     model_dim, offset_model, prior_scale, xps_model, xrd_model)
-from .smc import (CudaError, ModelChoice, RunReport, Session, SmcConfig, probe_mufu, device_count, energies, energy, ess,
+from .smc import (Comm, CudaError, ModelChoice, RunReport, Session, SmcConfig, probe_mufu, device_count, energies, energy, ess,
                   launch_shape, log_mean_exp, model_select, next_beta, predict_step_size, smc_run, smc_run_batch,
-                  stats, stats_reset, systematic_resample, validate_smc_config)
+                  stats, stats_reset, systematic_resample, validate_smc_config, smc_run_sharded)
 
 __all__ = [
     "GammaPrior", "GaussianApproxPoissonNoise", "GaussianFixedNoise", "ModelSpec", "NormalPrior", "PoissonNoise",
     "ScalarParam", "Spectrum", "UniformPrior", "XpsHeteroNoise", "gm_model", "model_dim", "offset_model",
     "prior_scale", "xps_model", "xrd_model", "PhaseRef", "Reflection", "CudaError", "ModelChoice", "RunReport", "Session", "SmcConfig", "probe_mufu", "device_count", "energies",
     "energy", "ess", "launch_shape", "log_mean_exp", "model_select", "next_beta", "predict_step_size", "smc_run",
-    "smc_run_batch", "stats", "stats_reset", "systematic_resample", "validate_smc_config",
+    "smc_run_batch", "smc_run_sharded", "Comm", "stats", "stats_reset", "systematic_resample", "validate_smc_config",
 ]

@@ -52,7 +52,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if failed:
         raise RuntimeError("nvcc failed")
     tmp = LIB.with_suffix(".so.tmp")
-    subprocess.run([NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"], check=True)
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart", "-ldl"], check=True)
     os.replace(tmp, LIB)
     for o in objs:
         o.unlink(missing_ok=True)

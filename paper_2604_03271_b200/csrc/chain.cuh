@@ -548,7 +548,7 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
   const double beta = st->beta;
   const double nd = g.n_data;
   const int adapt_sweeps = (n + 1) / 2;  // smc.cpp:136
-  const uint32_t cg = g.chain_base + (uint32_t)c;
+  const uint32_t cg = g.chain_base + (uint32_t)(st->chain_lo + c);  // global chain id
   double* thn = g.theta[cur ^ 1];
   double* En = g.E[cur ^ 1];
   // components inside a block (everything but the xps Shirley endpoints and the offset family)
@@ -755,7 +755,7 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   mbar_wait(bar, 0);
 
   const int c = cta_in_group * U + unit;
-  const int units = ENERGY ? g.T : g.S;
+  const int units = ENERGY ? g.st->T_loc : g.st->S_loc;  // == T, S unless the run is particle-sharded
   if (c >= units) return;  // the whole unit leaves; no CTA-wide barrier follows
 
   Unit<PPL, W> u;

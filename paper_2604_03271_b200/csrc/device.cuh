@@ -39,7 +39,9 @@ struct GroupState {  // mutable per-group scalars; read back by the host every r
   int active;
   int error;
   int hist_count;
-  int pad;
+  int T_loc;     // particles held by this group (== T unless the run is particle-sharded)
+  int S_loc;     // chains of the current level held by this group
+  int chain_lo;  // global index of its first chain (Philox stream: chain_base + chain_lo + c)
   unsigned long long trials;
 };
 
@@ -50,6 +52,8 @@ constexpr int kMaxSlices = 512;
 struct TemperScratch {
   double emin, lo, hi, full, beta_next;
   double m, lse, u;
+  double base;                 // global CDF offset of this group's first particle (sharded runs)
+  long long shard_lo, shard_hi;  // global chain range [lo, hi) resolved by this group
   int it, done, err, pad;
   unsigned int counter, pad2;
   double part[kMaxSlices][2];
@@ -63,6 +67,13 @@ struct GroupDesc {  // immutable per group
   uint32_t key0, key1;
   uint32_t chain_base;  // global chain offset (multi-GPU invariance)
   int N;                // real points
+  // particle sharding (shard.cu): this group is one shard of a run whose T and
+  // S are global; its level-0 particles are global ids [pbase, pbase + T_loc)
+  int sharded;
+  int pbase;
+  int shard, nshards;  // this shard's index and the shard count of the run
+  double* xbuf;        // [2] cross-shard exchange of the tempering phases
+  double* xgat;        // [nshards][2] gathered (weight total, particle count) per shard
   // energy: E = e_a0 + e_a1 * sum(l_k); device noise parameters
   double e_a0, e_a1;
   float nz_a0, nz_a1, nz_a2, nz_q;
@@ -98,7 +109,7 @@ struct GroupDesc {  // immutable per group
   TemperScratch* ts;  // grid-level tempering (large T)
   int nslices;        // slices of the grid-level tempering (0: single-CTA path)
   int slice_len;
-  double* stat_acc;   // [d] per-component accept sums of the level (k_stats_grid)
+  double* stat_acc;   // [2d] per-component accept sums and log-step sums of the level (k_stats_grid)
 };
 
 // ----------------------------------------------------------------- Philox4x32-10

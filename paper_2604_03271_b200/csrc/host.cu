@@ -26,6 +26,9 @@
 #include <tuple>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is resolved at run time (dlopen), see NcclApi
+
 #include "../../include/specmc_b200.h"
 #include "launch.h"
 
@@ -414,6 +417,10 @@ struct RunSpec {
   specmc_smc_config cfg;
   double x_shift;
   int64_t N;
+  // particle sharding (shard.cu): shard `shard` of `nshards` holds T_loc0 of the
+  // T level-0 particles, global ids [pbase, pbase + T_loc0)
+  int shard = 0, nshards = 1;
+  int64_t T_loc0 = 0, pbase = 0;
 };
 
 struct Device {
@@ -471,7 +478,9 @@ struct ClassRun {
   int *d_list = nullptr, *d_prefix = nullptr, *d_list_all = nullptr, *d_prefix_all = nullptr;
   int *d_list_small = nullptr, *d_list_big = nullptr;
   int max_slices = 0;
+  Exchange* xch = nullptr;  // non-null: the groups are shards of particle-sharded runs
   std::vector<GroupDesc> gds;
+  std::vector<int64_t> runs_T0;  // level-0 particles per group
   std::vector<int> order;
   GroupState* h_st = nullptr;
   int* h_list = nullptr;
@@ -523,9 +532,10 @@ struct ClassRun {
       bytes += Arena::al(S * 4) + Arena::al(d * sp * 4) + Arena::al(d * sp * 8);
       bytes += Arena::al(T * 8) + Arena::al(kHist * (1 + 2 * d) * 8);
       bytes += Arena::al((size_t)R.cfg.max_levels * 4 * 8);
-      bytes += Arena::al(d * 8);                                                // stat_acc
+      bytes += Arena::al(2 * d * 8);                                            // stat_acc
+      bytes += Arena::al(2 * 8) + Arena::al(2 * 8 * (size_t)R.nshards);        // xbuf, xgat
       bytes += Arena::al(R.refl.size() * 4 + 8) + Arena::al(R.refl_off.size() * 4 + 4);  // xrd reflections
-      if (T > kGridTemperT) bytes += Arena::al(sizeof(TemperScratch));         // grid tempering
+      if (T > kGridTemperT || xch) bytes += Arena::al(sizeof(TemperScratch));  // grid tempering
     }
     ar.reserve(bytes, dev.ordinal, dev.stream);
     d_gds = ar.take<GroupDesc>(G);
@@ -549,8 +559,10 @@ struct ClassRun {
       dspec[kv.first] = std::make_tuple(x, c, y);
     }
     gds.resize(G);
+    runs_T0.resize(G);
     for (int gi = 0; gi < G; ++gi) {
       const RunSpec& R = runs[idx[gi]];
+      runs_T0[gi] = R.nshards > 1 || xch ? R.T_loc0 : (int64_t)R.cfg.T;
       const auto key = std::make_pair(R.spectrum, R.x_shift);
       const PreparedSpectrum& ps = prep.at(key);
       GroupDesc& g = gds[gi];
@@ -608,7 +620,13 @@ struct ClassRun {
       g.hist = ar.take<double>(kHist * (1 + 2 * d));
       g.diag = ar.take<double>((size_t)R.cfg.max_levels * 4);
       g.st = d_st + gi;
-      g.stat_acc = ar.take<double>(d);
+      g.stat_acc = ar.take<double>(2 * d);
+      g.sharded = xch ? 1 : 0;
+      g.shard = R.shard;
+      g.nshards = R.nshards;
+      g.pbase = (int)R.pbase;
+      g.xbuf = ar.take<double>(2);
+      g.xgat = ar.take<double>(2 * (size_t)R.nshards);
       if (!R.refl.empty()) {
         float2* rf = ar.take<float2>(R.refl.size() / 2);
         int* ro = ar.take<int>(R.refl_off.size());
@@ -617,7 +635,7 @@ struct ClassRun {
         g.refl = rf;
         g.refl_off = ro;
       }
-      if (T > kGridTemperT) {  // grid-level tempering: slices of <= 512 x slice_len particles
+      if (T > kGridTemperT || xch) {  // grid-level tempering: slices of <= 512 x slice_len particles
         g.ts = ar.take<TemperScratch>(1);
         size_t sl = std::max<size_t>(32768, (T + kMaxSlices - 1) / kMaxSlices);
         sl = (sl + 1023) & ~(size_t)1023;
@@ -644,7 +662,7 @@ struct ClassRun {
     for (int gi : groups) {
       list.push_back(gi);
       prefix.push_back(total);
-      const int units = energy ? gds[gi].T : gds[gi].S;
+      const int units = energy ? (int)runs_T0[gi] : h_st[gi].S_loc;
       total += (units + shape.U - 1) / shape.U;
     }
     prefix.push_back(total);
@@ -655,9 +673,14 @@ struct ClassRun {
   void run(Device& dev) {
     cudaStream_t st = dev.stream;
     std::vector<GroupState> sts(G);
-    for (auto& s : sts) {
+    for (int gi = 0; gi < G; ++gi) {
+      GroupState& s = sts[gi];
       std::memset(&s, 0, sizeof(s));
       s.active = 1;
+      s.T_loc = (int)runs_T0[gi];
+      s.S_loc = gds[gi].S;
+      s.chain_lo = 0;
+      h_st[gi] = s;
     }
     Timer whole, mv;
     cuda_check(cudaEventRecord(whole.a, st), "event");
@@ -674,7 +697,43 @@ struct ClassRun {
     std::vector<int> active = order;
     double move_ms = 0.0;
     int64_t move_launches = 0;
-    while (!active.empty()) {
+    while (!active.empty() && xch) {
+      // particle-sharded level: every shard of the run takes part in every exchange.
+      // The chains a shard resolves are known only after its tempering, so the
+      // move grid is sized from a read-back of the shard states.
+      dev.sync();
+      std::copy(active.begin(), active.end(), h_list + 3 * (G + 1));
+      h2d(d_list_big, h_list + 3 * (G + 1), active.size(), st);
+      cuda_check(launch_temper_sharded(d_gds, d_list_big, (int)active.size(), max_slices, *xch, st),
+                 "k_tp_* (sharded)");
+      count_launch(temper_sharded_launches());
+      d2h(h_st, d_st, G, st);
+      dev.sync();
+      bool alive = true;
+      for (int gi : active) alive = alive && h_st[gi].active;
+      if (!alive) break;  // an error ends the run on every shard (identical global state)
+      total = build_list(active, false, list, prefix);
+      const int na = (int)list.size();
+      std::memcpy(h_list, list.data(), sizeof(int) * na);
+      std::memcpy(h_list + (G + 1), prefix.data(), sizeof(int) * (na + 1));
+      h2d(d_list, h_list, na, st);
+      h2d(d_prefix, h_list + (G + 1), na + 1, st);
+      cuda_check(cudaEventRecord(mv.a, st), "event");
+      if (total > 0)
+        cuda_check(launch_move(family, noise, shape, dmax, d_gds, d_list, d_prefix, na, total, st), "k_chain<move>");
+      cuda_check(cudaEventRecord(mv.b, st), "event");
+      cuda_check(launch_stats_sharded(d_gds, d_list, na, dmax, *xch, st), "k_stats (sharded)");
+      count_launch(4);
+      d2h(h_st, d_st, G, st);
+      dev.sync();
+      move_ms += mv.ms();
+      ++move_launches;
+      std::vector<int> next;
+      for (int gi : active)
+        if (h_st[gi].active) next.push_back(gi);
+      active.swap(next);
+    }
+    while (!active.empty() && !xch) {
       total = build_list(active, false, list, prefix);
       const int na = (int)list.size();
       std::vector<int> small, big;
@@ -728,12 +787,12 @@ struct ClassRun {
       const RunSpec& R = runs[idx[gi]];
       specmc_smc_result& o = out[idx[gi]];
       const GroupState& s = h_st[gi];
-      const size_t T = R.cfg.T, d = R.m.d;
+      const size_t T = (size_t)s.T_loc, d = R.m.d;  // T_loc == T unless sharded
       o.d = (int)d;
       o.T = (int64_t)T;
       o.levels = s.level;
       o.trials = (int64_t)s.trials;
-      o.proposals = (int64_t)T * (int64_t)d * s.level;
+      o.proposals = (int64_t)R.cfg.T * (int64_t)d * s.level;
       o.device_seconds = device_seconds;
       if (s.error != GE_NONE) {
         o.status = SPECMC_ERUNTIME;
@@ -895,6 +954,148 @@ int run_batch(int n_problems, const specmc_problem* problems, int n_spectra, con
   return first;
 }
 
+// ------------------------------------------------------ particle sharding
+// Shards resident on this device: the exchanges are kernels over their descriptors.
+struct VirtualExchange : Exchange {
+  const ClassRun* cr;
+  explicit VirtualExchange(const ClassRun* c) : cr(c) {}
+  cudaError_t reduce(int buf, int count, int op, cudaStream_t st) override {
+    return launch_xreduce(cr->d_gds, cr->d_list_all, cr->G, buf, count, op, st);
+  }
+  cudaError_t gather(cudaStream_t st) override { return launch_xgather(cr->d_gds, cr->d_list_all, cr->G, st); }
+};
+
+// NCCL, resolved with dlopen so that the library has no link-time NCCL
+// dependency and shares the copy a host process (e.g. torch) already loaded
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*ErrorString)(ncclResult_t) = nullptr;
+  static NcclApi& get() {
+    static NcclApi api = [] {
+      NcclApi a;
+      a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+      if (!a.h) a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (!a.h) a.h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+      if (!a.h) return a;
+      a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(a.h, "ncclGetUniqueId"));
+      a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(a.h, "ncclCommInitRank"));
+      a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(a.h, "ncclAllReduce"));
+      a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(a.h, "ncclAllGather"));
+      a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(a.h, "ncclCommDestroy"));
+      a.ErrorString = reinterpret_cast<decltype(a.ErrorString)>(dlsym(a.h, "ncclGetErrorString"));
+      return a;
+    }();
+    if (!api.h || !api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.AllGather || !api.CommDestroy)
+      throw Error(SPECMC_ECOMM, "NCCL (libnccl.so.2) is not available");
+    return api;
+  }
+  void check(ncclResult_t r, const char* what) const {
+    if (r != ncclSuccess)
+      throw Error(SPECMC_ECOMM, std::string(what) + ": " + (ErrorString ? ErrorString(r) : "nccl error"));
+  }
+};
+
+struct CommImpl {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1, device = 0;
+};
+
+// One shard per rank: the exchanges are NCCL collectives on the shard's buffers,
+// enqueued on the level stream (no host round trip inside a level)
+struct NcclExchange : Exchange {
+  const ClassRun* cr;
+  CommImpl* c;
+  NcclExchange(const ClassRun* r, CommImpl* cc) : cr(r), c(cc) {}
+  cudaError_t reduce(int buf, int count, int op, cudaStream_t st) override {
+    NcclApi& api = NcclApi::get();
+    double* p = buf == 0 ? cr->gds[0].xbuf : cr->gds[0].stat_acc;
+    const ncclRedOp_t o = op == XOP_SUM ? ncclSum : (op == XOP_MIN ? ncclMin : ncclMax);
+    api.check(api.AllReduce(p, p, (size_t)count, ncclFloat64, o, c->comm, st), "ncclAllReduce");
+    return cudaSuccess;
+  }
+  cudaError_t gather(cudaStream_t st) override {
+    NcclApi& api = NcclApi::get();
+    api.check(api.AllGather(cr->gds[0].xbuf, cr->gds[0].xgat, 2, ncclFloat64, c->comm, st), "ncclAllGather");
+    return cudaSuccess;
+  }
+};
+
+// Particle-sharded smc_run: the T particles of one run are
+// split over nshards shards; comm == nullptr runs all of them on this device.
+// Results: F, ladder and diagnostics are global (identical on every shard);
+// the posterior holds this process's particles (all of them for virtual shards).
+int run_sharded(const specmc_model_desc& m, const double* xs, const double* ys, int64_t n_points,
+                const specmc_smc_config& cfg, int n_virtual, CommImpl* comm, specmc_smc_result* out) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const int nsh = comm ? comm->world : n_virtual;
+  if (nsh < 1) throw Error(SPECMC_EINVAL, "sharded run: shard count must be >= 1");
+  if (cfg.T % nsh != 0) throw Error(SPECMC_EINVAL, "sharded run: T must be divisible by the shard count");
+  if (comm && cfg.device != comm->device)
+    throw Error(SPECMC_EINVAL, "sharded run: cfg.device differs from the communicator's device");
+  specmc_spectrum sp{xs, ys, n_points};
+  std::vector<RunSpec> runs;
+  const int first = comm ? comm->rank : 0, count = comm ? 1 : nsh;
+  for (int r = first; r < first + count; ++r) {
+    RunSpec R = make_runspec(m, 0, cfg, sp);
+    R.shard = r;
+    R.nshards = nsh;
+    R.T_loc0 = cfg.T / nsh;
+    R.pbase = (int64_t)r * (cfg.T / nsh);
+    runs.push_back(std::move(R));
+  }
+  Device dev(cfg.device);
+  std::vector<specmc_spectrum> spectra{sp};
+  ClassRun cr;
+  cr.idx.resize(runs.size());
+  std::iota(cr.idx.begin(), cr.idx.end(), 0);
+  std::unique_ptr<Exchange> x;
+  if (comm)
+    x = std::make_unique<NcclExchange>(&cr, comm);
+  else
+    x = std::make_unique<VirtualExchange>(&cr);
+  cr.xch = x.get();
+  cr.prepare(dev, runs, spectra);
+  cr.run(dev);
+  std::vector<specmc_smc_result> res(runs.size());
+  for (auto& r : res) std::memset(&r, 0, sizeof(r));
+  cr.fetch(dev, runs, res.data());
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  // merge this process's shards into one result (shard order)
+  std::memset(out, 0, sizeof(*out));
+  specmc_smc_result& o = *out;
+  o = res[0];
+  int64_t Ttot = 0, trials = 0;
+  for (auto& r : res) {
+    Ttot += r.T;
+    trials += r.trials;
+    if (r.status != SPECMC_OK) o.status = r.status;
+  }
+  o.trials = trials;
+  o.T = Ttot;
+  o.proposals = (int64_t)cfg.T * m.d * o.levels * count / nsh;
+  o.wall_seconds = wall;
+  if (o.status == SPECMC_OK && res.size() > 1) {
+    const size_t d = m.d;
+    o.posterior = static_cast<double*>(std::malloc(sizeof(double) * d * std::max<int64_t>(Ttot, 1)));
+    o.energies = static_cast<double*>(std::malloc(sizeof(double) * std::max<int64_t>(Ttot, 1)));
+    size_t at = 0;
+    for (auto& r : res) {
+      std::memcpy(o.posterior + at * d, r.posterior, sizeof(double) * d * r.T);
+      std::memcpy(o.energies + at, r.energies, sizeof(double) * r.T);
+      at += r.T;
+    }
+    std::free(res[0].posterior);
+    std::free(res[0].energies);
+    for (size_t i = 1; i < res.size(); ++i) specmc_result_free(&res[i]);
+  }
+  return o.status;
+}
+
 template <typename F>
 int guarded(char* err, size_t errlen, F&& f) {
   try {
@@ -983,6 +1184,62 @@ int specmc_session_fetch(specmc_session* s, specmc_smc_result* out, char* err, s
 }
 
 void specmc_session_destroy(specmc_session* s) { delete reinterpret_cast<Session*>(s); }
+
+int specmc_smc_run_sharded(const specmc_model_desc* model, const double* xs, const double* ys, int64_t n_points,
+                           const specmc_smc_config* cfg, int32_t n_virtual, specmc_comm* comm,
+                           specmc_smc_result* out, char* err, size_t errlen) {
+  if (out) std::memset(out, 0, sizeof(*out));
+  return guarded(err, errlen, [&]() -> int {
+    if (!model || !cfg || !out) throw Error(SPECMC_EINVAL, "null argument");
+    const int rc = run_sharded(*model, xs, ys, n_points, *cfg, n_virtual, reinterpret_cast<CommImpl*>(comm), out);
+    if (rc != SPECMC_OK)
+      copy_err(err, errlen, "smc: max_levels exceeded before reaching beta = 1 (or total weight is zero)");
+    return rc;
+  });
+}
+
+int specmc_nccl_unique_id(uint8_t* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> int {
+    if (!out) throw Error(SPECMC_EINVAL, "null argument");
+    NcclApi& api = NcclApi::get();
+    ncclUniqueId id;
+    api.check(api.GetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == SPECMC_COMM_ID_BYTES, "ncclUniqueId size");
+    std::memcpy(out, &id, sizeof(id));
+    return SPECMC_OK;
+  });
+}
+
+int specmc_comm_init_nccl(int32_t rank, int32_t world, const uint8_t* id, int32_t device, specmc_comm** out,
+                          char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> int {
+    if (!id || !out) throw Error(SPECMC_EINVAL, "null argument");
+    if (world < 1 || rank < 0 || rank >= world) throw Error(SPECMC_EINVAL, "comm: bad rank / world size");
+    Device dev(device);
+    NcclApi& api = NcclApi::get();
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    auto c = std::make_unique<CommImpl>();
+    c->rank = rank;
+    c->world = world;
+    c->device = device;
+    api.check(api.CommInitRank(&c->comm, world, uid, rank), "ncclCommInitRank");
+    *out = reinterpret_cast<specmc_comm*>(c.release());
+    return SPECMC_OK;
+  });
+}
+
+void specmc_comm_destroy(specmc_comm* c) {
+  auto* p = reinterpret_cast<CommImpl*>(c);
+  if (!p) return;
+  if (p->comm) {
+    try {
+      NcclApi::get().CommDestroy(p->comm);
+    } catch (...) {
+    }
+  }
+  delete p;
+}
 
 void specmc_result_free(specmc_smc_result* r) {
   if (!r) return;
@@ -1098,6 +1355,8 @@ int specmc_energy_batch(const specmc_model_desc* model, const double* xs, const 
     g.refl_off = ro;
     GroupState s;
     std::memset(&s, 0, sizeof(s));
+    s.T_loc = (int)T;
+    s.S_loc = (int)T;
     h2d(gd, &g, 1, st);
     h2d(gst, &s, 1, st);
     const int total = (int)((T + shape.U - 1) / shape.U);

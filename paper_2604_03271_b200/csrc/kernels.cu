@@ -44,10 +44,10 @@ __device__ double gamma_draw(double shape, double rate, uint32_t p, uint32_t& se
 __global__ void k_init_draw(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
   const GroupDesc& g = gds[list[blockIdx.y]];
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= g.T) return;
+  if (p >= g.st->T_loc) return;
   double* th = g.theta[0];
   uint32_t seq = 0;
-  const uint32_t pid = g.chain_base * 0u + (uint32_t)p;
+  const uint32_t pid = (uint32_t)(g.pbase + p);  // global particle id (sharded runs: shard offset)
   for (int i = 0; i < g.d; ++i) {
     const int kind = g.pkind[i];
     const double a = g.pa[i], b = g.pb[i];
@@ -432,13 +432,106 @@ struct SliceCtx {
   int64_t i0, i1;
 };
 
+// slice blockIdx.x of the group's current particles [0, T_loc); trailing
+// slices of a sharded group may be empty (i0 == i1) but still take part
 __device__ __forceinline__ bool slice_ctx(const GroupDesc* gds, const int* list, SliceCtx& c) {
   c.g = &gds[list[blockIdx.y]];
   c.ts = c.g->ts;
   if ((int)blockIdx.x >= c.g->nslices) return false;
+  const int64_t T = c.g->st->T_loc;
   c.i0 = (int64_t)blockIdx.x * c.g->slice_len;
-  c.i1 = c.i0 + c.g->slice_len < c.g->T ? c.i0 + c.g->slice_len : c.g->T;
+  if (c.i0 > T) c.i0 = T;
+  c.i1 = c.i0 + c.g->slice_len < T ? c.i0 + c.g->slice_len : T;
   return true;
+}
+
+// ---- finalisers: run by the last slice block of a launch for an unsharded
+// group, or by k_tpf_* after the cross-shard exchange (shard.cu) with the
+// globally reduced values in g.xbuf
+__device__ void fin_emin(const GroupDesc& g, TemperScratch* ts, double e) {
+  ts->emin = isfinite(e) ? e : 0.0;
+  ts->full = 1.0 - g.st->beta;
+  ts->lo = 0.0;
+  ts->hi = ts->full;
+  ts->it = -1;
+  ts->done = 0;
+  ts->err = 0;
+}
+__device__ void fin_ess(const GroupDesc& g, TemperScratch* ts, double s1, double s2) {
+  GroupState* st = g.st;
+  const double delta = ts->it < 0 ? ts->full : 0.5 * (ts->lo + ts->hi);
+  if (!(s1 > 0.0)) {  // ess: total weight is zero (smc.cpp:63)
+    ts->err = 1;
+    st->error = GE_ZERO_WEIGHT;
+    st->active = 0;
+    return;
+  }
+  const double r = (s1 * s1 / s2) / (double)g.T;
+  if (ts->it < 0) {
+    if (r >= g.ess_target) {
+      ts->beta_next = 1.0;
+      ts->done = 1;
+    } else {
+      ts->it = 0;
+    }
+  } else {
+    ts->it += 1;
+    if (fabs(r - g.ess_target) <= 1e-6 || ts->it >= 60) {
+      ts->beta_next = st->beta + delta;
+      ts->done = 1;
+    } else if (r > g.ess_target) {
+      ts->lo = delta;
+    } else {
+      ts->hi = delta;
+    }
+  }
+}
+__device__ void fin_wmax(const GroupDesc& g, TemperScratch* ts, double mm) {
+  ts->m = mm;
+  if (mm == -dinf()) {
+    ts->err = 1;
+    g.st->error = GE_ZERO_WEIGHT;
+    g.st->active = 0;
+  }
+}
+__device__ void fin_wsum(const GroupDesc& g, TemperScratch* ts, double s1, double s2) {
+  GroupState* st = g.st;
+  const double lse = ts->m + log(s1);
+  const double lmw = lse - log((double)g.T);
+  ts->lse = lse;
+  double* dg = g.diag + (size_t)st->level * 4;
+  dg[0] = ts->beta_next;
+  dg[1] = (s1 * s1 / s2) / (double)g.T;
+  dg[2] = lmw;
+  st->neg_log_z -= lmw;
+  const u32x4 o = philox(u32x4{0u, (uint32_t)(st->level + 1), 0u, ROLE_RESAMPLE}, g.key0, g.key1);
+  ts->u = u53(o.x, o.y);
+}
+// this group's global chain range from the gathered (weight total, particle
+// count) of every shard in shard order: CDF base = sequential sum of the
+// earlier totals; the first shard holding particles starts at chain 0 and the
+// last one takes the rounding tail up to S (the reference's tail goes to the
+// last particle, smc.cpp:100-112)
+__device__ void fin_offsets(const GroupDesc& g, TemperScratch* ts, const double* gat, int nsh, int me) {
+  double base = 0.0, mine = 0.0;
+  int first = -1, last = -1;
+  for (int r = 0; r < nsh; ++r) {
+    if (r < me) base += gat[2 * r];
+    if (r == me) mine = gat[2 * r];
+    if (gat[2 * r + 1] > 0.0) {
+      if (first < 0) first = r;
+      last = r;
+    }
+  }
+  const long long S = g.S;
+  ts->base = base;
+  if (g.st->T_loc == 0) {
+    ts->shard_lo = ts->shard_hi = 0;
+    return;
+  }
+  ts->shard_lo = me == first ? 0 : count_le(base, ts->u, S);
+  ts->shard_hi = me == last ? S : count_le(base + mine, ts->u, S);
+  if (ts->shard_hi < ts->shard_lo) ts->shard_hi = ts->shard_lo;
 }
 
 __global__ void __launch_bounds__(kGridThreads) k_tp_emin(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
@@ -464,14 +557,12 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_emin(const GroupDesc* __res
   if (last_block(&ts->counter, g.nslices) && threadIdx.x == 0) {
     double e = dinf();
     for (int s = 0; s < g.nslices; ++s) e = ts->part[s][0] < e ? ts->part[s][0] : e;
-    ts->emin = isfinite(e) ? e : 0.0;
-    ts->full = 1.0 - st->beta;
-    ts->lo = 0.0;
-    ts->hi = ts->full;
-    ts->it = -1;
-    ts->done = 0;
-    ts->err = 0;
     ts->counter = 0;
+    ts->err = 0;
+    if (g.sharded)
+      g.xbuf[0] = e;
+    else
+      fin_emin(g, ts, e);
   }
 }
 
@@ -505,30 +596,11 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_ess(const GroupDesc* __rest
       s2 += ts->part[s][1];
     }
     ts->counter = 0;
-    if (!(s1 > 0.0)) {  // ess: total weight is zero (smc.cpp:63)
-      ts->err = 1;
-      st->error = GE_ZERO_WEIGHT;
-      st->active = 0;
-      return;
-    }
-    const double r = (s1 * s1 / s2) / (double)g.T;
-    if (ts->it < 0) {
-      if (r >= g.ess_target) {
-        ts->beta_next = 1.0;
-        ts->done = 1;
-      } else {
-        ts->it = 0;
-      }
+    if (g.sharded) {
+      g.xbuf[0] = s1;
+      g.xbuf[1] = s2;
     } else {
-      ts->it += 1;
-      if (fabs(r - g.ess_target) <= 1e-6 || ts->it >= 60) {
-        ts->beta_next = st->beta + delta;
-        ts->done = 1;
-      } else if (r > g.ess_target) {
-        ts->lo = delta;
-      } else {
-        ts->hi = delta;
-      }
+      fin_ess(g, ts, s1, s2);
     }
   }
 }
@@ -551,13 +623,11 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_wmax(const GroupDesc* __res
   if (last_block(&ts->counter, g.nslices) && threadIdx.x == 0) {
     double mm = -dinf();
     for (int s = 0; s < g.nslices; ++s) mm = fmax(mm, ts->part[s][0]);
-    ts->m = mm;
     ts->counter = 0;
-    if (mm == -dinf()) {
-      ts->err = 1;
-      g.st->error = GE_ZERO_WEIGHT;
-      g.st->active = 0;
-    }
+    if (g.sharded)
+      g.xbuf[0] = mm;
+    else
+      fin_wmax(g, ts, mm);
   }
 }
 
@@ -591,16 +661,12 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_wsum(const GroupDesc* __res
       s2 += ts->part[s][1];
     }
     ts->counter = 0;
-    const double lse = m + log(s1);
-    const double lmw = lse - log((double)g.T);
-    ts->lse = lse;
-    double* dg = g.diag + (size_t)st->level * 4;
-    dg[0] = ts->beta_next;
-    dg[1] = (s1 * s1 / s2) / (double)g.T;
-    dg[2] = lmw;
-    st->neg_log_z -= lmw;
-    const u32x4 o = philox(u32x4{0u, (uint32_t)(st->level + 1), 0u, ROLE_RESAMPLE}, g.key0, g.key1);
-    ts->u = u53(o.x, o.y);
+    if (g.sharded) {
+      g.xbuf[0] = s1;
+      g.xbuf[1] = s2;
+    } else {
+      fin_wsum(g, ts, s1, s2);
+    }
   }
 }
 
@@ -632,11 +698,20 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_offsets(const GroupDesc* __
       ts->offs[s + 1] = o;
     }
     ts->counter = 0;
+    if (g.sharded) {  // exchanged as (weight total, particle count) pairs
+      g.xbuf[0] = o;
+      g.xbuf[1] = (double)st->T_loc;
+    } else {
+      const double me[2] = {o, (double)st->T_loc};
+      fin_offsets(g, ts, me, 1, 0);
+    }
   }
 }
 
 // systematic resampling over the slices, then (last block) the step-size
-// prediction for the level and the state advance
+// prediction for the level and the state advance.  A slice resolves the
+// targets whose positions fall in its CDF range; the group's last non-empty
+// slice takes everything up to the group's range end.
 __global__ void __launch_bounds__(kGridThreads) k_tp_resample(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
   __shared__ TemperShared sh;
   SliceCtx c;
@@ -646,11 +721,19 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_resample(const GroupDesc* _
   if (ts->err) return;
   GroupState* st = g.st;
   const long long S = g.S;
-  const double u = ts->u;
+  const double u = ts->u, base = ts->base;
   const int s = blockIdx.x;
-  const long long lo_b = s == 0 ? 0 : count_le(ts->offs[s], u, S);
-  const long long hi_b = s == g.nslices - 1 ? S : count_le(ts->offs[s + 1], u, S);
-  block_resample_range(g.wbuf + c.i0, c.i1 - c.i0, ts->offs[s], lo_b, hi_b > lo_b ? hi_b : lo_b, S, u, g.anc, c.i0, sh);
+  const int64_t T = st->T_loc;
+  const int s_last = T > 0 ? (int)((T - 1) / g.slice_len) : -1;
+  const long long glo = ts->shard_lo, ghi = ts->shard_hi;
+  if (s <= s_last && ghi > glo) {
+    long long lo_b = s == 0 ? glo : count_le(base + ts->offs[s], u, S);
+    long long hi_b = s == s_last ? ghi : count_le(base + ts->offs[s + 1], u, S);
+    lo_b = lo_b < glo ? glo : (lo_b > ghi ? ghi : lo_b);
+    hi_b = hi_b < lo_b ? lo_b : (hi_b > ghi ? ghi : hi_b);
+    // local chain j - glo draws its start from local particle c.i0 + k
+    block_resample_range(g.wbuf + c.i0, c.i1 - c.i0, base + ts->offs[s], lo_b, hi_b, S, u, g.anc - glo, c.i0, sh);
+  }
   if (last_block(&ts->counter, g.nslices)) {
     for (int i = threadIdx.x; i < g.d; i += blockDim.x)
       g.ls0[i] = predict_log_step(g.hist, st->hist_count, g.d, i, ts->beta_next, g.pkind[i], g.pa[i], g.pb[i]);
@@ -658,20 +741,46 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_resample(const GroupDesc* _
     if (threadIdx.x == 0) {
       st->beta = ts->beta_next;
       st->level = st->level + 1;
+      st->S_loc = (int)(ghi - glo);
+      st->chain_lo = (int)glo;
+      st->T_loc = st->S_loc * g.n;
       ts->counter = 0;
     }
   }
 }
 
-// step-size statistics, one CTA per (component, group) (smc.cpp:162-179), then
-// k_stats_final: history entry, level acceptance, buffer flip
+// cross-shard finalisers (one thread per listed group), after the exchange
+__global__ void k_tpf_emin(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
+  const GroupDesc& g = gds[list[blockIdx.x]];
+  if (threadIdx.x == 0 && !g.ts->err) fin_emin(g, g.ts, g.xbuf[0]);
+}
+__global__ void k_tpf_ess(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
+  const GroupDesc& g = gds[list[blockIdx.x]];
+  if (threadIdx.x == 0 && !g.ts->done && !g.ts->err) fin_ess(g, g.ts, g.xbuf[0], g.xbuf[1]);
+}
+__global__ void k_tpf_wmax(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
+  const GroupDesc& g = gds[list[blockIdx.x]];
+  if (threadIdx.x == 0 && !g.ts->err) fin_wmax(g, g.ts, g.xbuf[0]);
+}
+__global__ void k_tpf_wsum(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
+  const GroupDesc& g = gds[list[blockIdx.x]];
+  if (threadIdx.x == 0 && !g.ts->err) fin_wsum(g, g.ts, g.xbuf[0], g.xbuf[1]);
+}
+__global__ void k_tpf_offsets(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
+  const GroupDesc& g = gds[list[blockIdx.x]];
+  if (threadIdx.x == 0 && !g.ts->err) fin_offsets(g, g.ts, g.xgat, g.nshards, g.shard);
+}
+
+// step-size statistics, one CTA per (component, group) (smc.cpp:162-179): sums
+// over this group's chains into stat_acc = (accepts[d], log-steps[d]); then
+// (after the cross-shard sum for sharded runs) k_stats_final: history entry,
+// level acceptance, buffer flip
 __global__ void __launch_bounds__(256) k_stats_grid(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
   __shared__ TemperShared sh;
   const GroupDesc& g = gds[list[blockIdx.y]];
   const int i = blockIdx.x;
   if (i >= g.d) return;
-  GroupState* st = g.st;
-  const int d = g.d, S = g.S;
+  const int S = g.st->S_loc;
   double a = 0.0, l = 0.0;
   for (int c = threadIdx.x; c < S; c += blockDim.x) {
     a += (double)g.chain_acc[(size_t)i * g.sp + c];
@@ -680,11 +789,8 @@ __global__ void __launch_bounds__(256) k_stats_grid(const GroupDesc* __restrict_
   a = block_reduce(a, sh.red, OpAdd(), 0.0);
   l = block_reduce(l, sh.red, OpAdd(), 0.0);
   if (threadIdx.x == 0) {
-    double* h = g.hist + (size_t)(st->hist_count % kHist) * (1 + 2 * d);
-    const double prop = (double)S * g.n;
-    h[1 + i] = prop > 0 ? a / prop : 0.0;
-    h[1 + d + i] = exp(l / (double)S);
     g.stat_acc[i] = a;
+    g.stat_acc[g.d + i] = l;
   }
 }
 
@@ -692,13 +798,19 @@ __global__ void k_stats_final(const GroupDesc* __restrict__ gds, const int* __re
   const GroupDesc& g = gds[list[blockIdx.x]];
   if (threadIdx.x != 0) return;
   GroupState* st = g.st;
-  const int d = g.d, S = g.S, H = st->hist_count;
+  const int d = g.d, S = g.S, H = st->hist_count;  // S: all chains of the level (every shard)
   double* h = g.hist + (size_t)(H % kHist) * (1 + 2 * d);
+  const double prop = (double)S * g.n;
   double acc_all = 0.0;
-  for (int i = 0; i < d; ++i) acc_all += g.stat_acc[i];
+  for (int i = 0; i < d; ++i) {
+    const double a = g.stat_acc[i];
+    h[1 + i] = prop > 0 ? a / prop : 0.0;
+    h[1 + d + i] = exp(g.stat_acc[d + i] / (double)S);
+    acc_all += a;
+  }
   const double beta = st->beta;
   h[0] = beta;
-  const double prop_all = (double)S * g.n * d;
+  const double prop_all = prop * d;
   g.diag[(size_t)(st->level - 1) * 4 + 3] = prop_all > 0 ? acc_all / prop_all : 0.0;
   st->hist_count = H + 1;
   st->cur ^= 1;
@@ -924,6 +1036,44 @@ cudaError_t launch_temper_grid(const GroupDesc* gds, const int* list, int n_list
   return cudaGetLastError();
 }
 int temper_grid_launches() { return 66; }
+
+cudaError_t launch_temper_sharded(const GroupDesc* gds, const int* list, int n_list, int max_slices, Exchange& x,
+                                  cudaStream_t st) {
+  const dim3 grid(max_slices, n_list);
+  cudaError_t e;
+#define SMC_X(CALL)                  \
+  if ((e = (CALL)) != cudaSuccess) return e;
+  k_tp_emin<<<grid, kGridThreads, 0, st>>>(gds, list);
+  SMC_X(x.reduce(0, 1, XOP_MIN, st));
+  k_tpf_emin<<<n_list, 32, 0, st>>>(gds, list);
+  for (int it = 0; it < 61; ++it) {
+    k_tp_ess<<<grid, kGridThreads, 0, st>>>(gds, list);
+    SMC_X(x.reduce(0, 2, XOP_SUM, st));
+    k_tpf_ess<<<n_list, 32, 0, st>>>(gds, list);
+  }
+  k_tp_wmax<<<grid, kGridThreads, 0, st>>>(gds, list);
+  SMC_X(x.reduce(0, 1, XOP_MAX, st));
+  k_tpf_wmax<<<n_list, 32, 0, st>>>(gds, list);
+  k_tp_wsum<<<grid, kGridThreads, 0, st>>>(gds, list);
+  SMC_X(x.reduce(0, 2, XOP_SUM, st));
+  k_tpf_wsum<<<n_list, 32, 0, st>>>(gds, list);
+  k_tp_offsets<<<grid, kGridThreads, 0, st>>>(gds, list);
+  SMC_X(x.gather(st));
+  k_tpf_offsets<<<n_list, 32, 0, st>>>(gds, list);
+  k_tp_resample<<<grid, kGridThreads, 0, st>>>(gds, list);
+#undef SMC_X
+  return cudaGetLastError();
+}
+int temper_sharded_launches() { return 2 * 66 - 1; }  // + one exchange per phase (kernels or NCCL)
+
+cudaError_t launch_stats_sharded(const GroupDesc* gds, const int* list, int n_list, int dmax, Exchange& x,
+                                 cudaStream_t st) {
+  k_stats_grid<<<dim3(dmax, n_list), 256, 0, st>>>(gds, list);
+  cudaError_t e = x.reduce(1, 2 * dmax, XOP_SUM, st);
+  if (e != cudaSuccess) return e;
+  k_stats_final<<<n_list, 32, 0, st>>>(gds, list);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_stats_grid(const GroupDesc* gds, const int* list, int n_list, int dmax, cudaStream_t st) {
   k_stats_grid<<<dim3(dmax, n_list), 256, 0, st>>>(gds, list);

@@ -55,6 +55,29 @@ cudaError_t launch_temper(const GroupDesc* d_gds, const int* d_list, int n_list,
 // resampling + step prediction (66 launches, each over (slices x groups))
 cudaError_t launch_temper_grid(const GroupDesc* d_gds, const int* d_list, int n_list, int max_slices, cudaStream_t st);
 int temper_grid_launches();
+// ---- particle sharding (shard.cu): one run's particles split over shards that
+// exchange a few scalars per tempering phase
+enum ExchangeOp : int { XOP_SUM = 0, XOP_MIN = 1, XOP_MAX = 2 };
+struct Exchange {
+  virtual ~Exchange() = default;
+  // reduce `count` doubles of every shard's g.xbuf (buf 0) or g.stat_acc (buf 1)
+  // across the shards of the run; every shard receives the result
+  virtual cudaError_t reduce(int buf, int count, int op, cudaStream_t st) = 0;
+  // every shard's (xbuf[0], xbuf[1]) into every shard's g.xgat, in shard order
+  virtual cudaError_t gather(cudaStream_t st) = 0;
+};
+// one sharded level's tempering: the k_tp_* phases with an exchange and a
+// k_tpf_* finaliser after each cross-shard reduction
+cudaError_t launch_temper_sharded(const GroupDesc* d_gds, const int* d_list, int n_list, int max_slices, Exchange& x,
+                                  cudaStream_t st);
+int temper_sharded_launches();
+cudaError_t launch_stats_sharded(const GroupDesc* d_gds, const int* d_list, int n_list, int dmax, Exchange& x,
+                                 cudaStream_t st);
+// exchange among shards resident on this device (one stream, kernels)
+cudaError_t launch_xreduce(const GroupDesc* d_gds, const int* d_list, int n, int buf, int count, int op,
+                           cudaStream_t st);
+cudaError_t launch_xgather(const GroupDesc* d_gds, const int* d_list, int n, cudaStream_t st);
+
 // step-size statistics, one CTA per (component, group), + per-group finalisation
 cudaError_t launch_stats_grid(const GroupDesc* d_gds, const int* d_list, int n_list, int dmax, cudaStream_t st);
 // step-size statistics + history + buffer flip (one CTA per group)

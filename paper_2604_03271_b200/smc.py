@@ -209,6 +209,74 @@ class Session:
             pass
 
 
+# ------------------------------------------------------- particle sharding
+class Comm:
+    """NCCL communicator with one shard per rank (specmc_comm_init_nccl).
+
+    ``Comm.from_torch(device)`` bootstraps it over an initialised
+    torch.distributed process group (rank 0 creates the id, a broadcast
+    shares it)."""
+
+    def __init__(self, rank: int, world: int, uid: bytes, device: int = 0):
+        if len(uid) != _lib.SPECMC_COMM_ID_BYTES:
+            raise ValueError("comm: unique id must be 128 bytes")
+        self.rank, self.world, self.device = rank, world, device
+        self._h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        rc = lib.specmc_comm_init_nccl(rank, world, uid, device, C.byref(self._h), err, 1024)
+        if rc:
+            _raise(rc, err)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(_lib.SPECMC_COMM_ID_BYTES)
+        err = C.create_string_buffer(512)
+        rc = lib.specmc_nccl_unique_id(buf, err, 512)
+        if rc:
+            _raise(rc, err)
+        return buf.raw
+
+    @classmethod
+    def from_torch(cls, device: int = 0) -> "Comm":
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        box = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        return cls(rank, world, box[0], device)
+
+    def close(self):
+        if self._h:
+            lib.specmc_comm_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def smc_run_sharded(spec: ModelSpec, data: Spectrum, cfg: SmcConfig, n_virtual: int = 1,
+                    comm: Optional[Comm] = None) -> RunReport:
+    """One run with its particles split over shards.
+
+    comm=None: ``n_virtual`` shards in this process on cfg.device (the
+    exchanges are device kernels); the report holds every particle.  With a
+    Comm: this rank's shard; F and the level diagnostics are global, the
+    posterior holds this rank's particles."""
+    desc, keep = spec.desc()
+    res = _lib.SmcResultC()
+    err = C.create_string_buffer(1024)
+    rc = lib.specmc_smc_run_sharded(C.byref(desc), _p(data.xs), _p(data.ys), len(data.xs), C.byref(cfg.c()),
+                                    int(n_virtual), comm._h if comm is not None else None, C.byref(res), err, 1024)
+    try:
+        if rc:
+            _raise(rc, err)
+        return _report(spec, cfg, len(data.xs), res)
+    finally:
+        lib.specmc_result_free(C.byref(res))
+
+
 def probe_mufu(device: int = 0) -> float:
     """Measured MUFU ex2 throughput (ops/s) of the device."""
     v = C.c_double()
