@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--T", type=int, default=None, help="override particle count (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard", default="trials", choices=["trials", "particles"],
+                    help="multi-GPU split: one model-selection trial per GPU (weak scaling, default) or one "
+                         "trial with every run's particles split across the GPUs (strong scaling, SURVEY 8e-3)")
     return ap.parse_args()
 
 
@@ -208,12 +211,7 @@ def run_ours(args, ws, rank, local):
     for _ in range(args.steps):
         flush.fill_(1.0)  # L2 flush between timed steps (outside the timed window)
         torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        sess.run()
-        b.record()
-        torch.cuda.synchronize()
-        elapsed += a.elapsed_time(b) * 1e-3
+        elapsed += sess.run()  # CUDA events on the session's launch stream, first to last kernel
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -309,11 +307,95 @@ def run_ours(args, ws, rank, local):
         dist.destroy_process_group()
 
 
+def run_particles(args, ws, rank, local):
+    """One model-selection trial whose every run is particle-sharded over the ws
+    GPUs (smc_run_sharded, NCCL exchanges): strong scaling of one workload."""
+    import torch
+    import paper_2604_03271_b200 as S
+    from paper_2604_03271_b200 import synthetic as syn
+
+    torch.cuda.set_device(local)
+    dist = None
+    comm = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = S.Comm.from_torch(local)
+    w = syn.config(args.config, args.T)
+    ks = list(range(w.k_range[0], w.k_range[1] + 1))
+    seed = syn.trial_seed(4242, 0)  # the same trial on every rank
+    cfgs = {K: S.SmcConfig(T=w.T, n=w.n, ess_target=0.5, seed=seed, device=local) for K in ks}
+    N = len(w.data.xs)
+    peak_mufu = S.probe_mufu(local)
+
+    def step():
+        dev, wall, evals, reps = 0.0, 0.0, 0, {}
+        for K in ks:
+            r = S.smc_run_sharded(w.spec(K), w.data, cfgs[K], n_virtual=1, comm=comm)
+            dev += r.device_seconds
+            wall += r.wall_seconds
+            evals += r.proposals
+            reps[K] = r
+        return dev, wall, evals, reps
+
+    for _ in range(args.warmup):
+        step()
+    clocks = Clocks(local)
+    S.stats_reset()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    elapsed = wall = 0.0
+    evals = 0
+    for _ in range(args.steps):
+        d, wl, e, reps = step()
+        elapsed += d
+        wall += wl
+        evals += e
+    clk = clocks.stop()
+    st = S.stats()
+    if dist:
+        from paper_2604_03271_b200 import dist as D
+        elapsed, evals = D.reduce_timing(elapsed, float(evals))
+        wall, _ = D.reduce_timing(wall, 0.0)
+    choice = S.model_select([(K, r) for K, r in reps.items()])
+    if rank == 0:
+        move_s = st["move_kernel_ms"] * 1e-3
+        pe_rate = st["point_evals"] / move_s if move_s > 0 else 0.0
+        mufu_pt = MUFU_SHAPE[w.family] + MUFU_NOISE[type(w.noise).__name__]
+        line = {
+            "metric": f"particle-likelihood evals/s (K=1..{ks[-1]} model selection, {args.config})",
+            "value": evals / elapsed, "unit": "evals/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed / args.steps * 1e3, "time_to_evidence_s": elapsed / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 point terms / f64 accumulation", "data": "synthetic",
+            "config": {"workload": f"{args.config}: N={N}, K={ks[0]}..{ks[-1]}, T={w.T} particles per run split "
+                                   f"over {ws} GPU(s), n={w.n}", "N": N, "K_range": [ks[0], ks[-1]], "T": w.T,
+                       "n": w.n, "l2": f"inputs larger than L2 ({w.T} particles x d fp64)",
+                       "parallelism": f"particles x{ws} (strong, NCCL per-level exchanges)"},
+            "K_selected": choice.K_best, "point_evals_per_s_move": pe_rate, "gpu_launches": st["kernel_launches"],
+            "roofline": {"bound": "sfu", "achieved": pe_rate * mufu_pt / 1e9, "peak": peak_mufu / 1e9,
+                         "unit": "Gop/s (MUFU)", "frac": pe_rate * mufu_pt / peak_mufu if peak_mufu else None,
+                         "traffic": None, "note": f"move kernel, rank 0; {mufu_pt:g} MUFU ops per point-eval"},
+            "clocks": clk,
+            "e2e": {"value": evals / wall, "unit": "evals/s", "h2d_bytes_per_step": 2 * N * 8,
+                    "d2h_bytes_per_step": int(sum(r.posterior.nbytes + r.energies.nbytes for r in reps.values()))},
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if dist:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     ws, rank, local = dist_init()
     if args.impl == "reference":
         run_reference(args, ws, rank)
+    elif args.shard == "particles":
+        run_particles(args, ws, rank, local)
     else:
         run_ours(args, ws, rank, local)
 
