@@ -436,6 +436,56 @@ class Ref:
     def trial_seed(self, base, trial) -> int:
         return self.lib.ref_trial_seed(base, trial)
 
+    # ---- output side (report.cpp, posterior.cpp)
+    def format_double(self, v) -> str:
+        buf = C.create_string_buffer(64)
+        self.lib.ref_format_double.argtypes = [C.c_double, C.c_char_p, C.c_int]
+        self.lib.ref_format_double(float(v), buf, 64)
+        return buf.value.decode()
+
+    def weighted_quantile(self, s, w, q) -> float:
+        s, w = _d(s), _d(w)
+        rc = C.c_int(0)
+        f = self.lib.ref_weighted_quantile
+        f.restype = C.c_double
+        f.argtypes = [_dp, _dp, C.c_int64, C.c_double, C.POINTER(C.c_int)]
+        v = f(_ptr(s), _ptr(w), len(s), float(q), C.byref(rc))
+        if rc.value:
+            raise ValueError("weighted_quantile")
+        return v
+
+    def sort_peak_blocks(self, post, block, center_off, n_blocks) -> np.ndarray:
+        P = np.ascontiguousarray(np.asarray(post, dtype=np.float64).T)  # draw-major
+        out = np.empty_like(P)
+        rc = self.lib.ref_sort_peak_blocks(_ptr(P), P.shape[1], P.shape[0], block, center_off, n_blocks, _ptr(out))
+        if rc:
+            raise ValueError("sort_peak_blocks")
+        return out.T.copy()
+
+    def write_report(self, path, sampler, label, F, diverged, wall, scalars, arrays, param_names, posterior,
+                     max_draws=20000, config_lines=()):
+        def strs(xs):
+            arr = (C.c_char_p * max(len(xs), 1))()
+            for i, x in enumerate(xs):
+                arr[i] = x.encode()
+            return arr
+        sk = list(scalars.keys())
+        sv = _d([scalars[k] for k in sk]) if sk else np.zeros(1)
+        ak = list(arrays.keys())
+        al = np.array([len(arrays[k]) for k in ak] or [0], dtype=np.int64)
+        av = _d(np.concatenate([np.asarray(arrays[k], dtype=np.float64).ravel() for k in ak])) if ak else np.zeros(1)
+        P = np.ascontiguousarray(np.asarray(posterior, dtype=np.float64).T)
+        f = self.lib.ref_write_report
+        f.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_double, C.c_int, C.c_double, C.c_int, C.c_void_p, _dp,
+                      C.c_int, C.c_void_p, C.POINTER(C.c_int64), _dp, C.c_int, C.c_void_p, C.c_int64, C.c_int64, _dp,
+                      C.c_int64, C.c_int, C.c_void_p]
+        cl = list(config_lines)
+        rc = f(str(path).encode(), sampler.encode(), label.encode(), float(F), int(diverged), float(wall), len(sk),
+               strs(sk), _ptr(sv), len(ak), strs(ak), al.ctypes.data_as(C.POINTER(C.c_int64)), _ptr(av),
+               len(param_names), strs(param_names), P.shape[1], P.shape[0], _ptr(P), int(max_draws), len(cl), strs(cl))
+        if rc:
+            raise OracleError(rc, "write_report")
+
 
 def ref_available() -> bool:
     return REF_SO.exists()

@@ -16,6 +16,7 @@
 #include "specmc/energy.hpp"
 #include "specmc/mcmc.hpp"
 #include "specmc/posterior.hpp"
+#include "specmc/report.hpp"
 #include "specmc/smc.hpp"
 #include "specmc/synthetic.hpp"
 
@@ -397,5 +398,71 @@ uint64_t ref_trial_seed(uint64_t base, int trial) {
 }
 
 int ref_hardware_workers() { return ThreadPool::hardware_workers(); }
+
+// ---- output side: report file format and posterior summaries (report.cpp, posterior.cpp)
+int ref_format_double(double v, char* out, int n) {
+  const std::string s = format_double(v);
+  std::strncpy(out, s.c_str(), (size_t)n - 1);
+  out[n - 1] = 0;
+  return (int)s.size();
+}
+
+double ref_weighted_quantile(const double* s, const double* w, int64_t n, double q, int* rc) {
+  *rc = 0;
+  try {
+    return weighted_quantile(ArrayXd(s, n), ArrayXd(w, n), q);
+  } catch (const std::invalid_argument&) {
+    *rc = 2;
+  }
+  return 0.0;
+}
+
+int ref_sort_peak_blocks(const double* post, int64_t d, int64_t m, int block, int center_off, int n_blocks,
+                         double* out) {
+  try {
+    MatrixXd P(d, m);
+    for (int64_t j = 0; j < m; ++j)
+      for (int64_t i = 0; i < d; ++i) P(i, j) = post[j * d + i];
+    const MatrixXd R = sort_peak_blocks(P, block, center_off, n_blocks);
+    for (int64_t j = 0; j < m; ++j)
+      for (int64_t i = 0; i < d; ++i) out[j * d + i] = R(i, j);
+    return 0;
+  } catch (const std::invalid_argument&) {
+    return 2;
+  }
+}
+
+// posterior: m draws of d values, draw-major (post[j * d + i])
+int ref_write_report(const char* path, const char* sampler, const char* label, double F, int diverged, double wall,
+                     int n_scalars, const char* const* skeys, const double* svals, int n_arrays,
+                     const char* const* akeys, const int64_t* alens, const double* avals, int n_params,
+                     const char* const* pnames, int64_t d, int64_t m, const double* post, int64_t max_draws,
+                     int n_cfg, const char* const* cfg) {
+  try {
+    RunReport r;
+    r.sampler = sampler;
+    r.label = label;
+    r.F = F;
+    r.diverged = diverged != 0;
+    r.wall_seconds = wall;
+    for (int i = 0; i < n_scalars; ++i) r.scalars[skeys[i]] = svals[i];
+    int64_t at = 0;
+    for (int a = 0; a < n_arrays; ++a) {
+      VectorXd v(alens[a]);
+      for (int64_t i = 0; i < alens[a]; ++i) v[i] = avals[at + i];
+      at += alens[a];
+      r.arrays[akeys[a]] = v;
+    }
+    for (int i = 0; i < n_params; ++i) r.param_names.push_back(pnames[i]);
+    r.posterior = MatrixXd(d, m);
+    for (int64_t j = 0; j < m; ++j)
+      for (int64_t i = 0; i < d; ++i) r.posterior(i, j) = post[j * d + i];
+    for (int i = 0; i < n_cfg; ++i) r.config_lines.push_back(cfg[i]);
+    write_report(r, path, max_draws);
+    return 0;
+  } catch (const std::exception&) {
+    return 3;
+  }
+}
 
 }  // extern "C"

@@ -92,6 +92,7 @@ class RunReport:
     device_seconds: float = 0.0
     proposals: int = 0
     trials: int = 0
+    config_lines: List[str] = field(default_factory=list)  # report.hpp:26, the config echo
 
 
 def _report(spec: ModelSpec, cfg: SmcConfig, n_data: int, r: _lib.SmcResultC) -> RunReport:
