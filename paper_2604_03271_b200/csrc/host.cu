@@ -481,6 +481,7 @@ struct ClassRun {
   Exchange* xch = nullptr;  // non-null: the groups are shards of particle-sharded runs
   std::vector<GroupDesc> gds;
   std::vector<int64_t> runs_T0;  // level-0 particles per group
+  std::vector<double*> out_shift;  // per group [d] device: posterior = theta + shift
   std::vector<int> order;
   GroupState* h_st = nullptr;
   int* h_list = nullptr;
@@ -532,7 +533,7 @@ struct ClassRun {
       bytes += Arena::al(S * 4) + Arena::al(d * sp * 4) + Arena::al(d * sp * 8);
       bytes += Arena::al(T * 8) + Arena::al(kHist * (1 + 2 * d) * 8);
       bytes += Arena::al((size_t)R.cfg.max_levels * 4 * 8);
-      bytes += Arena::al(2 * d * 8);                                            // stat_acc
+      bytes += Arena::al(2 * d * 8) + Arena::al(d * 8);                         // stat_acc, out_shift
       bytes += Arena::al(2 * 8) + Arena::al(2 * 8 * (size_t)R.nshards);        // xbuf, xgat
       bytes += Arena::al(R.refl.size() * 4 + 8) + Arena::al(R.refl_off.size() * 4 + 4);  // xrd reflections
       if (T > kGridTemperT || xch) bytes += Arena::al(sizeof(TemperScratch));  // grid tempering
@@ -560,6 +561,7 @@ struct ClassRun {
     }
     gds.resize(G);
     runs_T0.resize(G);
+    out_shift.resize(G);
     for (int gi = 0; gi < G; ++gi) {
       const RunSpec& R = runs[idx[gi]];
       runs_T0[gi] = R.nshards > 1 || xch ? R.T_loc0 : (int64_t)R.cfg.T;
@@ -621,6 +623,13 @@ struct ClassRun {
       g.diag = ar.take<double>((size_t)R.cfg.max_levels * 4);
       g.st = d_st + gi;
       g.stat_acc = ar.take<double>(2 * d);
+      {  // location shift undone on output (posterior = theta + shift)
+        std::vector<double> sh(d, 0.0);
+        for (size_t i = 0; i < d; ++i)
+          if (is_location(R.m.family, R.m.K, (int)i)) sh[i] = R.x_shift;
+        out_shift[gi] = ar.take<double>(d);
+        h2d(out_shift[gi], sh.data(), d, st);
+      }
       g.sharded = xch ? 1 : 0;
       g.shard = R.shard;
       g.nshards = R.nshards;
@@ -804,12 +813,13 @@ struct ClassRun {
       const int Lv = s.level;
       std::vector<double> diag((size_t)Lv * 4);
       d2h(diag.data(), gds[gi].diag, diag.size(), st);
-      std::vector<double> th(d * T);
-      cuda_check(cudaMemcpy2DAsync(th.data(), T * sizeof(double), gds[gi].theta[s.cur],
-                                   (size_t)gds[gi].tp * sizeof(double), T * sizeof(double), d,
-                                   cudaMemcpyDeviceToHost, st),
-                 "D2H theta");
-      o.energies = static_cast<double*>(std::malloc(sizeof(double) * T));
+      // posterior: transposed to [T][d] on the device into the idle theta buffer, one D2H
+      double* pout = gds[gi].theta[s.cur ^ 1];
+      cuda_check(launch_posterior_out(gds[gi].theta[s.cur], gds[gi].tp, (int)d, (int)T, out_shift[gi], pout, st),
+                 "k_posterior_out");
+      o.posterior = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(d * T, 1)));
+      d2h(o.posterior, pout, d * T, st);
+      o.energies = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(T, 1)));
       d2h(o.energies, gds[gi].E[s.cur], T, st);
       dev.sync();
       o.ladder = static_cast<double*>(std::malloc(sizeof(double) * (Lv + 1)));
@@ -823,13 +833,6 @@ struct ClassRun {
         o.level_log_mean_w[l] = diag[4 * l + 2];
         o.level_acc_rate[l] = diag[4 * l + 3];
       }
-      o.posterior = static_cast<double*>(std::malloc(sizeof(double) * d * T));
-      for (size_t c = 0; c < T; ++c)
-        for (size_t i = 0; i < d; ++i) {
-          double v = th[i * T + c];
-          if (is_location(R.m.family, R.m.K, (int)i) && R.x_shift != 0.0) v += R.x_shift;
-          o.posterior[c * d + i] = v;
-        }
     }
   }
 };

@@ -817,6 +817,23 @@ __global__ void k_stats_final(const GroupDesc* __restrict__ gds, const int* __re
   if (beta >= 1.0) st->active = 0;
 }
 
+// posterior output: component-major theta [d][tp] -> particle-major [T][d]
+// (the ABI's d x T column-major block) with the location shift undone
+__global__ void k_posterior_out(const double* __restrict__ theta, int tp, int d, int T,
+                                const double* __restrict__ shift, double* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= T) return;
+  for (int i = 0; i < d; ++i) {
+    const double v = theta[(size_t)i * tp + c], sh = shift[i];
+    out[(size_t)c * d + i] = sh != 0.0 ? v + sh : v;
+  }
+}
+cudaError_t launch_posterior_out(const double* theta, int tp, int d, int T, const double* shift, double* out,
+                                 cudaStream_t st) {
+  if (T > 0) k_posterior_out<<<(T + 255) / 256, 256, 0, st>>>(theta, tp, d, T, shift, out);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------- unit kernels
 __global__ void __launch_bounds__(kTemperThreads) k_unit_ess(const double* lw, int64_t n, double* out, int* err) {
   __shared__ TemperShared sh;

@@ -86,6 +86,10 @@ cudaError_t launch_stats(const GroupDesc* d_gds, const int* d_list, int n_list, 
 // load every kernel of one class (family, noise, shape) before its timed run
 cudaError_t prime_level_kernels(int family, int noise, const Shape& s, int dmax);
 
+// theta [d][tp] -> out [T][d] + shift[i] (result posterior block)
+cudaError_t launch_posterior_out(const double* theta, int tp, int d, int T, const double* shift, double* out,
+                                 cudaStream_t st);
+
 cudaError_t launch_probe_mufu(float* d_out, int blocks, int iters, cudaStream_t st);
 
 // ---- parity units (single-array versions of the temper building blocks)

@@ -109,7 +109,7 @@ def _report(spec: ModelSpec, cfg: SmcConfig, n_data: int, r: _lib.SmcResultC) ->
         "level_acc_rate": np.ctypeslib.as_array(r.level_acc_rate, (max(L, 1),))[:L].copy(),
     }
     d, T = r.d, r.T
-    rep.posterior = np.ctypeslib.as_array(r.posterior, (T, d)).T.copy()
+    rep.posterior = np.ctypeslib.as_array(r.posterior, (T, d)).copy().T  # d x T view of the particle-major block
     rep.energies = np.ctypeslib.as_array(r.energies, (T,)).copy()
     return rep
 
