@@ -313,7 +313,10 @@ __device__ __forceinline__ float noise_term(const GroupDesc& g, float f, float2 
                                 // 1/s_k and q carry the s0^2 factor (host)
     return fmaf(g.nz_q, (r * r) * rcpf(f), lg2f(f * yq.y));
   } else {
-    return (f - yq.x) - yq.x * (kLn2 * lg2f(f * yq.y));
+    // y = 0 contributes f alone (no 0 * log f: a model value that underflowed in
+    // fp32 must not turn the term into NaN); f < 0 stays the sentinel
+    const float lt = yq.x > 0.f ? yq.x * (kLn2 * lg2f(f * yq.y)) : 0.f;
+    return f < 0.f ? __int_as_float(0x7fc00000) : (f - yq.x) - lt;
   }
 }
 
