@@ -957,7 +957,7 @@ size_t chain_smem_bytes(const Shape& s, int dmax) {  // must match Smem<PPL, W>:
   const size_t npt = (size_t)s.PPL * 32 * s.W;
   size_t b = 16 + npt * (4 + 8 + 8) + (size_t)s.U * dpad * (8 + 8 + 4 + 8 + 8 + 4 + 4 + 4 + 4);
   b = (b + 15) & ~(size_t)15;
-  return b + (size_t)s.U * sizeof(Xch) + (size_t)s.U * npt * ((s.W == 4 && s.PPL > 16) ? 8 : 4);  // Q (and P, p_in_smem)
+  return b + (size_t)s.U * sizeof(Xch) + (size_t)s.U * npt * (s.W == 4 ? 8 : 4);  // Q (and P, p_in_smem<W>() in chain.cuh)
 }
 
 cudaError_t launch_energy(int family, const Shape& s, int dmax, const GroupDesc* gds, const int* list,
