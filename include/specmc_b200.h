@@ -147,6 +147,14 @@ int specmc_session_run(specmc_session* s, double* device_seconds, char* err, siz
 int specmc_session_fetch(specmc_session* s, specmc_smc_result* out, char* err, size_t errlen);
 void specmc_session_destroy(specmc_session* s);
 
+/* init_ensemble (proj/src/smc.cpp:34-53) alone: the T prior draws of a run
+ * and their full energies, exactly as the sampler's level 0 makes them
+ * (same Philox streams).  out->posterior = the d x T draws, out->energies =
+ * their energies, levels = 0.  Parity unit for the initial ensemble and the
+ * importance-sampling identity (acceptance criterion 9a). */
+int specmc_init_ensemble(const specmc_model_desc* model, const double* xs, const double* ys, int64_t n_points,
+                         const specmc_smc_config* cfg, specmc_smc_result* out, char* err, size_t errlen);
+
 /* ---- particle-sharded runs (multi-GPU) -----------------
  * One run's T particles split over shards that exchange a few scalars per
  * tempering phase (ESS bisection sums, weight max / sums, per-shard weight

@@ -60,7 +60,7 @@ EXPORTS = [
     "specmc_validate_config", "specmc_validate_problem", "specmc_stats_get", "specmc_stats_reset",
     "specmc_launch_shape", "specmc_device_count", "specmc_version", "specmc_session_create", "specmc_session_run",
     "specmc_session_fetch", "specmc_session_destroy", "specmc_probe_mufu", "specmc_smc_run_sharded",
-    "specmc_nccl_unique_id", "specmc_comm_init_nccl", "specmc_comm_destroy",
+    "specmc_nccl_unique_id", "specmc_comm_init_nccl", "specmc_comm_destroy", "specmc_init_ensemble",
 ]
 SPECMC_COMM_ID_BYTES = 128
 
@@ -84,6 +84,8 @@ def _load():
     lib.specmc_session_destroy.argtypes = [C.c_void_p]
     lib.specmc_session_destroy.restype = None
     lib.specmc_probe_mufu.argtypes = [C.c_int32, _dp, E, Z]
+    lib.specmc_init_ensemble.argtypes = [C.POINTER(ModelDesc), _dp, _dp, C.c_int64, C.POINTER(SmcConfigC),
+                                         C.POINTER(SmcResultC), E, Z]
     if hasattr(lib, "specmc_smc_run_sharded"):  # (older builds under SPECMC_LIB A/B experiments lack it)
         lib.specmc_smc_run_sharded.argtypes = [C.POINTER(ModelDesc), _dp, _dp, C.c_int64, C.POINTER(SmcConfigC),
                                                C.c_int32, C.c_void_p, C.POINTER(SmcResultC), E, Z]

@@ -479,6 +479,7 @@ struct ClassRun {
   int *d_list_small = nullptr, *d_list_big = nullptr;
   int max_slices = 0;
   Exchange* xch = nullptr;  // non-null: the groups are shards of particle-sharded runs
+  bool init_only = false;   // stop after init_ensemble (parity unit specmc_init_ensemble)
   std::vector<GroupDesc> gds;
   std::vector<int64_t> runs_T0;  // level-0 particles per group
   std::vector<double*> out_shift;  // per group [d] device: posterior = theta + shift
@@ -703,7 +704,8 @@ struct ClassRun {
     cuda_check(launch_init_draw(d_gds, d_list_all, G, Tmax, st), "k_init_draw");
     cuda_check(launch_energy(family, shape, dmax, d_gds, d_list_all, d_prefix_all, G, total, st), "k_chain<energy>");
     count_launch(2);
-    std::vector<int> active = order;
+    std::vector<int> active = init_only ? std::vector<int>() : order;
+    if (init_only) d2h(h_st, d_st, G, st);
     double move_ms = 0.0;
     int64_t move_launches = 0;
     while (!active.empty() && xch) {
@@ -1187,6 +1189,25 @@ int specmc_session_fetch(specmc_session* s, specmc_smc_result* out, char* err, s
 }
 
 void specmc_session_destroy(specmc_session* s) { delete reinterpret_cast<Session*>(s); }
+
+int specmc_init_ensemble(const specmc_model_desc* model, const double* xs, const double* ys, int64_t n_points,
+                         const specmc_smc_config* cfg, specmc_smc_result* out, char* err, size_t errlen) {
+  if (out) std::memset(out, 0, sizeof(*out));
+  return guarded(err, errlen, [&]() -> int {
+    if (!model || !cfg || !out) throw Error(SPECMC_EINVAL, "null argument");
+    specmc_spectrum sp{xs, ys, n_points};
+    std::vector<RunSpec> runs{make_runspec(*model, 0, *cfg, sp)};
+    Device dev(cfg->device);
+    std::vector<specmc_spectrum> spectra{sp};
+    ClassRun cr;
+    cr.idx = {0};
+    cr.init_only = true;
+    cr.prepare(dev, runs, spectra);
+    cr.run(dev);
+    cr.fetch(dev, runs, out);
+    return out->status;
+  });
+}
 
 int specmc_smc_run_sharded(const specmc_model_desc* model, const double* xs, const double* ys, int64_t n_points,
                            const specmc_smc_config* cfg, int32_t n_virtual, specmc_comm* comm,

@@ -210,6 +210,25 @@ class Session:
             pass
 
 
+def init_ensemble(spec: ModelSpec, data: Spectrum, cfg: SmcConfig):
+    """init_ensemble (smc.cpp:34-53) on the device: the level-0 prior draws (d x T)
+    and their energies (T), the same streams smc_run starts from."""
+    desc, keep = spec.desc()
+    res = _lib.SmcResultC()
+    err = C.create_string_buffer(1024)
+    rc = lib.specmc_init_ensemble(C.byref(desc), _p(data.xs), _p(data.ys), len(data.xs), C.byref(cfg.c()),
+                                  C.byref(res), err, 1024)
+    try:
+        if rc:
+            _raise(rc, err)
+        d, T = res.d, res.T
+        th = np.ctypeslib.as_array(res.posterior, (T, d)).copy().T
+        E = np.ctypeslib.as_array(res.energies, (T,)).copy()
+        return th, E
+    finally:
+        lib.specmc_result_free(C.byref(res))
+
+
 # ------------------------------------------------------- particle sharding
 class Comm:
     """NCCL communicator with one shard per rank (specmc_comm_init_nccl).

@@ -219,3 +219,73 @@ def test_every_move_kernel_matches_oracle(smc, port, fam, nz):
     f_gpu, f_cpu, se = _compare_F(smc, port, spec, data, 256, 8, range(200, 224), range(6))
     assert np.all(np.isfinite(f_gpu)) and np.all(np.isfinite(f_cpu))
     assert abs(f_gpu.mean() - f_cpu.mean()) <= 4 * se + 0.1, (f_gpu.mean(), f_cpu.mean(), se)
+
+
+def test_criterion3_error_decreases_with_particle_budget(smc):
+    # acceptance criterion 3 (acceptance_main.cpp:175-221): on the 3-peak gm data set the
+    # median |dF| over 10 trials, and the median error of the mu credible-interval
+    # endpoints, both shrink monotonically over T in {1e3, 3e3, 1e4, 3e4}; reference =
+    # the T = 1e5 runs
+    from paper_2604_03271_b200 import report as R
+    w = syn.config("C1")
+    spec = w.spec(3)
+    ts = [1000, 3000, 10000, 30000]
+    probs = [(spec, 0, smc.SmcConfig(T=T, n=10, seed=1000 + 17 * t)) for T in ts for t in range(10)]
+    probs += [(spec, 0, smc.SmcConfig(T=100000, n=10, seed=5 + t)) for t in range(3)]
+    reps = smc.smc_run_batch(probs, [w.data])
+    big = reps[len(ts) * 10:]
+    F_ref = np.mean([r.F for r in big])
+
+    def mu_ci(r):  # 90% intervals of the three centres after sorting the peak blocks by centre
+        post = R.sort_peak_blocks(r.posterior, 3, 1, 3)
+        wts = np.ones(post.shape[1])
+        return np.array([R.credible_interval(post[3 * b + 1], wts, 0.9) for b in range(3)])
+
+    ci_ref = np.mean([mu_ci(r) for r in big], axis=0)
+    df, ci_err = [], []
+    for k, T in enumerate(ts):
+        runs = reps[10 * k:10 * (k + 1)]
+        df.append(np.median([abs(r.F - F_ref) for r in runs]))
+        ci_err.append(np.median([np.abs(mu_ci(r) - ci_ref).max() for r in runs]))
+    assert all(a > b for a, b in zip(df, df[1:])), df
+    assert all(a > b for a, b in zip(ci_err, ci_err[1:])), ci_err
+
+
+def test_criterion9a_single_level_is_importance_sampling_bitwise(smc, port):
+    # acceptance criterion 9a (acceptance_main.cpp:468-483): with ess_target = 1e-9 the
+    # first level jumps to beta = 1 and F = -log_mean_exp(-N E_init) bit for bit
+    spec, data, *_ = conjugate(20, 404, port)
+    cfg = smc.SmcConfig(T=100, n=5, ess_target=1e-9, seed=31)
+    rep = smc.smc_run(spec, data, cfg)
+    th, E = smc.init_ensemble(spec, data, cfg)
+    assert rep.scalars["levels"] == 1 and th.shape == (1, 100)
+    f_is = -smc.log_mean_exp(-len(data.xs) * E)
+    assert rep.F == f_is
+
+
+def test_init_ensemble_draws_and_energies(smc, port):
+    # init_ensemble (smc.cpp:34-53): prior draws (moments) and their full energies
+    w = syn.config("C1")
+    spec = w.spec(3)
+    th, E = smc.init_ensemble(spec, w.data, smc.SmcConfig(T=65536, n=8, seed=3))
+    assert th.shape == (9, 65536) and np.all(np.isfinite(E))
+    A, mu, b = th[0], th[1], th[2]
+    assert abs(A.mean() - 1.0) < 0.01 and abs(A.var() - 0.2) < 0.01        # Gamma(5, 5)
+    assert abs(mu.mean() - 1.5) < 0.03 and abs(mu.var() / 0.75 - 1) < 0.03  # Uniform(0, 3)
+    assert abs(b.mean() - 125.0) < 1.0                                       # Gamma(5, 0.04)
+    E2 = smc.energies(spec, w.data, th[:, :512].T)
+    n = len(w.data.xs)
+    assert np.all(np.abs(E2 - E[:512]) <= 2e-6 * np.abs(E[:512]) + 0.02 / n)
+
+
+@pytest.mark.parametrize("T,n", [(60, 1), (60, 2), (60, 3), (60, 5), (60, 6), (60, 10), (60, 15), (60, 30),
+                                 (100, 4), (100, 10), (100, 50), (300, 10)])
+def test_criterion6_waste_free_bookkeeping(smc, port, T, n):
+    # acceptance criterion 6 (acceptance_main.cpp:325-363): every level runs S = T/n chains
+    # of n sweeps (T proposals for d = 1, all inside the normal prior's support) and
+    # outputs exactly T particles
+    spec, data, *_ = conjugate(12, 55, port)
+    rep = smc.smc_run(spec, data, smc.SmcConfig(T=T, n=n, seed=5))
+    L = int(rep.scalars["levels"])
+    assert rep.trials == T * L and rep.proposals == T * L
+    assert rep.posterior.shape == (1, T) and rep.energies.shape == (T,)
