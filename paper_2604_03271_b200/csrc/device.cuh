@@ -79,7 +79,6 @@ struct GroupDesc {  // immutable per group
   float nz_a0, nz_a1, nz_a2, nz_q;
   // shirley helpers (shifted x)
   float x0s, inv_range, range;
-  float x_shift_f;      // unused on device; kept for debugging
   // spectrum (lane-transposed, see header)
   const float* spec_x;   // shifted abscissa x' = x - x_shift
   const float2* spec_c;  // (c_k, h_{k+1}): trapezoid weights of the Shirley scan

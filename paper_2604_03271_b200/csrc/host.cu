@@ -7,10 +7,12 @@
 //   validate_spectrum          proj/src/spectrum.cpp:12-23
 //   smc_run (level loop)       proj/src/smc.cpp:186-211, report fields :218-249
 // The level loop runs every group (one SMC run = one (spectrum, K, seed)) of
-// a batch in lock-step: per round one k_temper (1 CTA per group), one k_chain
-// move launch covering every chain of every active group (longest d first),
-// and one k_stats.  The host reads back 48 bytes of state per group per round
-// to retire groups that reached beta = 1.
+// a batch in lock-step: per round the tempering (k_temper, one CTA per group,
+// or the k_tp_* grid phases for T > 2^17), one k_chain move launch covering
+// every chain of every active group (longest d first), and k_stats_grid +
+// k_stats_final.  The host reads back the small GroupState of every group per
+// round to retire groups that reached beta = 1.  Particle-sharded runs
+// (run_sharded) add the cross-shard exchanges between the tempering phases.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -594,7 +596,6 @@ struct ClassRun {
       g.x0s = ps.x0s;
       g.inv_range = ps.inv_range;
       g.range = ps.range;
-      g.x_shift_f = (float)R.x_shift;
       auto t = dspec.at(key);
       g.spec_x = std::get<0>(t);
       g.spec_c = std::get<1>(t);

@@ -3,7 +3,7 @@
 //   k_init_draw   prior draws, one thread per particle        (smc.cpp:34-53, priors.cpp:105-110)
 //   k_temper      ESS bisection, weights, evidence, systematic resampling, step prediction
 //                 (one CTA per SMC run)                       (smc.cpp:55-112, :128-135, mcmc.cpp:20-53)
-//   k_stats       step-size statistics and history            (smc.cpp:162-183)
+//   k_stats_grid  step-size statistics and history            (smc.cpp:162-183)
 //   k_unit_*      single-array parity units of the same device functions
 // The chain-parallel kernel (energies K2, fused move K3) lives in chain.cuh and
 // is instantiated per family in chain_<family>_<mode>.cu.
@@ -366,42 +366,6 @@ __global__ void __launch_bounds__(kTemperThreads) k_temper(const GroupDesc* __re
     st->level = level + 1;
   }
 }
-
-// one CTA per active group: pooled acceptance, geometric-mean step (smc.cpp:162-183)
-__global__ void __launch_bounds__(256) k_stats(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
-  __shared__ TemperShared sh;
-  const GroupDesc& g = gds[list[blockIdx.x]];
-  GroupState* st = g.st;
-  const int d = g.d, S = g.S, H = st->hist_count;
-  const int stride = 1 + 2 * d;
-  double* h = g.hist + (size_t)(H % kHist) * stride;
-  double acc_all = 0.0;
-  for (int i = 0; i < d; ++i) {
-    double a = 0.0, l = 0.0;
-    for (int c = threadIdx.x; c < S; c += blockDim.x) {
-      a += (double)g.chain_acc[(size_t)i * g.sp + c];
-      l += g.chain_ls[(size_t)i * g.sp + c];
-    }
-    a = block_reduce(a, sh.red, OpAdd(), 0.0);
-    l = block_reduce(l, sh.red, OpAdd(), 0.0);
-    if (threadIdx.x == 0) {
-      const double prop = (double)S * g.n;
-      h[1 + i] = prop > 0 ? a / prop : 0.0;
-      h[1 + d + i] = exp(l / (double)S);
-    }
-    acc_all += a;
-  }
-  if (threadIdx.x == 0) {
-    const double beta = st->beta;
-    h[0] = beta;
-    const double prop_all = (double)S * g.n * d;
-    g.diag[(size_t)(st->level - 1) * 4 + 3] = prop_all > 0 ? acc_all / prop_all : 0.0;
-    st->hist_count = H + 1;
-    st->cur ^= 1;
-    if (beta >= 1.0) st->active = 0;
-  }
-}
-
 
 // =================================================================
 // Grid-level tempering for large populations (T > 2^17): the same
@@ -1036,10 +1000,6 @@ cudaError_t launch_init_draw(const GroupDesc* gds, const int* list, int n_list, 
 }
 cudaError_t launch_temper(const GroupDesc* gds, const int* list, int n_list, cudaStream_t st) {
   k_temper<<<n_list, kTemperThreads, 0, st>>>(gds, list);
-  return cudaGetLastError();
-}
-cudaError_t launch_stats(const GroupDesc* gds, const int* list, int n_list, cudaStream_t st) {
-  k_stats<<<n_list, 256, 0, st>>>(gds, list);
   return cudaGetLastError();
 }
 cudaError_t launch_temper_grid(const GroupDesc* gds, const int* list, int n_list, int max_slices, cudaStream_t st) {

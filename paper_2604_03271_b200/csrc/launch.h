@@ -80,8 +80,6 @@ cudaError_t launch_xgather(const GroupDesc* d_gds, const int* d_list, int n, cud
 
 // step-size statistics, one CTA per (component, group), + per-group finalisation
 cudaError_t launch_stats_grid(const GroupDesc* d_gds, const int* d_list, int n_list, int dmax, cudaStream_t st);
-// step-size statistics + history + buffer flip (one CTA per group)
-cudaError_t launch_stats(const GroupDesc* d_gds, const int* d_list, int n_list, cudaStream_t st);
 
 // load every kernel of one class (family, noise, shape) before its timed run
 cudaError_t prime_level_kernels(int family, int noise, const Shape& s, int dmax);
