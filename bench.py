@@ -232,15 +232,18 @@ def run_ours(args, ws, rank, local):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         e2e_evals = 0
+        e2e_steps = []
         for _ in range(args.steps):
+            ts = time.perf_counter()
             rr = S.smc_run_batch(problems, [w.data], raise_on_error=False)
             e2e_evals += sum(r.proposals for r in rr if not isinstance(r, Exception))
+            e2e_steps.append(round(time.perf_counter() - ts, 4))
         torch.cuda.synchronize()
         e2e_t = time.perf_counter() - t0
         h2d = 2 * N * 8 + sum(p[0].d * (4 + 8 + 8) for p in problems)
         d2h = sum(p[0].d * w.T * 8 + w.T * 8 for p in problems) + sum(
             int(r.scalars["levels"]) * 4 * 8 for r in rr if not isinstance(r, Exception))
-        e2e = {"value": e2e_evals, "t": e2e_t, "h2d": h2d, "d2h": d2h}
+        e2e = {"value": e2e_evals, "t": e2e_t, "h2d": h2d, "d2h": d2h, "steps": e2e_steps}
 
     # ---- model selection over all trials (ranks); max-over-ranks timing
     Fs = [r.F if not isinstance(r, Exception) else float("nan") for r in reps]
@@ -296,7 +299,7 @@ def run_ours(args, ws, rank, local):
     }
     if e2e:
         line["e2e"] = {"value": e2e["value"] / e2e["t"], "unit": "evals/s", "h2d_bytes_per_step": e2e["h2d"],
-                       "d2h_bytes_per_step": e2e["d2h"]}
+                       "d2h_bytes_per_step": e2e["d2h"], "step_seconds": e2e.get("steps")}
     if ws == 1 and not args.no_cpu_baseline:
         ev, secs, cores, kind = cpu_reference_sample(w, seed, CPU_SAMPLE_T)
         line["cpu_baseline"] = {"value": ev / secs, "unit": "evals/s", "cores": cores, "kind": kind,
