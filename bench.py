@@ -337,15 +337,12 @@ def run_particles(args, ws, rank, local):
     N = len(w.data.xs)
     peak_mufu = S.probe_mufu(local)
 
-    def step():
-        dev, wall, evals, reps = 0.0, 0.0, 0, {}
-        for K in ks:
-            r = S.smc_run_sharded(w.spec(K), w.data, cfgs[K], n_virtual=1, comm=comm)
-            dev += r.device_seconds
-            wall += r.wall_seconds
-            evals += r.proposals
-            reps[K] = r
-        return dev, wall, evals, reps
+    problems = [(w.spec(K), 0, cfgs[K]) for K in ks]
+
+    def step():  # all K at once, every run's particles split over the ranks
+        rr = S.smc_run_sharded_batch(problems, [w.data], n_virtual=1, comm=comm)
+        reps = dict(zip(ks, rr))
+        return rr[0].device_seconds, rr[0].wall_seconds, sum(r.proposals for r in rr), reps
 
     for _ in range(args.warmup):
         step()

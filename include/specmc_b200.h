@@ -173,6 +173,11 @@ typedef struct specmc_comm specmc_comm;
 int specmc_smc_run_sharded(const specmc_model_desc* model, const double* xs, const double* ys, int64_t n_points,
                            const specmc_smc_config* cfg, int32_t n_virtual, specmc_comm* comm,
                            specmc_smc_result* out, char* err, size_t errlen);
+/* Batched form: every problem split over the same shards (all K of a model
+ * selection at once); out[i] as for specmc_smc_run_sharded. */
+int specmc_smc_run_sharded_batch(int32_t n_problems, const specmc_problem* problems, int32_t n_spectra,
+                                 const specmc_spectrum* spectra, int32_t n_virtual, specmc_comm* comm,
+                                 specmc_smc_result* out, char* err, size_t errlen);
 /* NCCL bootstrap: rank 0 creates the id, the host framework broadcasts it
  * (e.g. torch.distributed), every rank then creates its communicator. */
 int specmc_nccl_unique_id(uint8_t* out /* SPECMC_COMM_ID_BYTES */, char* err, size_t errlen);

@@ -61,6 +61,7 @@ EXPORTS = [
     "specmc_launch_shape", "specmc_device_count", "specmc_version", "specmc_session_create", "specmc_session_run",
     "specmc_session_fetch", "specmc_session_destroy", "specmc_probe_mufu", "specmc_smc_run_sharded",
     "specmc_nccl_unique_id", "specmc_comm_init_nccl", "specmc_comm_destroy", "specmc_init_ensemble",
+    "specmc_smc_run_sharded_batch",
 ]
 SPECMC_COMM_ID_BYTES = 128
 
@@ -89,6 +90,9 @@ def _load():
     if hasattr(lib, "specmc_smc_run_sharded"):  # (older builds under SPECMC_LIB A/B experiments lack it)
         lib.specmc_smc_run_sharded.argtypes = [C.POINTER(ModelDesc), _dp, _dp, C.c_int64, C.POINTER(SmcConfigC),
                                                C.c_int32, C.c_void_p, C.POINTER(SmcResultC), E, Z]
+        lib.specmc_smc_run_sharded_batch.argtypes = [C.c_int32, C.POINTER(ProblemC), C.c_int32,
+                                                     C.POINTER(SpectrumC), C.c_int32, C.c_void_p,
+                                                     C.POINTER(SmcResultC), E, Z]
         lib.specmc_nccl_unique_id.argtypes = [C.c_char_p, E, Z]
         lib.specmc_comm_init_nccl.argtypes = [C.c_int32, C.c_int32, C.c_char_p, C.c_int32, C.POINTER(C.c_void_p),
                                               E, Z]

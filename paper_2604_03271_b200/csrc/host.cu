@@ -423,6 +423,7 @@ struct RunSpec {
   // T level-0 particles, global ids [pbase, pbase + T_loc0)
   int shard = 0, nshards = 1;
   int64_t T_loc0 = 0, pbase = 0;
+  int problem = 0;  // index of the run in the caller's batch
 };
 
 struct Device {
@@ -482,6 +483,8 @@ struct ClassRun {
   int max_slices = 0;
   Exchange* xch = nullptr;  // non-null: the groups are shards of particle-sharded runs
   bool init_only = false;   // stop after init_ensemble (parity unit specmc_init_ensemble)
+  int* d_xlist = nullptr;   // sharded: every run's shards, run-major (idx order), for the exchanges
+  int nshards = 1;
   std::vector<GroupDesc> gds;
   std::vector<int64_t> runs_T0;  // level-0 particles per group
   std::vector<double*> out_shift;  // per group [d] device: posterior = theta + shift
@@ -525,7 +528,7 @@ struct ClassRun {
       }
     }
     const size_t npt = (size_t)shape.PPL * 32 * shape.W;
-    size_t bytes = Arena::al(sizeof(GroupDesc) * G) + Arena::al(sizeof(GroupState) * G) + 6 * Arena::al(4 * (G + 1));
+    size_t bytes = Arena::al(sizeof(GroupDesc) * G) + Arena::al(sizeof(GroupState) * G) + 7 * Arena::al(4 * (G + 1));
     bytes += prep.size() * (Arena::al(npt * 4) + 2 * Arena::al(npt * 8));
     for (int r : idx) {
       const auto& R = runs[r];
@@ -551,6 +554,13 @@ struct ClassRun {
     d_list_small = ar.take<int>(G + 1);
     d_list_big = ar.take<int>(G + 1);
     cudaStream_t st = dev.stream;
+    if (xch) {  // idx is run-major, shard order: the exchange list is the identity
+      nshards = runs[idx[0]].nshards;
+      std::vector<int> xl(G);
+      std::iota(xl.begin(), xl.end(), 0);
+      d_xlist = ar.take<int>(G);
+      h2d(d_xlist, xl.data(), G, st);
+    }
 
     std::map<std::pair<int, double>, std::tuple<float*, float2*, float2*>> dspec;
     for (auto& kv : prep) {
@@ -966,9 +976,11 @@ struct VirtualExchange : Exchange {
   const ClassRun* cr;
   explicit VirtualExchange(const ClassRun* c) : cr(c) {}
   cudaError_t reduce(int buf, int count, int op, cudaStream_t st) override {
-    return launch_xreduce(cr->d_gds, cr->d_list_all, cr->G, buf, count, op, st);
+    return launch_xreduce(cr->d_gds, cr->d_xlist, cr->G / cr->nshards, cr->nshards, buf, count, op, st);
   }
-  cudaError_t gather(cudaStream_t st) override { return launch_xgather(cr->d_gds, cr->d_list_all, cr->G, st); }
+  cudaError_t gather(cudaStream_t st) override {
+    return launch_xgather(cr->d_gds, cr->d_xlist, cr->G / cr->nshards, cr->nshards, st);
+  }
 };
 
 // NCCL, resolved with dlopen so that the library has no link-time NCCL
@@ -980,6 +992,8 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*ErrorString)(ncclResult_t) = nullptr;
   static NcclApi& get() {
     static NcclApi api = [] {
@@ -994,9 +1008,12 @@ struct NcclApi {
       a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(a.h, "ncclAllGather"));
       a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(a.h, "ncclCommDestroy"));
       a.ErrorString = reinterpret_cast<decltype(a.ErrorString)>(dlsym(a.h, "ncclGetErrorString"));
+      a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(a.h, "ncclGroupStart"));
+      a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(a.h, "ncclGroupEnd"));
       return a;
     }();
-    if (!api.h || !api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.AllGather || !api.CommDestroy)
+    if (!api.h || !api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.AllGather || !api.CommDestroy ||
+        !api.GroupStart || !api.GroupEnd)
       throw Error(SPECMC_ECOMM, "NCCL (libnccl.so.2) is not available");
     return api;
   }
@@ -1011,95 +1028,127 @@ struct CommImpl {
   int rank = 0, world = 1, device = 0;
 };
 
-// One shard per rank: the exchanges are NCCL collectives on the shard's buffers,
-// enqueued on the level stream (no host round trip inside a level)
+// One shard of every run per rank: the exchanges are NCCL collectives on the
+// shards' buffers, one per run, aggregated in an NCCL group and enqueued on the
+// level stream (no host round trip inside a level)
 struct NcclExchange : Exchange {
   const ClassRun* cr;
   CommImpl* c;
   NcclExchange(const ClassRun* r, CommImpl* cc) : cr(r), c(cc) {}
   cudaError_t reduce(int buf, int count, int op, cudaStream_t st) override {
     NcclApi& api = NcclApi::get();
-    double* p = buf == 0 ? cr->gds[0].xbuf : cr->gds[0].stat_acc;
     const ncclRedOp_t o = op == XOP_SUM ? ncclSum : (op == XOP_MIN ? ncclMin : ncclMax);
-    api.check(api.AllReduce(p, p, (size_t)count, ncclFloat64, o, c->comm, st), "ncclAllReduce");
+    api.check(api.GroupStart(), "ncclGroupStart");
+    for (const GroupDesc& g : cr->gds) {
+      double* p = buf == 0 ? g.xbuf : g.stat_acc;
+      const size_t n = count < 0 ? (size_t)2 * g.d : (size_t)count;
+      api.check(api.AllReduce(p, p, n, ncclFloat64, o, c->comm, st), "ncclAllReduce");
+    }
+    api.check(api.GroupEnd(), "ncclGroupEnd");
     return cudaSuccess;
   }
   cudaError_t gather(cudaStream_t st) override {
     NcclApi& api = NcclApi::get();
-    api.check(api.AllGather(cr->gds[0].xbuf, cr->gds[0].xgat, 2, ncclFloat64, c->comm, st), "ncclAllGather");
+    api.check(api.GroupStart(), "ncclGroupStart");
+    for (const GroupDesc& g : cr->gds)
+      api.check(api.AllGather(g.xbuf, g.xgat, 2, ncclFloat64, c->comm, st), "ncclAllGather");
+    api.check(api.GroupEnd(), "ncclGroupEnd");
     return cudaSuccess;
   }
 };
 
-// Particle-sharded smc_run: the T particles of one run are
+// Particle-sharded runs: the T particles of every problem are
 // split over nshards shards; comm == nullptr runs all of them on this device.
+// Problems of one (family, noise, launch shape) advance together in one class.
 // Results: F, ladder and diagnostics are global (identical on every shard);
 // the posterior holds this process's particles (all of them for virtual shards).
-int run_sharded(const specmc_model_desc& m, const double* xs, const double* ys, int64_t n_points,
-                const specmc_smc_config& cfg, int n_virtual, CommImpl* comm, specmc_smc_result* out) {
+int run_sharded_batch(int n_problems, const specmc_problem* problems, int n_spectra, const specmc_spectrum* sps,
+                      int n_virtual, CommImpl* comm, specmc_smc_result* out) {
   const auto t0 = std::chrono::steady_clock::now();
+  if (n_problems < 1 || !problems) throw Error(SPECMC_EINVAL, "sharded batch: no problems");
+  if (n_spectra < 1 || !sps) throw Error(SPECMC_EINVAL, "sharded batch: no spectra");
   const int nsh = comm ? comm->world : n_virtual;
   if (nsh < 1) throw Error(SPECMC_EINVAL, "sharded run: shard count must be >= 1");
-  if (cfg.T % nsh != 0) throw Error(SPECMC_EINVAL, "sharded run: T must be divisible by the shard count");
-  if (comm && cfg.device != comm->device)
-    throw Error(SPECMC_EINVAL, "sharded run: cfg.device differs from the communicator's device");
-  specmc_spectrum sp{xs, ys, n_points};
+  const int device = problems[0].cfg.device;
   std::vector<RunSpec> runs;
   const int first = comm ? comm->rank : 0, count = comm ? 1 : nsh;
-  for (int r = first; r < first + count; ++r) {
-    RunSpec R = make_runspec(m, 0, cfg, sp);
-    R.shard = r;
-    R.nshards = nsh;
-    R.T_loc0 = cfg.T / nsh;
-    R.pbase = (int64_t)r * (cfg.T / nsh);
-    runs.push_back(std::move(R));
+  for (int p = 0; p < n_problems; ++p) {
+    const specmc_problem& pr = problems[p];
+    if (pr.spectrum < 0 || pr.spectrum >= n_spectra) throw Error(SPECMC_EINVAL, "batch: spectrum index out of range");
+    if (pr.cfg.T % nsh != 0) throw Error(SPECMC_EINVAL, "sharded run: T must be divisible by the shard count");
+    if (pr.cfg.device != device) throw Error(SPECMC_EINVAL, "batch: all problems must target the same device");
+    if (comm && pr.cfg.device != comm->device)
+      throw Error(SPECMC_EINVAL, "sharded run: cfg.device differs from the communicator's device");
+    for (int r = first; r < first + count; ++r) {
+      RunSpec R = make_runspec(pr.model, pr.spectrum, pr.cfg, sps[pr.spectrum]);
+      R.shard = r;
+      R.nshards = nsh;
+      R.T_loc0 = pr.cfg.T / nsh;
+      R.pbase = (int64_t)r * (pr.cfg.T / nsh);
+      R.problem = p;
+      runs.push_back(std::move(R));
+    }
   }
-  Device dev(cfg.device);
-  std::vector<specmc_spectrum> spectra{sp};
-  ClassRun cr;
-  cr.idx.resize(runs.size());
-  std::iota(cr.idx.begin(), cr.idx.end(), 0);
-  std::unique_ptr<Exchange> x;
-  if (comm)
-    x = std::make_unique<NcclExchange>(&cr, comm);
-  else
-    x = std::make_unique<VirtualExchange>(&cr);
-  cr.xch = x.get();
-  cr.prepare(dev, runs, spectra);
-  cr.run(dev);
+  Device dev(device);
+  std::vector<specmc_spectrum> spectra(sps, sps + n_spectra);
+  // one class per (family, noise model, launch shape); runs stay run-major, shard order
+  std::map<std::tuple<int, int, int>, std::vector<int>> cls;
+  for (int i = 0; i < (int)runs.size(); ++i) {
+    const Shape s = pick_shape(runs[i].N);
+    cls[{runs[i].m.family, dev_noise(runs[i].m), s.W * 100 + s.PPL}].push_back(i);
+  }
   std::vector<specmc_smc_result> res(runs.size());
   for (auto& r : res) std::memset(&r, 0, sizeof(r));
-  cr.fetch(dev, runs, res.data());
+  for (auto& kv : cls) {  // same order on every rank (map order)
+    ClassRun cr;
+    cr.idx = kv.second;
+    std::unique_ptr<Exchange> x;
+    if (comm)
+      x = std::make_unique<NcclExchange>(&cr, comm);
+    else
+      x = std::make_unique<VirtualExchange>(&cr);
+    cr.xch = x.get();
+    cr.prepare(dev, runs, spectra);
+    cr.run(dev);
+    cr.fetch(dev, runs, res.data());
+  }
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  // merge this process's shards into one result (shard order)
-  std::memset(out, 0, sizeof(*out));
-  specmc_smc_result& o = *out;
-  o = res[0];
-  int64_t Ttot = 0, trials = 0;
-  for (auto& r : res) {
-    Ttot += r.T;
-    trials += r.trials;
-    if (r.status != SPECMC_OK) o.status = r.status;
-  }
-  o.trials = trials;
-  o.T = Ttot;
-  o.proposals = (int64_t)cfg.T * m.d * o.levels * count / nsh;
-  o.wall_seconds = wall;
-  if (o.status == SPECMC_OK && res.size() > 1) {
-    const size_t d = m.d;
-    o.posterior = static_cast<double*>(std::malloc(sizeof(double) * d * std::max<int64_t>(Ttot, 1)));
-    o.energies = static_cast<double*>(std::malloc(sizeof(double) * std::max<int64_t>(Ttot, 1)));
-    size_t at = 0;
-    for (auto& r : res) {
-      std::memcpy(o.posterior + at * d, r.posterior, sizeof(double) * d * r.T);
-      std::memcpy(o.energies + at, r.energies, sizeof(double) * r.T);
-      at += r.T;
+  // merge each problem's local shards into one result (shard order)
+  int first_bad = SPECMC_OK;
+  for (int p = 0; p < n_problems; ++p) {
+    specmc_smc_result& o = out[p];
+    const int i0 = p * count;
+    o = res[i0];
+    int64_t Ttot = 0, trials = 0;
+    for (int r = 0; r < count; ++r) {
+      Ttot += res[i0 + r].T;
+      trials += res[i0 + r].trials;
+      if (res[i0 + r].status != SPECMC_OK) o.status = res[i0 + r].status;
     }
-    std::free(res[0].posterior);
-    std::free(res[0].energies);
-    for (size_t i = 1; i < res.size(); ++i) specmc_result_free(&res[i]);
+    o.trials = trials;
+    o.T = Ttot;
+    o.proposals = (int64_t)problems[p].cfg.T * problems[p].model.d * o.levels * count / nsh;
+    o.wall_seconds = wall;
+    if (count > 1) {
+      if (o.status == SPECMC_OK) {
+        const size_t d = problems[p].model.d;
+        o.posterior = static_cast<double*>(std::malloc(sizeof(double) * d * std::max<int64_t>(Ttot, 1)));
+        o.energies = static_cast<double*>(std::malloc(sizeof(double) * std::max<int64_t>(Ttot, 1)));
+        size_t at = 0;
+        for (int r = 0; r < count; ++r) {
+          const specmc_smc_result& q = res[i0 + r];
+          std::memcpy(o.posterior + at * d, q.posterior, sizeof(double) * d * q.T);
+          std::memcpy(o.energies + at, q.energies, sizeof(double) * q.T);
+          at += q.T;
+        }
+        std::free(res[i0].posterior);
+        std::free(res[i0].energies);
+      }
+      for (int r = 1; r < count; ++r) specmc_result_free(&res[i0 + r]);
+    }
+    if (o.status != SPECMC_OK && first_bad == SPECMC_OK) first_bad = o.status;
   }
-  return o.status;
+  return first_bad;
 }
 
 template <typename F>
@@ -1210,17 +1259,35 @@ int specmc_init_ensemble(const specmc_model_desc* model, const double* xs, const
   });
 }
 
+int specmc_smc_run_sharded_batch(int32_t n_problems, const specmc_problem* problems, int32_t n_spectra,
+                                 const specmc_spectrum* spectra, int32_t n_virtual, specmc_comm* comm,
+                                 specmc_smc_result* out, char* err, size_t errlen) {
+  if (out && n_problems > 0) std::memset(out, 0, sizeof(specmc_smc_result) * (size_t)n_problems);
+  const int rc = guarded(err, errlen, [&]() -> int {
+    if (!out) throw Error(SPECMC_EINVAL, "null results");
+    const int r = run_sharded_batch(n_problems, problems, n_spectra, spectra, n_virtual,
+                                    reinterpret_cast<CommImpl*>(comm), out);
+    if (r != SPECMC_OK)
+      copy_err(err, errlen, "smc: max_levels exceeded before reaching beta = 1 (or total weight is zero)");
+    return r;
+  });
+  if (rc != SPECMC_OK && out)
+    for (int i = 0; i < n_problems; ++i)
+      if (out[i].status == SPECMC_OK && !out[i].posterior) out[i].status = rc;
+  return rc;
+}
+
 int specmc_smc_run_sharded(const specmc_model_desc* model, const double* xs, const double* ys, int64_t n_points,
                            const specmc_smc_config* cfg, int32_t n_virtual, specmc_comm* comm,
                            specmc_smc_result* out, char* err, size_t errlen) {
   if (out) std::memset(out, 0, sizeof(*out));
-  return guarded(err, errlen, [&]() -> int {
-    if (!model || !cfg || !out) throw Error(SPECMC_EINVAL, "null argument");
-    const int rc = run_sharded(*model, xs, ys, n_points, *cfg, n_virtual, reinterpret_cast<CommImpl*>(comm), out);
-    if (rc != SPECMC_OK)
-      copy_err(err, errlen, "smc: max_levels exceeded before reaching beta = 1 (or total weight is zero)");
-    return rc;
-  });
+  if (!model || !cfg || !out) {
+    copy_err(err, errlen, "null argument");
+    return SPECMC_EINVAL;
+  }
+  const specmc_problem p{*model, 0, *cfg};
+  const specmc_spectrum sp{xs, ys, n_points};
+  return specmc_smc_run_sharded_batch(1, &p, 1, &sp, n_virtual, comm, out, err, errlen);
 }
 
 int specmc_nccl_unique_id(uint8_t* out, char* err, size_t errlen) {

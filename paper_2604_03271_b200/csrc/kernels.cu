@@ -1046,7 +1046,7 @@ int temper_sharded_launches() { return 2 * 66 - 1; }  // + one exchange per phas
 cudaError_t launch_stats_sharded(const GroupDesc* gds, const int* list, int n_list, int dmax, Exchange& x,
                                  cudaStream_t st) {
   k_stats_grid<<<dim3(dmax, n_list), 256, 0, st>>>(gds, list);
-  cudaError_t e = x.reduce(1, 2 * dmax, XOP_SUM, st);
+  cudaError_t e = x.reduce(1, -1, XOP_SUM, st);  // 2d step statistics of each run
   if (e != cudaSuccess) return e;
   k_stats_final<<<n_list, 32, 0, st>>>(gds, list);
   return cudaGetLastError();

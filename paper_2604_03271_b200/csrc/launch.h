@@ -61,7 +61,8 @@ enum ExchangeOp : int { XOP_SUM = 0, XOP_MIN = 1, XOP_MAX = 2 };
 struct Exchange {
   virtual ~Exchange() = default;
   // reduce `count` doubles of every shard's g.xbuf (buf 0) or g.stat_acc (buf 1)
-  // across the shards of the run; every shard receives the result
+  // across the shards of each run (count < 0: the run's 2d step statistics);
+  // every shard receives the result
   virtual cudaError_t reduce(int buf, int count, int op, cudaStream_t st) = 0;
   // every shard's (xbuf[0], xbuf[1]) into every shard's g.xgat, in shard order
   virtual cudaError_t gather(cudaStream_t st) = 0;
@@ -73,10 +74,11 @@ cudaError_t launch_temper_sharded(const GroupDesc* d_gds, const int* d_list, int
 int temper_sharded_launches();
 cudaError_t launch_stats_sharded(const GroupDesc* d_gds, const int* d_list, int n_list, int dmax, Exchange& x,
                                  cudaStream_t st);
-// exchange among shards resident on this device (one stream, kernels)
-cudaError_t launch_xreduce(const GroupDesc* d_gds, const int* d_list, int n, int buf, int count, int op,
+// exchange among shards resident on this device (one stream, kernels); d_list
+// holds the nsh shards of each of nruns runs, run-major
+cudaError_t launch_xreduce(const GroupDesc* d_gds, const int* d_list, int nruns, int nsh, int buf, int count, int op,
                            cudaStream_t st);
-cudaError_t launch_xgather(const GroupDesc* d_gds, const int* d_list, int n, cudaStream_t st);
+cudaError_t launch_xgather(const GroupDesc* d_gds, const int* d_list, int nruns, int nsh, cudaStream_t st);
 
 // step-size statistics, one CTA per (component, group), + per-group finalisation
 cudaError_t launch_stats_grid(const GroupDesc* d_gds, const int* d_list, int n_list, int dmax, cudaStream_t st);

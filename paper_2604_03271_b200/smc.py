@@ -297,6 +297,22 @@ def smc_run_sharded(spec: ModelSpec, data: Spectrum, cfg: SmcConfig, n_virtual: 
         lib.specmc_result_free(C.byref(res))
 
 
+def smc_run_sharded_batch(problems: Sequence[Tuple[ModelSpec, int, SmcConfig]], spectra: Sequence[Spectrum],
+                          n_virtual: int = 1, comm: Optional[Comm] = None, raise_on_error: bool = True):
+    """Every (spec, spectrum index, cfg) split over the same shards, all at once
+    (e.g. the K range of a model selection); see smc_run_sharded."""
+    probs, sps, keep = _pack(problems, spectra)
+    res = (_lib.SmcResultC * len(problems))()
+    err = C.create_string_buffer(1024)
+    rc = lib.specmc_smc_run_sharded_batch(len(problems), probs, len(spectra), sps, int(n_virtual),
+                                          comm._h if comm is not None else None, res, err, 1024)
+    if rc and rc != _lib.SPECMC_ERUNTIME:
+        for i in range(len(problems)):
+            lib.specmc_result_free(C.byref(res[i]))
+        _raise(rc, err)
+    return _collect(problems, spectra, res, raise_on_error)
+
+
 def probe_mufu(device: int = 0) -> float:
     """Measured MUFU ex2 throughput (ops/s) of the device."""
     v = C.c_double()

@@ -80,3 +80,14 @@ def test_nccl_single_rank_equals_one_virtual_shard(smc):
         comm.close()
     b = smc.smc_run_sharded(w.spec(3), w.data, cfg, n_virtual=1)
     assert a.F == b.F and np.array_equal(a.posterior, b.posterior)
+
+
+def test_sharded_batch_equals_single_sharded_runs(smc):
+    # all K of a selection split over the same shards at once == one call per K, bitwise
+    w = syn.config("C1")
+    cfgs = {K: smc.SmcConfig(T=2048, n=8, seed=40 + K) for K in (1, 2, 3)}
+    batch = smc.smc_run_sharded_batch([(w.spec(K), 0, cfgs[K]) for K in (1, 2, 3)], [w.data], n_virtual=4)
+    for K, b in zip((1, 2, 3), batch):
+        one = smc.smc_run_sharded(w.spec(K), w.data, cfgs[K], n_virtual=4)
+        assert b.F == one.F and np.array_equal(b.posterior, one.posterior)
+    assert smc.model_select(list(zip((1, 2, 3), batch))).K_best == 3
