@@ -26,7 +26,6 @@ enum PriorKind : int { PR_NORMAL = 0, PR_GAMMA = 1, PR_UNIFORM = 2 };
 enum Role : uint32_t { ROLE_INIT = 1, ROLE_CHAIN = 2, ROLE_RESAMPLE = 3 };
 enum GroupError : int { GE_NONE = 0, GE_MAX_LEVELS = 1, GE_ZERO_WEIGHT = 2 };
 
-constexpr int kDMax = 128;     // max parameters per model on the device path
 constexpr int kHist = 5;       // predict_step_size window (mcmc.cpp:28)
 constexpr double kLogStepMin = -27.631021115928547;  // log(1e-12), mcmc.hpp:8
 constexpr double kLogStepMax = 27.631021115928547;   // log(1e12),  mcmc.hpp:9

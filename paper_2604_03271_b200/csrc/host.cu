@@ -96,7 +96,9 @@ void validate_model(const specmc_model_desc& m) {
     for (int b = 0; b < m.K; ++b)
       if (!cnt[b]) throw Error(SPECMC_EINVAL, "xrd phase has no reflections");
   }
-  if (m.K > 64 && m.family != SPECMC_FAMILY_OFFSET) throw Error(SPECMC_EINVAL, "device path supports K <= 64");
+  // the move kernel tracks faulty blocks in a 64-bit mask: K peaks, or K phases + the xrd background block
+  if (m.family != SPECMC_FAMILY_OFFSET && m.K + (m.family == SPECMC_FAMILY_XRD ? 1 : 0) > 64)
+    throw Error(SPECMC_EINVAL, "device path supports at most 64 blocks (K <= 64; xrd K <= 63)");
   if (m.d != model_dim(m)) throw Error(SPECMC_EINVAL, "model layout length mismatch");
   if (!m.prior_kind || !m.prior_a || !m.prior_b) throw Error(SPECMC_EINVAL, "model priors missing");
   for (int i = 0; i < m.d; ++i) {  // priors.cpp:9-20
@@ -514,10 +516,10 @@ struct ClassRun {
     shape = pick_shape(Nmax);
     if ((int64_t)32 * shape.W * shape.PPL < Nmax)
       throw Error(SPECMC_EINVAL, "spectrum has more points than the device path supports (8192)");
-    // module load of this class's kernels happens here, outside the timed level loop
-    cuda_check(prime_level_kernels(family, noise, shape, dmax), "loading the level kernels");
     if (chain_smem_bytes(shape, dmax) > 227 * 1024)
       throw Error(SPECMC_EINVAL, "model too large for the device path (shared memory)");
+    // module load of this class's kernels happens here, outside the timed level loop
+    cuda_check(prime_level_kernels(family, noise, shape, dmax), "loading the level kernels");
 
     std::map<std::pair<int, double>, PreparedSpectrum> prep;
     for (int r : idx) {

@@ -289,3 +289,18 @@ def test_criterion6_waste_free_bookkeeping(smc, port, T, n):
     L = int(rep.scalars["levels"])
     assert rep.trials == T * L and rep.proposals == T * L
     assert rep.posterior.shape == (1, T) and rep.energies.shape == (T,)
+
+
+@pytest.mark.parametrize("K", [16, 40, 64])
+def test_large_models_run(smc, K):
+    # d = 4K + 2 up to 258 components per chain (shared-memory chain state, 64-block fault mask)
+    sp, _ = syn.gen_xps(3, 5)
+    rep = smc.smc_run(M.xps_model(K, sp), sp, smc.SmcConfig(T=256, n=8, seed=1))
+    assert math.isfinite(rep.F) and rep.posterior.shape == (4 * K + 2, 256)
+
+
+def test_xrd_block_limit(smc):
+    xr, _ = syn.gen_xrd(300, 5)
+    phases = [syn.TIO2_PHASES[0]] * 64  # 64 phases + the background block > 64
+    with pytest.raises(ValueError):
+        smc.smc_run(M.xrd_model(phases, xr), xr, smc.SmcConfig(T=256, n=8, seed=1))
