@@ -47,8 +47,10 @@ __device__ __forceinline__ constexpr int block_stride() {
 }
 
 // gm:  g = A exp(-b/2 (x-mu)^2) = c1 2^(c2 d^2)                   (model.cpp:216-220)
-// xps: g = c1 2^(-t^2) + c2 / (1 + t^2), t = x/sigma - mu/sigma = fma(x, c3, mu'),
-//      c1 = A eta, c2 = A (1-eta)
+// xps: g = c1 2^(-u) + 1 / (c2 (1 + u)), u = t^2, t = x/sigma - mu/sigma = fma(x, c3, mu'),
+//      c1 = A eta, c2 = 1 / (A (1-eta)) (the Lorentzian amplitude folded into its
+//      reciprocal: one FMUL less per point; a zero Lorentzian amplitude becomes
+//      c2 = 1e30, i.e. a contribution <= 1e-30)
 //      (= A [eta exp(-ln2 d^2/s^2) + (1-eta) s^2/(s^2+d^2)], model.cpp:269-280)
 // offset: g = theta_0                              (conjugate_oracle.hpp:22-26)
 template <int FAM>
@@ -66,7 +68,8 @@ __device__ __forceinline__ BlockC block_consts(const float* p) {  // p: fp32 sha
     c.c3 = rcpf(sig);
     c.mu = -p[1] * c.c3;
     c.c1 = A * eta;
-    c.c2 = A - c.c1;
+    const float aL = A - c.c1;
+    c.c2 = aL != 0.f ? rcpf(aL) : 1e30f;
   } else {
     c.c1 = p[0];
     c.mu = 0.f;
@@ -82,7 +85,8 @@ __device__ __forceinline__ float shape(const BlockC& b, float x) {
     return b.c1 * ex2f(b.c2 * (d * d));
   } else if (FAM == FAM_XPS) {
     const float t = fmaf(x, b.c3, b.mu);
-    return fmaf(b.c1, ex2f(-(t * t)), b.c2 * rcpf(fmaf(t, t, 1.0f)));
+    const float u = t * t;
+    return fmaf(b.c1, ex2f(-u), rcpf(fmaf(u, b.c2, b.c2)));
   } else {
     return b.c1;
   }
@@ -103,10 +107,11 @@ struct Xch {  // per-unit cross-warp exchange, double-buffered by parity
 //             unit computes and writes identical values (idempotent), one unit
 //             barrier per sweep orders the sweep-level rewrites
 //   per unit: Xch, then G float [PPL][L] (cached g_b(x) of the block being swept)
-// committed peak signal P: registers, except for W == 4 where shared memory was
-// measured faster (register pressure); chosen per shape
+// committed peak signal P: shared memory for W = 2 and 4 (one trial signal in
+// registers leaves the allocator room: no spills at 128 registers), registers
+// for W = 1 and 8; see chain_p_in_smem (launch.h)
 template <int W>
-__host__ __device__ constexpr bool p_in_smem() { return W == 4; }
+__host__ __device__ constexpr bool p_in_smem() { return chain_p_in_smem(W); }
 
 template <int PPL, int W>
 struct Smem {
@@ -127,17 +132,21 @@ struct Smem {
 template <int PPL, int W>
 struct Unit {
   static constexpr int L = 32 * W;
+  static constexpr int NPT = PPL * L;
   const float* sx;
   const float2* sc;
   const float2* sy;
-  int nv;      // real (non-padding) points of this lane
-  float npad;  // PPL - nv
+  int nv;      // leading real (non-padding) points of this lane
+  float npad;  // padding points of this lane
+  bool tail;   // uniform xps layout: this lane's last slot holds the last real point
   Xch* xc;
   int lg, wiu, lane, bar_id;
   int par;
   __device__ __forceinline__ float x(int k) const { return sx[k * L + lg]; }
   __device__ __forceinline__ float2 c(int k) const { return sc[k * L + lg]; }
   __device__ __forceinline__ float2 y(int k) const { return sy[k * L + lg]; }
+  // paired noise layout (nz_pairs): (y_2p, y_2p+1) per point pair p
+  __device__ __forceinline__ float2 y2(int p) const { return sy[p * L + lg]; }
   __device__ __forceinline__ void sync() const {
     if (W > 1) named_bar(bar_id, L);
   }
@@ -232,7 +241,7 @@ __device__ __forceinline__ bool add_block(const GroupDesc& g, int b, const float
   } else {
     BlockC c = block_consts<FAM>(p);
     if (!c.ok) return false;
-    c.c1 *= sign;                      // amplitudes: gm c1; xps c1, c2 (gm c2 is the exponent)
+    c.c1 *= sign;                      // amplitudes: gm c1; xps c1, 1/c2 (gm c2 is the exponent)
     if (FAM == FAM_XPS) c.c2 *= sign;
 #pragma unroll
     for (int k = 0; k < PPL; ++k) acc[k] += shape<FAM>(c, u.x(k));
@@ -336,26 +345,44 @@ __device__ __forceinline__ float nz_var(const GroupDesc& g, float f) {
   if (NZ == NZ_HLIN) return fmaf(g.nz_a0, f, g.nz_a2);
   return f;  // NZ_HPROP
 }
+// (ya, yb) = the pair's observations (host, paired layout).  The lane keeps
+// three partials: quad += (ra^2 vb + rb^2 va) / (va vb), lg += lg2(va vb),
+// mn = min over the variances; its noise sum is q' quad + lg, and NaN
+// (E = +inf) unless every variance is > 0.  The lg2 terms are not centred
+// (~25 each at C2 counts; the host moves the per-point scales into e_a0): a
+// lane's fp32 sum of 16 of them carries ~1e-4 of rounding, ~1e-4 nats in N E.
+struct PairAcc {
+  float quad, lg, mn;
+};
 template <int NZ>
-__device__ __forceinline__ float noise_pair(const GroupDesc& g, float fa, float fb, float2 ya, float2 yb) {
-  const float ra = ya.x - fa, rb = yb.x - fb;
+__device__ __forceinline__ void noise_pair(const GroupDesc& g, float fa, float fb, float2 yab, PairAcc& a) {
+  const float ra = yab.x - fa, rb = yab.y - fb;
   const float va = nz_var<NZ>(g, fa), vb = nz_var<NZ>(g, fb);
   const float num = fmaf(ra * ra, vb, (rb * rb) * va);
-  const float la = copysignf((va * ya.y) * (vb * yb.y), fminf(va, vb));
-  return fmaf(g.nz_q, num * rcpf(va * vb), lg2f(la));
+  const float vv = va * vb;
+  a.quad = fmaf(num, rcpf(vv), a.quad);
+  a.lg += lg2f(vv);
+  a.mn = fminf(a.mn, fminf(va, vb));  // one FMNMX3
 }
-// f(k) -> sum of the noise terms of this lane's PPL points, and the padding
-// correction: padding points (k >= nv) replicate the lane's last point, so
-// npad copies of its term are removed at once
-template <int NZ, int PPL, int W, class F>
+template <int NZ>
+__device__ __forceinline__ float pair_total(const GroupDesc& g, const PairAcc& a) {
+  const float t = fmaf(g.nz_q, a.quad, a.lg);
+  return a.mn > 0.f ? t : __int_as_float(0x7fc00000);
+}
+// f(k) -> sum of the noise terms of this lane's PPL points, and (CORR) the
+// padding correction: padding points (k >= nv) replicate the lane's last point,
+// so npad copies of its term are removed at once.  Without CORR the caller
+// removes the padding terms (uniform xps layout, eval_shirley_nz).
+template <int NZ, int PPL, int W, bool CORR = true, class F>
 __device__ __forceinline__ float lane_noise_sum(const GroupDesc& g, const Unit<PPL, W>& u, F&& fk) {
   float acc = 0.f, tl = 0.f, fprev = 0.f, flast = 0.f;
+  PairAcc pa{0.f, 0.f, FLT_MAX};
 #pragma unroll
   for (int k = 0; k < PPL; ++k) {
     const float f = fk(k);
     if (nz_pairs<NZ>()) {
       if (k & 1)
-        acc += noise_pair<NZ>(g, fprev, f, u.y(k - 1), u.y(k));
+        noise_pair<NZ>(g, fprev, f, u.y2(k >> 1), pa);
       else
         fprev = f;
       flast = f;
@@ -364,8 +391,10 @@ __device__ __forceinline__ float lane_noise_sum(const GroupDesc& g, const Unit<P
       acc += tl;
     }
   }
+  if (nz_pairs<NZ>()) acc = pair_total<NZ>(g, pa);
+  if (!CORR) return acc;
   if (!nz_pairs<NZ>()) return fmaf(-u.npad, tl, acc);
-  if (u.npad > 0.f) acc = fmaf(-u.npad, noise_term<NZ>(g, flast, u.y(PPL - 1)), acc);
+  if (u.npad > 0.f) acc = fmaf(-u.npad, noise_term<NZ>(g, flast, make_float2(g.y_last, g.s_last)), acc);
   return acc;
 }
 
@@ -384,23 +413,13 @@ __device__ __forceinline__ double eval_plain_nz(const GroupDesc& g, Unit<PPL, W>
 // Shirley background + energy (lineshapes.hpp:65-83, model.cpp:289-292).
 // amp_bound >= max_k |P_k| (sum of |amplitudes|) decides the degenerate-signal
 // test without a max reduction unless it is inconclusive.
-template <int PPL, int W, int NZ>
-__device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, W>& u, const float (&Pn)[PPL],
-                                                  float bga, float bgb, float amp_bound) {
-  // pass 1: lane-local inclusive scan of c_k Pn_k; C_k is kept for PPL <= 16 and
-  // recomputed in pass 2 for longer lanes (register budget)
-  constexpr bool kKeepC = PPL <= 16;
-  float Cn[kKeepC ? PPL : 1];
-  float run = 0.f;
-#pragma unroll
-  for (int k = 0; k < PPL; ++k) {
-    const float2 c = u.c(k);
-    run = fmaf(c.x, Pn[k], run);
-    if (kKeepC) Cn[k] = fmaf(-c.y, Pn[k], run);
-  }
-  const float incl = warp_incl_scan_f(run, u.lane);
-  float prefix = incl - run;
-  float total = __shfl_sync(0xffffffffu, incl, 31);
+// scan of the lane values v over the unit: exclusive prefix and total (every
+// lane of every warp gets the same total)
+template <int PPL, int W>
+__device__ __forceinline__ void unit_scan(Unit<PPL, W>& u, float v, float& prefix, float& total) {
+  const float incl = warp_incl_scan_f(v, u.lane);
+  prefix = incl - v;
+  total = __shfl_sync(0xffffffffu, incl, 31);
   if (W > 1) {
     if (u.lane == 0) u.xc->scan[u.par][u.wiu] = total;
     u.sync();
@@ -414,23 +433,92 @@ __device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, 
     prefix += pre;
     total = tot;
   }
+}
+
+// inconclusive degenerate-signal bound: exact max of Pn over the real points
+// of the unit (rare)
+template <int PPL, int W>
+__device__ __forceinline__ float unit_max_real(Unit<PPL, W>& u, const float (&Pn)[PPL]) {
+  float mx = -FLT_MAX;
+#pragma unroll
+  for (int k = 0; k < PPL; ++k)
+    if (k < u.nv) mx = fmaxf(mx, Pn[k]);
+  if (u.tail) mx = fmaxf(mx, Pn[PPL - 1]);
+  mx = warp_max_f(mx);
+  if (W > 1) {
+    u.sync();  // everyone has consumed scan[par] above
+    if (u.lane == 0) u.xc->scan[u.par][u.wiu] = mx;
+    u.sync();
+    for (int w = 0; w < W; ++w) mx = fmaxf(mx, u.xc->scan[u.par][w]);
+    u.sync();
+  }
+  return mx;
+}
+
+// Shirley background on a uniform grid (GroupDesc::sh_uniform).  With spacing
+// D the trapezoid integral is C_k = D (R_k - P_0/2 - P_k/2), R_k = sum_{j<=k} P_j,
+// and D cancels in C/C_{N-1}: the scan sums Pn alone, with -P_0/2 seeded on
+// lane 0 and -P_{N-1}/2 taken off the last lane's contribution (the layout
+// keeps both endpoints at fixed slots; padding has Pn = 0, so it adds nothing
+// and all padding points of a lane share one f).  Per point: one FADD in each
+// pass and two FFMA for f, no weight loads.
+template <int PPL, int W, int NZ>
+__device__ __forceinline__ double eval_shirley_uniform(const GroupDesc& g, Unit<PPL, W>& u, const float (&Pn)[PPL],
+                                                       float bga, float bgb, float amp_bound) {
+  const float init = u.lg == 0 ? -0.5f * Pn[0] : 0.f;
+  float run = init;
+#pragma unroll
+  for (int k = 0; k < PPL; ++k) run += Pn[k];
+  const float v = u.tail ? fmaf(-0.5f, Pn[PPL - 1], run) : run;
+  float prefix, total;
+  unit_scan(u, v, prefix, total);
+  const float ba = bgb - bga;
+  const float rng = (float)(g.N - 1);  // range / D
+  bool degen = !(total > 1e-12f * amp_bound * rng);
+  if (degen) degen = !(total > 1e-12f * unit_max_real(u, Pn) * rng);
+  float acc, fpad;
+  if (!degen) {
+    const float scale = ba * rcpf(total);
+    const float m = fmaf(-0.5f, scale, 1.f);
+    // f_k = Pn_k + a + scale (R_k - P_0/2 - Pn_k/2) = B_k + m Pn_k with the
+    // running background B_k = a + scale (R_k - P_0/2): two FFMA per point
+    float B = fmaf(scale, prefix + init, bga);
+    acc = lane_noise_sum<NZ, PPL, W, false>(g, u, [&](int k) {
+      B = fmaf(scale, Pn[k], B);
+      return fmaf(m, Pn[k], B);
+    });
+    fpad = u.tail ? fmaf(-scale, Pn[PPL - 1], B) : B;
+  } else {  // linear ramp a -> b (padding sits at x = 1e30: clamp to the last point)
+    const float sl = ba * g.inv_range;
+    acc = lane_noise_sum<NZ, PPL, W, false>(g, u, [&](int k) {
+      return Pn[k] + fmaf(sl, fminf(u.x(k), g.x1s) - g.x0s, bga);
+    });
+    fpad = fmaf(sl, g.x1s - g.x0s, bga);
+  }
+  if (u.npad > 0.f) acc = fmaf(-u.npad, noise_term<NZ>(g, fpad, make_float2(g.y_last, g.s_last)), acc);
+  return finish_energy<NZ>(g, unit_sum(u, acc));
+}
+
+template <int PPL, int W, int NZ>
+__device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, W>& u, const float (&Pn)[PPL],
+                                                  float bga, float bgb, float amp_bound) {
+  if (g.sh_uniform) return eval_shirley_uniform<PPL, W, NZ>(g, u, Pn, bga, bgb, amp_bound);
+  // pass 1: lane-local inclusive scan of c_k Pn_k; C_k is kept for PPL <= 16 and
+  // recomputed in pass 2 for longer lanes (register budget)
+  constexpr bool kKeepC = PPL <= 16;
+  float Cn[kKeepC ? PPL : 1];
+  float run = 0.f;
+#pragma unroll
+  for (int k = 0; k < PPL; ++k) {
+    const float2 c = u.c(k);
+    run = fmaf(c.x, Pn[k], run);
+    if (kKeepC) Cn[k] = fmaf(-c.y, Pn[k], run);
+  }
+  float prefix, total;
+  unit_scan(u, run, prefix, total);
   const float ba = bgb - bga;
   bool degen = !(total > 1e-12f * amp_bound * g.range);
-  if (degen) {  // inconclusive bound: exact max over the real points (rare)
-    float mx = -FLT_MAX;
-#pragma unroll
-    for (int k = 0; k < PPL; ++k)
-      if (k < u.nv) mx = fmaxf(mx, Pn[k]);
-    mx = warp_max_f(mx);
-    if (W > 1) {
-      u.sync();  // everyone has consumed scan[par] above
-      if (u.lane == 0) u.xc->scan[u.par][u.wiu] = mx;
-      u.sync();
-      for (int w = 0; w < W; ++w) mx = fmaxf(mx, u.xc->scan[u.par][w]);
-      u.sync();
-    }
-    degen = !(total > 1e-12f * mx * g.range);
-  }
+  if (degen) degen = !(total > 1e-12f * unit_max_real(u, Pn) * g.range);  // inconclusive bound
   float acc;
   if (!degen) {
     const float scale = ba * rcpf(total);
@@ -517,7 +605,7 @@ __device__ __forceinline__ float amp_sum(const GroupDesc& g, const float* thf) {
 // registers: PPL <= 8 -> 3 CTAs of 256 threads per SM (<= 85 regs), else 2 (<= 128)
 template <int W, int PPL>
 struct Bounds {
-  static constexpr int threads = W >= 8 ? 32 * W : 256;
+  static constexpr int threads = chain_threads(W);
   static constexpr int min_blocks = (65536 / threads) / (PPL <= 8 ? 85 : 128) > 0 ? (65536 / threads) / (PPL <= 8 ? 85 : 128) : 1;
   // (PPL = 32: 2 x 256 threads at <= 128 registers as well)
 };
@@ -556,7 +644,7 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
   double* En = g.E[cur ^ 1];
   // components inside a block (everything but the xps Shirley endpoints and the offset family)
   const int npeak = FAM == FAM_OFFSET ? 0 : (FAM == FAM_XRD ? g.d : stride * g.K);
-  unsigned long long trials = 0;
+  unsigned trials = 0;
   // Q[k] at Qs[k * L]: signal of every block except the one being swept (P - g_b)
   float* Qs = gcache + (size_t)unit * SM::NPT + u.lg;
   // committed peak signal: registers, or shared memory (Ps[k * L]) when p_in_smem<W>()
@@ -570,6 +658,7 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
 #define SMC_P(k) (kPsm ? Ps[(k) * L] : P[k])
 
   const double bnd = beta * nd;
+  const bool beta0 = beta == 0.0;
   for (int t = 1; t <= n; ++t) {
     u.sync();  // every warp of the unit is done with the previous sweep's shared arrays
     // ---- sweep prologue, lane-parallel over components.  Component i's value
@@ -609,13 +698,18 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
       float Pn[PPL];
       unsigned long long fnew = fmask;
       float dA = 0.f;
+      // Shirley endpoint: enters combine() only (block -1), the peak signal is
+      // unchanged and (registers) evaluated in place: no copy, no commit
+      const bool endpoint = FAM == FAM_XPS && !peak;  // (gm, xrd: every component is in a block)
       if (FAM == FAM_OFFSET) {
         const float dv = newf - oldf;
 #pragma unroll
         for (int k = 0; k < PPL; ++k) Pn[k] = SMC_P(k) + dv;
-      } else if (!peak) {  // Shirley endpoint: enters combine() only (block -1)
+      } else if (endpoint) {
+        if (kPsm) {
 #pragma unroll
-        for (int k = 0; k < PPL; ++k) Pn[k] = SMC_P(k);
+          for (int k = 0; k < PPL; ++k) Pn[k] = SMC_P(k);
+        }
       } else if (j == 0 && oldf != 0.f && !((fmask >> b) & 1ull) &&
                  (FAM != FAM_XRD || b < g.K)) {  // amplitude: g' = (A'/A) g
         const float r = (newf - oldf) * rcpf(oldf);
@@ -643,15 +737,21 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
         bga = i == ibg ? newf : thf[ibg];
         bgb = i == ibg + 1 ? newf : thf[ibg + 1];
       }
-      const double e_new = fnew ? dinf() : evaluate_nz<FAM, PPL, W, NZ>(g, u, Pn, bga, bgb, asum + dA);
+      double e_new;
+      if (fnew)
+        e_new = dinf();
+      else if (!kPsm && endpoint)
+        e_new = evaluate_nz<FAM, PPL, W, NZ>(g, u, P, bga, bgb, asum);
+      else
+        e_new = evaluate_nz<FAM, PPL, W, NZ>(g, u, Pn, bga, bgb, asum + dA);
       // mcmc.cpp:72-80
       const double dlp = dlpb[i];
       double lr;
-      if (e_new < dinf() && e < dinf() && beta != 0.0) {
+      if (e_new < dinf() && e < dinf() && !beta0) {
         lr = fma(-bnd, e_new - e, dlp);
       } else {
         const bool inf_new = e_new == dinf(), inf_old = e == dinf();
-        if (beta == 0.0 || (inf_new && inf_old))
+        if (beta0 || (inf_new && inf_old))
           lr = dlp;
         else if (inf_new)
           lr = -dinf();
@@ -660,12 +760,12 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
       }
       const bool accept = lr >= 0.0 || (double)lub[i] < lr;
       // commit: Q (other blocks) is unchanged; P updated in place (select) or in shared memory
-      if (!kPsm) {
+      if (!kPsm && !endpoint) {
 #pragma unroll
         for (int k = 0; k < PPL; ++k) P[k] = accept ? Pn[k] : P[k];
       }
       if (accept) {
-        if (kPsm) {
+        if (kPsm && !endpoint) {
 #pragma unroll
           for (int k = 0; k < PPL; ++k) Ps[k * L] = Pn[k];
         }
@@ -710,8 +810,8 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
     }
   }
 #undef SMC_P
-  trials = __reduce_add_sync(0xffffffffu, (unsigned)trials);
-  if (wiu == 0 && lane == 0) atomicAdd(&g.st->trials, trials);
+  trials = __reduce_add_sync(0xffffffffu, trials);
+  if (wiu == 0 && lane == 0) atomicAdd(&g.st->trials, (unsigned long long)trials);
 }
 
 template <int FAM, int PPL, int W, bool ENERGY, int NZ>
@@ -749,9 +849,10 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     constexpr uint32_t bx = SM::NPT * 4u, bc = SM::NPT * 8u, by = SM::NPT * 8u;
-    mbar_expect_tx(bar, bx + (FAM == FAM_XPS ? bc : 0u) + by);
+    const bool wc = FAM == FAM_XPS && !g.sh_uniform;  // trapezoid weights (non-uniform grids only)
+    mbar_expect_tx(bar, bx + (wc ? bc : 0u) + by);
     bulk_g2s(sx, g.spec_x, bx, bar);
-    if (FAM == FAM_XPS) bulk_g2s(sc, g.spec_c, bc, bar);
+    if (wc) bulk_g2s(sc, g.spec_c, bc, bar);
     bulk_g2s(sy, g.spec_y, by, bar);
   }
   __syncthreads();
@@ -771,8 +872,15 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   u.lane = lane;
   u.bar_id = 1 + unit;
   u.par = 0;
-  u.nv = min(max(g.N - u.lg * PPL, 0), PPL);
-  u.npad = (float)(PPL - u.nv);
+  if (FAM == FAM_XPS && g.sh_uniform) {  // points 0..N-2 lead, point N-1 in the last slot
+    u.nv = min(max(g.N - 1 - u.lg * PPL, 0), PPL);
+    u.tail = u.lg == Unit<PPL, W>::L - 1;
+    u.npad = (float)(PPL - u.nv - (u.tail ? 1 : 0));
+  } else {
+    u.nv = min(max(g.N - u.lg * PPL, 0), PPL);
+    u.tail = false;
+    u.npad = (float)(PPL - u.nv);
+  }
 
   const GroupState* st = g.st;
   const int cur = st->cur;

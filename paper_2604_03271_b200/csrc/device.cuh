@@ -78,10 +78,19 @@ struct GroupDesc {  // immutable per group
   float nz_a0, nz_a1, nz_a2, nz_q;
   // shirley helpers (shifted x)
   float x0s, inv_range, range;
+  // xps on a uniform ascending grid (sh_uniform): the trapezoid weights are
+  // constant, so the Shirley scan sums Pn alone (no per-point weights).  The
+  // spectrum layout then keeps the first and the last real point at fixed lane
+  // slots: points 0..N-2 at positions 0..N-2, point N-1 at the last position,
+  // padding in between at x = 1e30 (every peak shape is exactly 0 there)
+  int sh_uniform;
+  float x1s;  // shifted abscissa of the last point (linear-ramp fallback clamp)
   // spectrum (lane-transposed, see header)
   const float* spec_x;   // shifted abscissa x' = x - x_shift
   const float2* spec_c;  // (c_k, h_{k+1}): trapezoid weights of the Shirley scan
-  const float2* spec_y;  // (y_k, 1/s_k): observation and inverse noise scale
+  const float2* spec_y;  // (y_k, 1/s_k): observation and inverse noise scale; paired noise
+                         // models: (y_2p, y_2p+1) per point pair, then 1/(s_2p s_2p+1)
+  float y_last, s_last;  // (y, 1/s) of the last point (padding replicates it)
   // xrd reflections (mu_ref, rel_intensity) grouped by phase: phase b owns [refl_off[b], refl_off[b+1])
   const float2* refl;
   const int* refl_off;

@@ -301,7 +301,9 @@ struct PreparedSpectrum {
   std::vector<float> c;  // (c_k, h_{k+1}) pairs
   std::vector<float> y;  // (y_k, 1/s_k) pairs
   double x_shift = 0.0;
-  float x0s = 0.f, inv_range = 0.f, range = 0.f;
+  float x0s = 0.f, inv_range = 0.f, range = 0.f, x1s = 0.f;
+  bool uniform = false;  // xps on a uniform grid (GroupDesc::sh_uniform)
+  float y_last = 0.f, s_last = 1.f;
   double e_a0 = 0.0, e_a1 = 0.0;
   float a0 = 0.f, a1 = 0.f, a2 = 0.f, q = 0.5f;
   int nz = NZ_GAUSS;
@@ -335,6 +337,7 @@ PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, 
   ps.range = (float)range;
   ps.inv_range = (float)(1.0 / range);
   ps.x0s = (float)(xs[0] - x_shift);
+  ps.x1s = (float)(xs[N - 1] - x_shift);
   // noise
   std::vector<double> inv_s(N, 1.0);
   double a0 = 0.0;
@@ -386,20 +389,51 @@ PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, 
       break;
     }
   }
-  // padding points replicate the last real point; the kernel skips them by lane count
+  // xps on a uniform ascending grid: constant trapezoid weights (chain.cuh
+  // eval_shirley_nz).  Uniform = every spacing within 2e-7 (relative) of the
+  // mean, below the fp32 rounding of the per-point weights it replaces.
+  if (m.family == SPECMC_FAMILY_XPS && N >= 3 && range > 0.0) {
+    const double dx = range / (double)(N - 1);
+    bool uni = true;
+    for (int64_t i = 1; i < N && uni; ++i) uni = std::fabs((xs[i] - xs[i - 1]) - dx) <= 2e-7 * dx;
+    ps.uniform = uni;
+  }
+  // noise models whose terms the kernel evaluates two points at a time
+  // (chain.cuh nz_pairs): (y_2p, y_2p+1) per pair, 4 B per point.  Their lg2
+  // terms are not centred by 1/s_k: e_a0 takes sum_k ln(1/s_k) / 2N instead
+  const bool paired = ps.nz == NZ_HETERO || ps.nz == NZ_HLIN || ps.nz == NZ_HPROP;
+  if (paired) {
+    double ls = 0.0;
+    for (int64_t i = 0; i < N; ++i) ls += std::log(inv_s[i]);
+    ps.e_a0 += 0.5 * ls / (double)N;
+  }
+  // padding points replicate the last real point (the kernel removes their
+  // terms by lane count); uniform xps: points 0..N-2 first, point N-1 in the
+  // last slot, padding between at x = 1e30 (peak signal exactly 0)
+  auto src = [&](size_t p) -> int64_t {  // spectrum point stored at slot p
+    if (ps.uniform) return p + 1 < (size_t)N ? (int64_t)p : N - 1;
+    return p < (size_t)N ? (int64_t)p : N - 1;
+  };
   for (size_t p = 0; p < npt; ++p) {
-    const int64_t q = p < (size_t)N ? (int64_t)p : N - 1;
-    const bool real = p < (size_t)N;
+    const int64_t q = src(p);
+    const bool real = ps.uniform ? (p + 1 < (size_t)N || p + 1 == npt) : p < (size_t)N;
     const int lane = (int)(p / s.PPL), k = (int)(p % s.PPL);
     const size_t idx = (size_t)k * L + lane;
     const double hk = q > 0 ? 0.5 * (xs[q] - xs[q - 1]) : 0.0;
     const double hk1 = q + 1 < N ? 0.5 * (xs[q + 1] - xs[q]) : 0.0;
-    ps.x[idx] = (float)(xs[q] - x_shift);
+    ps.x[idx] = (ps.uniform && !real) ? 1e30f : (float)(xs[q] - x_shift);
     ps.c[2 * idx] = real ? (float)(hk + hk1) : 0.f;
     ps.c[2 * idx + 1] = real ? (float)hk1 : 0.f;
-    ps.y[2 * idx] = (float)ys[q];
-    ps.y[2 * idx + 1] = (float)inv_s[q];
+    if (paired) {  // (y_2p, y_2p+1) at pair slot (k/2) * L + lane
+      const size_t pidx = (size_t)(k >> 1) * L + lane;
+      ps.y[2 * pidx + (k & 1)] = (float)ys[q];
+    } else {
+      ps.y[2 * idx] = (float)ys[q];
+      ps.y[2 * idx + 1] = (float)inv_s[q];
+    }
   }
+  ps.y_last = (float)ys[N - 1];
+  ps.s_last = paired ? 1.f : (float)inv_s[N - 1];
   return ps;
 }
 
@@ -427,6 +461,12 @@ struct RunSpec {
   int64_t T_loc0 = 0, pbase = 0;
   int problem = 0;  // index of the run in the caller's batch
 };
+
+using SpecKey = std::tuple<int, double, int, int, double, double, double, double, int>;
+SpecKey spec_key(const RunSpec& R) {
+  const auto& m = R.m;
+  return SpecKey(R.spectrum, R.x_shift, m.family, m.noise, m.s0, m.s1, m.s2, m.noise_sigma, m.paper_literal);
+}
 
 struct Device {
   int ordinal;
@@ -513,17 +553,19 @@ struct ClassRun {
       dmax = std::max(dmax, runs[r].m.d);
       Tmax = std::max<int>(Tmax, (int)runs[r].cfg.T);
     }
-    shape = pick_shape(Nmax);
+    shape = pick_shape(Nmax, dmax);
     if ((int64_t)32 * shape.W * shape.PPL < Nmax)
       throw Error(SPECMC_EINVAL, "spectrum has more points than the device path supports (8192)");
-    if (chain_smem_bytes(shape, dmax) > 227 * 1024)
+    if (chain_smem_bytes(shape, dmax) > kChainSmemMax)
       throw Error(SPECMC_EINVAL, "model too large for the device path (shared memory)");
     // module load of this class's kernels happens here, outside the timed level loop
     cuda_check(prime_level_kernels(family, noise, shape, dmax), "loading the level kernels");
 
-    std::map<std::pair<int, double>, PreparedSpectrum> prep;
+    // one prepared copy per (spectrum, shift, noise parameters): the inverse
+    // noise scales and the centring constants depend on the noise model
+    std::map<SpecKey, PreparedSpectrum> prep;
     for (int r : idx) {
-      const auto key = std::make_pair(runs[r].spectrum, runs[r].x_shift);
+      const auto key = spec_key(runs[r]);
       if (!prep.count(key)) {
         const auto& sp = spectra[runs[r].spectrum];
         prep.emplace(key, prepare_spectrum(runs[r].m, sp.xs, sp.ys, sp.n, shape, runs[r].x_shift));
@@ -564,7 +606,7 @@ struct ClassRun {
       h2d(d_xlist, xl.data(), G, st);
     }
 
-    std::map<std::pair<int, double>, std::tuple<float*, float2*, float2*>> dspec;
+    std::map<SpecKey, std::tuple<float*, float2*, float2*>> dspec;
     for (auto& kv : prep) {
       float* x = ar.take<float>(npt);
       float2* c = ar.take<float2>(npt);
@@ -580,7 +622,7 @@ struct ClassRun {
     for (int gi = 0; gi < G; ++gi) {
       const RunSpec& R = runs[idx[gi]];
       runs_T0[gi] = R.nshards > 1 || xch ? R.T_loc0 : (int64_t)R.cfg.T;
-      const auto key = std::make_pair(R.spectrum, R.x_shift);
+      const auto key = spec_key(R);
       const PreparedSpectrum& ps = prep.at(key);
       GroupDesc& g = gds[gi];
       std::memset(&g, 0, sizeof(g));
@@ -608,6 +650,10 @@ struct ClassRun {
       g.x0s = ps.x0s;
       g.inv_range = ps.inv_range;
       g.range = ps.range;
+      g.sh_uniform = ps.uniform ? 1 : 0;
+      g.x1s = ps.x1s;
+      g.y_last = ps.y_last;
+      g.s_last = ps.s_last;
       auto t = dspec.at(key);
       g.spec_x = std::get<0>(t);
       g.spec_c = std::get<1>(t);
@@ -925,7 +971,7 @@ struct Session {
     // one class per (family, noise model, launch shape): each has its own move kernel
     std::map<std::tuple<int, int, int>, std::vector<int>> cls;
     for (int i = 0; i < n_problems; ++i) {
-      const Shape s = pick_shape(runs[i].N);
+      const Shape s = pick_shape(runs[i].N, runs[i].m.d);
       cls[{runs[i].m.family, dev_noise(runs[i].m), s.W * 100 + s.PPL}].push_back(i);
     }
     for (auto& kv : cls) {
@@ -1096,7 +1142,7 @@ int run_sharded_batch(int n_problems, const specmc_problem* problems, int n_spec
   // one class per (family, noise model, launch shape); runs stay run-major, shard order
   std::map<std::tuple<int, int, int>, std::vector<int>> cls;
   for (int i = 0; i < (int)runs.size(); ++i) {
-    const Shape s = pick_shape(runs[i].N);
+    const Shape s = pick_shape(runs[i].N, runs[i].m.d);
     cls[{runs[i].m.family, dev_noise(runs[i].m), s.W * 100 + s.PPL}].push_back(i);
   }
   std::vector<specmc_smc_result> res(runs.size());
@@ -1374,7 +1420,7 @@ int specmc_energy_batch(const specmc_model_desc* model, const double* xs, const 
     specmc_spectrum sp{xs, ys, n_points};
     RunSpec R = make_runspec(*model, 0, cfg, sp);
     Device dev(device);
-    const Shape shape = pick_shape(n_points);
+    const Shape shape = pick_shape(n_points, model->d);
     if ((int64_t)32 * shape.W * shape.PPL < n_points)
       throw Error(SPECMC_EINVAL, "spectrum has more points than the device path supports (8192)");
     const PreparedSpectrum ps = prepare_spectrum(*model, xs, ys, n_points, shape, R.x_shift);
@@ -1436,6 +1482,10 @@ int specmc_energy_batch(const specmc_model_desc* model, const double* xs, const 
     g.x0s = ps.x0s;
     g.inv_range = ps.inv_range;
     g.range = ps.range;
+    g.sh_uniform = ps.uniform ? 1 : 0;
+    g.x1s = ps.x1s;
+    g.y_last = ps.y_last;
+    g.s_last = ps.s_last;
     g.spec_x = dx;
     g.spec_c = dc;
     g.spec_y = dy;
@@ -1598,7 +1648,7 @@ void specmc_stats_reset(void) {
 
 int specmc_launch_shape(int64_t n_points, int32_t* W, int32_t* PPL, int32_t* U) {
   if (n_points < 1) return SPECMC_EINVAL;
-  const Shape s = pick_shape(n_points);
+  const Shape s = pick_shape(n_points, 0);  // shape for a model that fits any W
   if (W) *W = s.W;
   if (PPL) *PPL = s.PPL;
   if (U) *U = s.U;

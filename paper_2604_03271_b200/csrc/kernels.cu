@@ -881,7 +881,7 @@ bool ppl_supported(int ppl) { return ppl >= 2 && ppl <= 16 && ppl % 2 == 0; }
 // W warps per chain, PPL points per lane; must match SMC_FOR_EACH_SHAPE (chain.cuh).
 // Fewest warps per chain first (fewer cross-warp barriers per proposal), then
 // the smallest PPL that covers N (least padding).
-Shape pick_shape(int64_t N) {
+Shape pick_shape(int64_t N, int dmax) {
   Shape s;
   static const int w1[] = {2, 4, 6, 8, 10, 12, 14, 16};
   static const int w2[] = {10, 12, 14, 16, 20, 24, 28, 32};
@@ -891,7 +891,7 @@ Shape pick_shape(int64_t N) {
     if (sscanf(env, "%d,%d", &w, &p) == 2 && (int64_t)32 * w * p >= N) {
       s.W = w;
       s.PPL = p;
-      s.U = 8 / s.W;
+      s.U = chain_threads(s.W) / (32 * s.W);
       return s;
     }
   }
@@ -912,7 +912,19 @@ Shape pick_shape(int64_t N) {
       s.PPL = list[i];
       break;
     }
-  s.U = 8 / s.W;
+  s.U = chain_threads(s.W) / (32 * s.W);
+  // W = 2 keeps 8 units' P and Q caches in shared memory: a large model that
+  // does not fit takes the W = 4 shape (2 units per CTA) instead
+  if (s.W == 2 && chain_smem_bytes(s, dmax) > kChainSmemMax) {
+    s.W = 4;
+    s.PPL = w48[0];
+    for (int i = 0; i < 4; ++i)
+      if ((int64_t)128 * w48[i] >= N) {
+        s.PPL = w48[i];
+        break;
+      }
+    s.U = chain_threads(s.W) / (32 * s.W);
+  }
   return s;
 }
 
@@ -921,7 +933,7 @@ size_t chain_smem_bytes(const Shape& s, int dmax) {  // must match Smem<PPL, W>:
   const size_t npt = (size_t)s.PPL * 32 * s.W;
   size_t b = 16 + npt * (4 + 8 + 8) + (size_t)s.U * dpad * (8 + 8 + 4 + 8 + 8 + 4 + 4 + 4 + 4);
   b = (b + 15) & ~(size_t)15;
-  return b + (size_t)s.U * sizeof(Xch) + (size_t)s.U * npt * (s.W == 4 ? 8 : 4);  // Q (and P, p_in_smem<W>() in chain.cuh)
+  return b + (size_t)s.U * sizeof(Xch) + (size_t)s.U * npt * (chain_p_in_smem(s.W) ? 8 : 4);  // Q (and P)
 }
 
 cudaError_t launch_energy(int family, const Shape& s, int dmax, const GroupDesc* gds, const int* list,

@@ -16,7 +16,14 @@ struct Shape {
   int U;
 };
 
-Shape pick_shape(int64_t N);
+// chain-kernel CTA size per unit width W (units per CTA = threads / 32 W):
+// W = 2 runs 8 units per 512-thread CTA, one CTA per SM, so the spectrum is
+// staged once per SM and the 8 units' P and Q caches fit in shared memory
+__host__ __device__ constexpr int chain_threads(int W) { return W >= 8 ? 32 * W : (W == 2 ? 512 : 256); }
+__host__ __device__ constexpr bool chain_p_in_smem(int W) { return W == 2 || W == 4; }
+
+constexpr size_t kChainSmemMax = 227 * 1024;  // dynamic shared memory per CTA
+Shape pick_shape(int64_t N, int dmax);
 bool ppl_supported(int ppl);
 size_t chain_smem_bytes(const Shape& s, int dmax);
 

@@ -40,6 +40,16 @@ def _cases():
     cases.append(("c2_xps6", w.spec(6), w.data))
     w1 = syn.config("C1")
     cases.append(("c1_gm3", w1.spec(3), w1.data))
+    # grid layouts of the xps Shirley scan: uniform grids take the weight-free
+    # scan (endpoints at fixed lane slots), others the per-point trapezoid weights
+    rng = np.random.default_rng(3)
+    xj = np.sort(sp.xs + rng.uniform(-0.02, 0.02, len(sp.xs)))
+    spj = M.Spectrum(xj, sp.ys.copy())
+    cases.append(("xps3_jittered_grid", M.xps_model(3, spj), spj))
+    for n in (64, 65, 3):  # no padding, one real point past a full lane set, tiny
+        idx = np.linspace(0, len(sp.xs) - 1, n).round().astype(int)
+        spn = M.Spectrum(np.linspace(sp.xs[0], sp.xs[-1], n), sp.ys[idx].copy())
+        cases.append((f"xps2_n{n}", M.xps_model(2, spn), spn))
     xr, _ = syn.gen_xrd(600, 5)
     cases.append(("xrd3_poisson", M.xrd_model(syn.TIO2_PHASES, xr), xr))
     cases.append(("xrd3_gapprox", M.xrd_model(syn.TIO2_PHASES, xr, M.GaussianApproxPoissonNoise()), xr))
