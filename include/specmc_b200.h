@@ -135,6 +135,11 @@ int specmc_smc_run_batch(int32_t n_problems, const specmc_problem* problems, int
 
 void specmc_result_free(specmc_smc_result* r);
 
+/* Frees one result array whose ownership the caller took over (it then sets
+ * the field to NULL before specmc_result_free): lets a binding hand the
+ * posterior block to its own array type without copying it. */
+void specmc_free(void* p);
+
 /* ---- device-resident sessions -----------------------------------------
  * specmc_smc_run_batch == create + run + fetch + destroy.  A session keeps the
  * spectra, priors and particle buffers resident in HBM; run() re-runs every

@@ -55,7 +55,7 @@ class StatsC(C.Structure):
 
 # every symbol include/specmc_b200.h declares (tests/test_abi.py checks the header agrees)
 EXPORTS = [
-    "specmc_smc_run", "specmc_smc_run_batch", "specmc_result_free", "specmc_energy_batch", "specmc_ess",
+    "specmc_smc_run", "specmc_smc_run_batch", "specmc_result_free", "specmc_free", "specmc_energy_batch", "specmc_ess",
     "specmc_log_mean_exp", "specmc_next_beta", "specmc_systematic_resample", "specmc_predict_step_size",
     "specmc_validate_config", "specmc_validate_problem", "specmc_stats_get", "specmc_stats_reset",
     "specmc_launch_shape", "specmc_device_count", "specmc_version", "specmc_session_create", "specmc_session_run",
@@ -100,6 +100,8 @@ def _load():
         lib.specmc_comm_destroy.restype = None
     lib.specmc_result_free.argtypes = [C.POINTER(SmcResultC)]
     lib.specmc_result_free.restype = None
+    lib.specmc_free.argtypes = [C.c_void_p]
+    lib.specmc_free.restype = None
     lib.specmc_energy_batch.argtypes = [C.POINTER(ModelDesc), _dp, _dp, C.c_int64, _dp, C.c_int64, C.c_int32, _dp,
                                         E, Z]
     lib.specmc_ess.argtypes = [_dp, C.c_int64, C.c_int32, _dp, E, Z]

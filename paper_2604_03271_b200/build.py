@@ -20,7 +20,7 @@ SOURCES = sorted(CSRC.glob("*.cu"))
 HEADERS = [CSRC / "device.cuh", CSRC / "chain.cuh", CSRC / "launch.h", ROOT / "include" / "specmc_b200.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--use_fast_math", "--split-compile=4",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--use_fast_math",
          "-Xptxas", "-warn-spills", f"-I{ROOT / 'include'}"]
 
 

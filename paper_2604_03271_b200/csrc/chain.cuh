@@ -117,13 +117,18 @@ template <int PPL, int W>
 struct Smem {
   static constexpr int L = 32 * W;
   static constexpr int NPT = PPL * L;
+  // lay: spectrum layout flags (launch.h); W <= 2 always uses kLayFull
+  __host__ __device__ static constexpr int layout(int lay) { return chain_dyn_layout(W) ? lay : kLayFull; }
   static constexpr size_t off_x = 16;
   static constexpr size_t off_c = off_x + (size_t)NPT * 4;
-  static constexpr size_t off_y = off_c + (size_t)NPT * 8;
-  static constexpr size_t off_w = off_y + (size_t)NPT * 8;
+  __host__ __device__ static constexpr size_t off_y(int lay) {
+    return off_c + ((layout(lay) & kLayWeights) ? (size_t)NPT * 8 : 0);
+  }
+  __host__ __device__ static constexpr size_t y_bytes(int lay) { return (layout(lay) & kLayY4) ? 4 : 8; }
+  __host__ __device__ static constexpr size_t off_w(int lay) { return off_y(lay) + (size_t)NPT * y_bytes(lay); }
   __host__ __device__ static size_t per_unit(int dpad) { return (size_t)dpad * (8 + 8 + 4 + 8 + 8 + 4 + 4 + 4 + 4); }
-  __host__ __device__ static size_t bytes(int U, int dpad) {
-    size_t b = off_w + (size_t)U * per_unit(dpad);
+  __host__ __device__ static size_t bytes(int U, int dpad, int lay) {
+    size_t b = off_w(lay) + (size_t)U * per_unit(dpad);
     b = (b + 15) & ~(size_t)15;
     return b + (size_t)U * sizeof(Xch) + (size_t)U * NPT * (p_in_smem<W>() ? 8 : 4);  // + caches Q (and P)
   }
@@ -819,6 +824,13 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
     k_chain(const GroupDesc* __restrict__ gds, const int* __restrict__ list, const int* __restrict__ cta_prefix,
             int n_list, int U, int dpad) {
   using SM = Smem<PPL, W>;
+  // W >= 4: the launch's spectrum layout rides in the high half of dpad
+  // (W <= 2 kernels keep their parameter list and compile-time layout)
+  int lay = kLayFull;
+  if (chain_dyn_layout(W)) {
+    lay = dpad >> 16;
+    dpad &= 0xffff;
+  }
   extern __shared__ __align__(16) unsigned char smem[];
   const int gi = find_group(cta_prefix, n_list, blockIdx.x);
   const GroupDesc& g = gds[list[gi]];
@@ -827,10 +839,10 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   float* sx = reinterpret_cast<float*>(smem + SM::off_x);
   float2* sc = reinterpret_cast<float2*>(smem + SM::off_c);
-  float2* sy = reinterpret_cast<float2*>(smem + SM::off_y);
+  float2* sy = reinterpret_cast<float2*>(smem + SM::off_y(lay));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int unit = warp / W, wiu = warp - unit * W;
-  unsigned char* wb = smem + SM::off_w + (size_t)unit * SM::per_unit(dpad);
+  unsigned char* wb = smem + SM::off_w(lay) + (size_t)unit * SM::per_unit(dpad);
   double* th = reinterpret_cast<double*>(wb);
   double* lsv = th + dpad;
   int* acc = reinterpret_cast<int*>(lsv + dpad);
@@ -840,7 +852,7 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   int* flg = reinterpret_cast<int*>(lub + dpad);
   float* thf = reinterpret_cast<float*>(flg + dpad);  // fp32 shadow of th (block constants)
   float* nvf = thf + dpad;                            // fp32 shadow of the proposals
-  const size_t xoff = ((SM::off_w + (size_t)U * SM::per_unit(dpad)) + 15) & ~(size_t)15;
+  const size_t xoff = ((SM::off_w(lay) + (size_t)U * SM::per_unit(dpad)) + 15) & ~(size_t)15;
   Xch* xcs = reinterpret_cast<Xch*>(smem + xoff);
   float* gcache = reinterpret_cast<float*>(smem + xoff + (size_t)U * sizeof(Xch));
   float* pcache = gcache + (size_t)U * SM::NPT;
@@ -848,8 +860,9 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   // ---- stage the spectrum: cp.async.bulk (UBLKCP) completing on an mbarrier
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
-    constexpr uint32_t bx = SM::NPT * 4u, bc = SM::NPT * 8u, by = SM::NPT * 8u;
-    const bool wc = FAM == FAM_XPS && !g.sh_uniform;  // trapezoid weights (non-uniform grids only)
+    const uint32_t bx = SM::NPT * 4u, bc = SM::NPT * 8u, by = SM::NPT * (uint32_t)SM::y_bytes(lay);
+    // trapezoid weights: non-uniform grids only (the launch layout stages them then)
+    const bool wc = FAM == FAM_XPS && !g.sh_uniform && (SM::layout(lay) & kLayWeights);
     mbar_expect_tx(bar, bx + (wc ? bc : 0u) + by);
     bulk_g2s(sx, g.spec_x, bx, bar);
     if (wc) bulk_g2s(sc, g.spec_c, bc, bar);
@@ -903,17 +916,18 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
 
 // ------------------------------------------------------------------ launch
 template <int FAM, int PPL, int W, bool ENERGY, int NZ>
-cudaError_t launch_chain_t(int U, int dmax, const GroupDesc* gds, const int* list, const int* prefix, int n_list,
-                           int total_ctas, cudaStream_t st) {
+cudaError_t launch_chain_t(int U, int lay, int dmax, const GroupDesc* gds, const int* list, const int* prefix,
+                           int n_list, int total_ctas, cudaStream_t st) {
   const int dpad = (dmax + 1) & ~1;
-  const size_t smem = Smem<PPL, W>::bytes(U, dpad);
+  const size_t smem = Smem<PPL, W>::bytes(U, dpad, lay);
   auto kern = k_chain<FAM, PPL, W, ENERGY, NZ>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   if (total_ctas <= 0) return cudaSuccess;  // prime only (module load + attributes, see prime_level_kernels)
-  kern<<<total_ctas, Bounds<W, PPL>::threads, smem, st>>>(gds, list, prefix, n_list, U, dpad);
+  const int dpad_lay = chain_dyn_layout(W) ? (dpad | (lay << 16)) : dpad;
+  kern<<<total_ctas, Bounds<W, PPL>::threads, smem, st>>>(gds, list, prefix, n_list, U, dpad_lay);
   return cudaGetLastError();
 }
 
@@ -928,7 +942,7 @@ template <int FAM, bool ENERGY, int NZ>
 cudaError_t launch_chain_fam(const Shape& s, int dmax, const GroupDesc* gds, const int* list, const int* prefix,
                              int n_list, int total_ctas, cudaStream_t st) {
 #define SMC_CASE(WW, PP) \
-  if (s.W == WW && s.PPL == PP) return launch_chain_t<FAM, PP, WW, ENERGY, NZ>(s.U, dmax, gds, list, prefix, n_list, total_ctas, st);
+  if (s.W == WW && s.PPL == PP) return launch_chain_t<FAM, PP, WW, ENERGY, NZ>(s.U, s.lay, dmax, gds, list, prefix, n_list, total_ctas, st);
   SMC_FOR_EACH_SHAPE(SMC_CASE)
 #undef SMC_CASE
   return cudaErrorInvalidValue;

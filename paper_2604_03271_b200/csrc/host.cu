@@ -25,6 +25,7 @@
 #include <numeric>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -254,6 +255,68 @@ ArenaCache& arena_cache() {
   return *c;
 }
 
+// Process-wide cache of pinned host staging buffers (results of run_batch are
+// copied D2H into pinned memory while the remaining runs still step; pinning
+// 100+ MB costs tens of ms, so buffers are kept for later calls).
+struct PinnedCache {
+  static constexpr size_t kMaxCached = size_t(4) << 30;
+  std::mutex mu;
+  std::multimap<size_t, void*> free_;
+  size_t cached = 0;
+  void* get(size_t b, size_t& got) {
+    b = std::max<size_t>(b, size_t(64) << 10);  // small buffers share a 64 KB size class
+    const size_t cap = b <= (size_t(64) << 10) ? b : 2 * b + (size_t(64) << 20);
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = free_.lower_bound(b);
+      if (it != free_.end() && it->first <= cap) {
+        void* p = it->second;
+        got = it->first;
+        cached -= it->first;
+        free_.erase(it);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    cuda_check(cudaHostAlloc(&p, b, cudaHostAllocPortable), "cudaHostAlloc");
+    got = b;
+    return p;
+  }
+  void put(void* p, size_t b) {
+    std::lock_guard<std::mutex> lk(mu);
+    free_.emplace(b, p);
+    cached += b;
+    while (cached > kMaxCached && !free_.empty()) {
+      auto it = free_.begin();
+      cudaFreeHost(it->second);
+      cached -= it->first;
+      free_.erase(it);
+    }
+  }
+};
+PinnedCache& pinned_cache() {
+  static PinnedCache* c = new PinnedCache();
+  return *c;
+}
+
+// copy of a large block on up to 4 host threads (fresh result arrays fault
+// their pages in; one thread does ~5 GB/s)
+void par_memcpy(void* dst, const void* src, size_t n) {
+  constexpr size_t kChunk = size_t(8) << 20;
+  const int nt = (int)std::min<size_t>(4, (n + kChunk - 1) / kChunk);
+  if (nt <= 1) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t per = (n + nt - 1) / nt;
+  for (int t = 0; t < nt; ++t) {
+    const size_t a = std::min(n, per * t), b = std::min(n, per * (t + 1));
+    th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a); });
+  }
+  for (auto& x : th) x.join();
+}
+
 // Row pitch (elements) of the [d][n] device arrays: a multiple of 32 doubles
 // with pitch / 32 odd (GroupDesc::tp, device.cuh)
 inline size_t row_pitch(size_t n) {
@@ -280,10 +343,16 @@ struct Arena {
   Arena(const Arena&) = delete;
   ~Arena() {
     if (!p) return;
+    static const bool trace = std::getenv("SPECMC_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     if (cudaStreamSynchronize(st) == cudaSuccess)
       arena_cache().put(dev, p, bytes);
     else
       cudaFree(p);  // the context is in an error state: do not recycle
+    if (trace)
+      std::fprintf(stderr, "[specmc]   ~Arena %.1f MB %.4f s (cached %.1f MB)\n", bytes / 1e6,
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(),
+                   arena_cache().cached / 1e6);
   }
   template <typename T>
   T* take(size_t count) {
@@ -437,6 +506,17 @@ PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, 
   return ps;
 }
 
+// shared-memory spectrum layout of a class (launch.h kLay*): the trapezoid
+// weights only when an xps spectrum of the class is on a non-uniform grid, y
+// at 4 B/point for the paired noise models
+template <class M>
+int spectrum_layout(int family, int noise, const M& prep) {
+  bool weights = false;
+  for (const auto& kv : prep) weights = weights || (family == SPECMC_FAMILY_XPS && !kv.second.uniform);
+  const bool paired = noise == NZ_HETERO || noise == NZ_HLIN || noise == NZ_HPROP;
+  return (weights ? kLayWeights : 0) | (paired ? kLayY4 : 0);
+}
+
 double pick_shift(const specmc_model_desc& m, const double* xs, int64_t N) {
   if (m.family != SPECMC_FAMILY_GM && m.family != SPECMC_FAMILY_XPS) return 0.0;
   for (int i = 0; i < m.d; ++i)
@@ -533,13 +613,123 @@ struct ClassRun {
   std::vector<int> order;
   GroupState* h_st = nullptr;
   int* h_list = nullptr;
+  size_t h_st_bytes = 0, h_list_bytes = 0;
   double device_seconds = 0.0;
+  // early staging (run_batch): as soon as a run reaches beta = 1 its posterior,
+  // energies and diagnostics go D2H into pinned memory on a copy stream while
+  // the other runs of the class still step; fetch() then only copies host-side
+  bool stage_early = false;
+  cudaStream_t cst = nullptr;
+  cudaEvent_t cev = nullptr;
+  double* stage = nullptr;
+  size_t stage_bytes = 0;
+  std::vector<size_t> stage_off;  // per group: [diag (4 max_levels) | posterior (d T) | energies (T)]
+  std::vector<char> staged;       // 1: copy enqueued, 2: copied into hres
+  std::vector<cudaEvent_t> gev;   // per group: its staging copy is done
+  struct HostRes {
+    double* post = nullptr;
+    double* ener = nullptr;
+    std::vector<double> diag;
+  };
+  std::vector<HostRes> hres;  // results copied out of the staging buffer (owned until fetch)
 
   ClassRun() = default;
   ClassRun(const ClassRun&) = delete;
   ~ClassRun() {
-    if (h_st) cudaFreeHost(h_st);
-    if (h_list) cudaFreeHost(h_list);
+    static const bool trace = std::getenv("SPECMC_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto tick = [&](const char* what) {
+      if (trace)
+        std::fprintf(stderr, "[specmc]   ~ClassRun %s %.4f s\n", what,
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    };
+    if (cst) {
+      const bool ok = cudaStreamSynchronize(cst) == cudaSuccess;
+      tick("sync");
+      if (stage) {
+        if (ok)
+          pinned_cache().put(stage, stage_bytes);
+        else
+          cudaFreeHost(stage);
+      }
+      tick("pinned");
+      cudaStreamDestroy(cst);
+      tick("stream");
+    }
+    if (cev) cudaEventDestroy(cev);
+    for (cudaEvent_t e : gev) cudaEventDestroy(e);
+    for (auto& r : hres) {
+      std::free(r.post);
+      std::free(r.ener);
+    }
+    if (h_st) pinned_cache().put(h_st, h_st_bytes);
+    if (h_list) pinned_cache().put(h_list, h_list_bytes);
+    tick("host");
+  }
+
+  void init_staging() {
+    if (!stage_early || xch || init_only) {
+      stage_early = false;
+      return;
+    }
+    stage_off.assign(G + 1, 0);
+    for (int gi = 0; gi < G; ++gi) {
+      const size_t T = (size_t)runs_T0[gi], d = (size_t)gds[gi].d;
+      stage_off[gi + 1] = stage_off[gi] + 4 * (size_t)gds[gi].max_levels + d * T + T;
+    }
+    stage = static_cast<double*>(pinned_cache().get(stage_off[G] * sizeof(double), stage_bytes));
+    staged.assign(G, 0);
+    cuda_check(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaEventCreateWithFlags(&cev, cudaEventDisableTiming), "cudaEventCreate");
+    gev.assign(G, nullptr);
+    for (auto& e : gev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    hres.resize(G);
+  }
+
+  // host side of the staging: copy finished runs out of pinned memory into
+  // their result arrays -- between level launches (wait = false: only copies
+  // that are complete; the host would otherwise idle in the level sync) and in
+  // fetch (wait = true)
+  void drain(bool wait) {
+    for (int gi = 0; gi < G; ++gi) {
+      if (staged[gi] != 1) continue;
+      const GroupState& s = h_st[gi];
+      if (s.error != GE_NONE) {
+        staged[gi] = 2;
+        continue;
+      }
+      if (wait)
+        cuda_check(cudaEventSynchronize(gev[gi]), "cudaEventSynchronize");
+      else if (cudaEventQuery(gev[gi]) != cudaSuccess)
+        continue;
+      const size_t T = (size_t)s.T_loc, d = (size_t)gds[gi].d, L4 = 4 * (size_t)gds[gi].max_levels;
+      const double* h = stage + stage_off[gi];
+      HostRes& r = hres[gi];
+      r.diag.assign(h, h + (size_t)s.level * 4);
+      r.post = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(d * T, 1)));
+      par_memcpy(r.post, h + L4, d * T * sizeof(double));
+      r.ener = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(T, 1)));
+      std::memcpy(r.ener, h + L4 + d * T, T * sizeof(double));
+      staged[gi] = 2;
+    }
+  }
+
+  // enqueue the result copy of a run that just finished (h_st is current)
+  void stage_group(int gi, cudaStream_t st) {
+    const GroupState& s = h_st[gi];
+    staged[gi] = 1;
+    if (s.error != GE_NONE) return;
+    const size_t T = (size_t)s.T_loc, d = (size_t)gds[gi].d;
+    double* h = stage + stage_off[gi];
+    cuda_check(cudaEventRecord(cev, st), "event");
+    cuda_check(cudaStreamWaitEvent(cst, cev, 0), "cudaStreamWaitEvent");
+    double* pout = gds[gi].theta[s.cur ^ 1];  // idle once the run is done
+    cuda_check(launch_posterior_out(gds[gi].theta[s.cur], gds[gi].tp, (int)d, (int)T, out_shift[gi], pout, cst),
+               "k_posterior_out");
+    d2h(h, gds[gi].diag, (size_t)s.level * 4, cst);
+    d2h(h + 4 * (size_t)gds[gi].max_levels, pout, d * T, cst);
+    d2h(h + 4 * (size_t)gds[gi].max_levels + d * T, gds[gi].E[s.cur], T, cst);
+    cuda_check(cudaEventRecord(gev[gi], cst), "event");
   }
 
   // allocation + H2D of spectra, priors and descriptors
@@ -571,6 +761,7 @@ struct ClassRun {
         prep.emplace(key, prepare_spectrum(runs[r].m, sp.xs, sp.ys, sp.n, shape, runs[r].x_shift));
       }
     }
+    shape.lay = spectrum_layout(family, noise, prep);
     const size_t npt = (size_t)shape.PPL * 32 * shape.W;
     size_t bytes = Arena::al(sizeof(GroupDesc) * G) + Arena::al(sizeof(GroupState) * G) + 7 * Arena::al(4 * (G + 1));
     bytes += prep.size() * (Arena::al(npt * 4) + 2 * Arena::al(npt * 8));
@@ -719,8 +910,11 @@ struct ClassRun {
     order.resize(G);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return gds[a].d > gds[b].d; });
-    cuda_check(cudaMallocHost(&h_st, sizeof(GroupState) * G), "cudaMallocHost");
-    cuda_check(cudaMallocHost(&h_list, sizeof(int) * 4 * (G + 1)), "cudaMallocHost");
+    // pinned host mirrors from the process cache (cudaMallocHost/cudaFreeHost
+    // per call measured up to 0.1 s / 0.7 s)
+    h_st = static_cast<GroupState*>(pinned_cache().get(sizeof(GroupState) * G, h_st_bytes));
+    h_list = static_cast<int*>(pinned_cache().get(sizeof(int) * 4 * (G + 1), h_list_bytes));
+    init_staging();
     dev.sync();
   }
 
@@ -741,6 +935,7 @@ struct ClassRun {
   // init_ensemble + the level loop of smc_run (smc.cpp:186-211), all groups in lock-step
   void run(Device& dev) {
     cudaStream_t st = dev.stream;
+    if (stage_early) staged.assign(G, 0);
     std::vector<GroupState> sts(G);
     for (int gi = 0; gi < G; ++gi) {
       GroupState& s = sts[gi];
@@ -830,13 +1025,18 @@ struct ClassRun {
       cuda_check(cudaEventRecord(mv.b, st), "event");
       cuda_check(launch_stats_grid(d_gds, d_list, na, dmax, st), "k_stats_grid");
       count_launch(3);
+      if (stage_early) drain(false);  // host copies of finished runs while this level runs
       d2h(h_st, d_st, G, st);
       dev.sync();
       move_ms += mv.ms();
       ++move_launches;
       std::vector<int> next;
-      for (int gi : active)
-        if (h_st[gi].active) next.push_back(gi);
+      for (int gi : active) {
+        if (h_st[gi].active)
+          next.push_back(gi);
+        else if (stage_early)
+          stage_group(gi, st);
+      }
       active.swap(next);
     }
     cuda_check(cudaEventRecord(whole.b, st), "event");
@@ -853,6 +1053,7 @@ struct ClassRun {
   // D2H of diagnostics, posterior and energies (report fields of smc.cpp:221-247)
   void fetch(Device& dev, const std::vector<RunSpec>& runs, specmc_smc_result* out) {
     cudaStream_t st = dev.stream;
+    bool synced = false;
     for (int gi = 0; gi < G; ++gi) {
       const RunSpec& R = runs[idx[gi]];
       specmc_smc_result& o = out[idx[gi]];
@@ -873,16 +1074,28 @@ struct ClassRun {
       o.diverged = !std::isfinite(o.F);
       const int Lv = s.level;
       std::vector<double> diag((size_t)Lv * 4);
-      d2h(diag.data(), gds[gi].diag, diag.size(), st);
-      // posterior: transposed to [T][d] on the device into the idle theta buffer, one D2H
-      double* pout = gds[gi].theta[s.cur ^ 1];
-      cuda_check(launch_posterior_out(gds[gi].theta[s.cur], gds[gi].tp, (int)d, (int)T, out_shift[gi], pout, st),
-                 "k_posterior_out");
-      o.posterior = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(d * T, 1)));
-      d2h(o.posterior, pout, d * T, st);
-      o.energies = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(T, 1)));
-      d2h(o.energies, gds[gi].E[s.cur], T, st);
-      dev.sync();
+      if (stage_early && staged[gi]) {  // copied out during the run (or now): hand the arrays over
+        if (!synced) {
+          drain(true);
+          synced = true;
+        }
+        HostRes& r = hres[gi];
+        diag = r.diag;
+        o.posterior = r.post;
+        o.energies = r.ener;
+        r.post = r.ener = nullptr;
+      } else {
+        d2h(diag.data(), gds[gi].diag, diag.size(), st);
+        // posterior: transposed to [T][d] on the device into the idle theta buffer, one D2H
+        double* pout = gds[gi].theta[s.cur ^ 1];
+        cuda_check(launch_posterior_out(gds[gi].theta[s.cur], gds[gi].tp, (int)d, (int)T, out_shift[gi], pout, st),
+                   "k_posterior_out");
+        o.posterior = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(d * T, 1)));
+        d2h(o.posterior, pout, d * T, st);
+        o.energies = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(T, 1)));
+        d2h(o.energies, gds[gi].E[s.cur], T, st);
+        dev.sync();
+      }
       o.ladder = static_cast<double*>(std::malloc(sizeof(double) * (Lv + 1)));
       o.level_ess_ratio = static_cast<double*>(std::malloc(sizeof(double) * std::max(Lv, 1)));
       o.level_log_mean_w = static_cast<double*>(std::malloc(sizeof(double) * std::max(Lv, 1)));
@@ -955,7 +1168,8 @@ struct Session {
   std::vector<std::unique_ptr<ClassRun>> classes;
   double device_seconds = 0.0;
 
-  Session(int n_problems, const specmc_problem* problems, int n_spectra, const specmc_spectrum* sps) {
+  Session(int n_problems, const specmc_problem* problems, int n_spectra, const specmc_spectrum* sps,
+          bool stage_early = false) {
     if (n_problems < 1 || !problems) throw Error(SPECMC_EINVAL, "batch: no problems");
     if (n_spectra < 1 || !sps) throw Error(SPECMC_EINVAL, "batch: no spectra");
     spectra.assign(sps, sps + n_spectra);
@@ -977,6 +1191,7 @@ struct Session {
     for (auto& kv : cls) {
       classes.push_back(std::make_unique<ClassRun>());
       classes.back()->idx = kv.second;
+      classes.back()->stage_early = stage_early;
       classes.back()->prepare(*dev, runs, spectra);
     }
     spectra.clear();  // host inputs are borrowed only for the call
@@ -1008,10 +1223,24 @@ int run_batch(int n_problems, const specmc_problem* problems, int n_spectra, con
               specmc_smc_result* out, char* err, size_t errlen) {
   const auto t0 = std::chrono::steady_clock::now();
   if (!out) throw Error(SPECMC_EINVAL, "batch: null results");
-  Session s(n_problems, problems, n_spectra, spectra);
-  s.run();
-  const int first = s.fetch(out);
-  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  static const bool trace = std::getenv("SPECMC_TRACE") != nullptr;  // phase timings on stderr
+  auto since = [&](std::chrono::steady_clock::time_point a) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
+  };
+  int first;
+  double t_create, t_run, t_fetch;
+  {
+    Session s(n_problems, problems, n_spectra, spectra, /*stage_early=*/true);
+    t_create = since(t0);
+    s.run();
+    t_run = since(t0);
+    first = s.fetch(out);
+    t_fetch = since(t0);
+  }
+  const double wall = since(t0);
+  if (trace)
+    std::fprintf(stderr, "[specmc] run_batch create %.4f run %.4f fetch %.4f destroy %.4f s\n", t_create,
+                 t_run - t_create, t_fetch - t_run, wall - t_fetch);
   for (int i = 0; i < n_problems; ++i) out[i].wall_seconds = wall;
   if (first != SPECMC_OK)
     copy_err(err, errlen, "smc: max_levels exceeded before reaching beta = 1 (or total weight is zero)");
@@ -1381,6 +1610,8 @@ void specmc_comm_destroy(specmc_comm* c) {
   delete p;
 }
 
+void specmc_free(void* p) { std::free(p); }
+
 void specmc_result_free(specmc_smc_result* r) {
   if (!r) return;
   std::free(r->ladder);
@@ -1420,10 +1651,11 @@ int specmc_energy_batch(const specmc_model_desc* model, const double* xs, const 
     specmc_spectrum sp{xs, ys, n_points};
     RunSpec R = make_runspec(*model, 0, cfg, sp);
     Device dev(device);
-    const Shape shape = pick_shape(n_points, model->d);
+    Shape shape = pick_shape(n_points, model->d);
     if ((int64_t)32 * shape.W * shape.PPL < n_points)
       throw Error(SPECMC_EINVAL, "spectrum has more points than the device path supports (8192)");
     const PreparedSpectrum ps = prepare_spectrum(*model, xs, ys, n_points, shape, R.x_shift);
+    shape.lay = spectrum_layout(model->family, ps.nz, std::map<int, PreparedSpectrum>{{0, ps}});
     const int d = model->d;
     const int64_t T = n_thetas;
     Scratch sc;

@@ -931,7 +931,9 @@ Shape pick_shape(int64_t N, int dmax) {
 size_t chain_smem_bytes(const Shape& s, int dmax) {  // must match Smem<PPL, W>::bytes (chain.cuh)
   const int dpad = (dmax + 1) & ~1;
   const size_t npt = (size_t)s.PPL * 32 * s.W;
-  size_t b = 16 + npt * (4 + 8 + 8) + (size_t)s.U * dpad * (8 + 8 + 4 + 8 + 8 + 4 + 4 + 4 + 4);
+  const int lay = chain_dyn_layout(s.W) ? s.lay : kLayFull;
+  const size_t spec = 4 + ((lay & kLayWeights) ? 8 : 0) + ((lay & kLayY4) ? 4 : 8);  // bytes per point
+  size_t b = 16 + npt * spec + (size_t)s.U * dpad * (8 + 8 + 4 + 8 + 8 + 4 + 4 + 4 + 4);
   b = (b + 15) & ~(size_t)15;
   return b + (size_t)s.U * sizeof(Xch) + (size_t)s.U * npt * (chain_p_in_smem(s.W) ? 8 : 4);  // Q (and P)
 }

@@ -10,10 +10,20 @@ namespace smc {
 // Launch shape of the chain-parallel kernels for a spectrum of N points:
 // W warps cooperate on one chain (unit), each lane owns PPL consecutive
 // points in registers, U units share one CTA (and its staged spectrum).
+// Spectrum layout in the chain kernels' shared memory (bit flags): bit 0 = the
+// trapezoid weights are staged (xps on a non-uniform grid), bit 1 = y at 4 B
+// per point (paired noise models).  W <= 2 kernels use the fixed full layout
+// (weights + 8 B y: 20 B/point, compile-time offsets); W >= 4 kernels size
+// it per launch, which halves the footprint of the large spectra (C3, C5) and
+// lets two CTAs share an SM.
+constexpr int kLayWeights = 1, kLayY4 = 2, kLayFull = kLayWeights;
+__host__ __device__ constexpr bool chain_dyn_layout(int W) { return W >= 4; }
+
 struct Shape {
   int W;
   int PPL;
   int U;
+  int lay = kLayFull;
 };
 
 // chain-kernel CTA size per unit width W (units per CTA = threads / 32 W):

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import weakref
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -109,7 +110,14 @@ def _report(spec: ModelSpec, cfg: SmcConfig, n_data: int, r: _lib.SmcResultC) ->
         "level_acc_rate": np.ctypeslib.as_array(r.level_acc_rate, (max(L, 1),))[:L].copy(),
     }
     d, T = r.d, r.T
-    rep.posterior = np.ctypeslib.as_array(r.posterior, (T, d)).copy().T  # d x T view of the particle-major block
+    # the particle-major block is handed over without a copy: the array owns the
+    # malloc'd buffer (freed with specmc_free when the last view goes), and the
+    # result's field is cleared so specmc_result_free leaves it alone
+    ptr = C.cast(r.posterior, C.c_void_p).value
+    block = np.ctypeslib.as_array(r.posterior, (T, d))
+    weakref.finalize(block, lib.specmc_free, ptr)
+    r.posterior = None
+    rep.posterior = block.T  # d x T view
     rep.energies = np.ctypeslib.as_array(r.energies, (T,)).copy()
     return rep
 
