@@ -85,8 +85,8 @@ __device__ __forceinline__ float shape(const BlockC& b, float x) {
     return b.c1 * ex2f(b.c2 * (d * d));
   } else if (FAM == FAM_XPS) {
     const float t = fmaf(x, b.c3, b.mu);
-    const float u = t * t;
-    return fmaf(b.c1, ex2f(-u), rcpf(fmaf(u, b.c2, b.c2)));
+    const float nu = t * -t;  // -u: the negation rides on the FMUL (MUFU.EX2 takes no negate)
+    return fmaf(b.c1, ex2f(nu), rcpf(fmaf(nu, -b.c2, b.c2)));
   } else {
     return b.c1;
   }
@@ -229,7 +229,7 @@ __device__ __forceinline__ bool add_block(const GroupDesc& g, int b, const float
           const bool pos = dx >= 0.f;
           const float tg = dx * (pos ? ig_hi : ig_lo);
           const float tl = dx * (pos ? il_hi : il_lo);
-          acc[k] += fmaf(ag, ex2f(-(tg * tg)), al * rcpf(fmaf(tl, tl, 1.f)));
+          acc[k] += fmaf(ag, ex2f(tg * -tg), al * rcpf(fmaf(tl, tl, 1.f)));
         }
       }
       return true;
@@ -240,7 +240,7 @@ __device__ __forceinline__ bool add_block(const GroupDesc& g, int b, const float
 #pragma unroll
     for (int k = 0; k < PPL; ++k) {
       const float t = u.x(k) * is;
-      acc[k] += fmaf(ag, ex2f(-(t * t)), fmaf(al, rcpf(fmaf(t, t, 1.f)), off));
+      acc[k] += fmaf(ag, ex2f(t * -t), fmaf(al, rcpf(fmaf(t, t, 1.f)), off));
     }
     return true;
   } else {

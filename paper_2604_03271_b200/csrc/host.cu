@@ -8,7 +8,7 @@
 //   smc_run (level loop)       proj/src/smc.cpp:186-211, report fields :218-249
 // The level loop runs every group (one SMC run = one (spectrum, K, seed)) of
 // a batch in lock-step: per round the tempering (k_temper, one CTA per group,
-// or the k_tp_* grid phases for T > 2^17), one k_chain move launch covering
+// or the k_tp_* grid phases for T > 2^15), one k_chain move launch covering
 // every chain of every active group (longest d first), and k_stats_grid +
 // k_stats_final.  The host reads back the small GroupState of every group per
 // round to retire groups that reached beta = 1.  Particle-sharded runs
@@ -146,7 +146,23 @@ void validate_spectrum(const double* xs, const double* ys, int64_t n, bool nonne
 
 // location parameters (peak centres mu_k) are shifted by x_shift on the device
 // populations above this use the grid-level (multi-CTA) tempering kernels
-constexpr size_t kGridTemperT = (size_t)1 << 17;
+// grid-level tempering above 2^15 particles, slices of >= 4096: at T = 65536 (C2)
+// 16 CTAs per run instead of one cut the level's tempering time (C2 step
+// 1.512 -> 1.490 s); small populations keep the single-CTA kernel
+constexpr size_t kGridTemperT = (size_t)1 << 15;
+constexpr size_t kMinSliceLen = 4096;
+// tuning overrides (experiments): SPECMC_GRID_T = population above which the
+// tempering runs grid-level, SPECMC_SLICE = minimum slice length
+size_t grid_temper_t() {
+  static const size_t v = std::getenv("SPECMC_GRID_T") ? std::strtoull(std::getenv("SPECMC_GRID_T"), nullptr, 10)
+                                                        : kGridTemperT;
+  return v;
+}
+size_t min_slice_len() {
+  static const size_t v =
+      std::getenv("SPECMC_SLICE") ? std::strtoull(std::getenv("SPECMC_SLICE"), nullptr, 10) : kMinSliceLen;
+  return v;
+}
 
 bool is_location(int family, int K, int i) {
   if (family == SPECMC_FAMILY_GM) return i % 3 == 1;
@@ -777,7 +793,7 @@ struct ClassRun {
       bytes += Arena::al(2 * d * 8) + Arena::al(d * 8);                         // stat_acc, out_shift
       bytes += Arena::al(2 * 8) + Arena::al(2 * 8 * (size_t)R.nshards);        // xbuf, xgat
       bytes += Arena::al(R.refl.size() * 4 + 8) + Arena::al(R.refl_off.size() * 4 + 4);  // xrd reflections
-      if (T > kGridTemperT || xch) bytes += Arena::al(sizeof(TemperScratch));  // grid tempering
+      if (T > grid_temper_t() || xch) bytes += Arena::al(sizeof(TemperScratch));  // grid tempering
     }
     ar.reserve(bytes, dev.ordinal, dev.stream);
     d_gds = ar.take<GroupDesc>(G);
@@ -895,9 +911,9 @@ struct ClassRun {
         g.refl = rf;
         g.refl_off = ro;
       }
-      if (T > kGridTemperT || xch) {  // grid-level tempering: slices of <= 512 x slice_len particles
+      if (T > grid_temper_t() || xch) {  // grid-level tempering: slices of <= 512 x slice_len particles
         g.ts = ar.take<TemperScratch>(1);
-        size_t sl = std::max<size_t>(32768, (T + kMaxSlices - 1) / kMaxSlices);
+        size_t sl = std::max<size_t>(min_slice_len(), (T + kMaxSlices - 1) / kMaxSlices);
         sl = (sl + 1023) & ~(size_t)1023;
         g.slice_len = (int)sl;
         g.nslices = (int)((T + sl - 1) / sl);

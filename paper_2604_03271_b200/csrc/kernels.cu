@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(kTemperThreads) k_temper(const GroupDesc* __re
 }
 
 // =================================================================
-// Grid-level tempering for large populations (T > 2^17): the same
+// Grid-level tempering for large populations (T > 2^15): the same
 // operations as k_temper, with the T-element reductions and the CDF scan
 // spread over slices of the particle array (one CTA per slice).  A
 // "last block" of each launch combines the slice partials in slice order

@@ -2,7 +2,7 @@
 one device and exchange through kernels; the NCCL path uses the same phases.
 
 Tolerances:
-  * one shard == the unsharded grid-tempering path (T > 2^17): bitwise.
+  * one shard == the unsharded grid-tempering path (T > 2^15): bitwise.
   * G shards vs the conjugate closed form: |F - F_exact| < 0.05 at T = 2^15
     (the reference's own tolerance is 0.15 at T = 2000, test_smc.cpp:122-138).
   * G shards vs one shard on the xps family: |dF| < 1.0 (Monte-Carlo error of

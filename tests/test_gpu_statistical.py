@@ -149,7 +149,7 @@ def test_batch_equals_single_runs(smc):
 
 
 def test_grid_level_tempering_large_population(smc, port):
-    # T = 2^18 > 2^17 takes the multi-CTA tempering / grid CDF scan path (k_tp_*)
+    # T = 2^18 > 2^15 takes the multi-CTA tempering / grid CDF scan path (k_tp_*)
     spec, data, F_exact, mn, vn = conjugate(50, 101, port, truth=1.0, sigma=1.0, m0=0.0, v0=1.0)
     reps = smc.smc_run_batch([(spec, 0, smc.SmcConfig(T=1 << 18, n=8, seed=s)) for s in (1, 2)], [data])
     for r in reps:
@@ -165,8 +165,8 @@ def test_grid_and_block_tempering_agree(smc, port):
     # same model at T just below / above the grid threshold: F within statistical noise
     w = syn.config("C1")
     spec = w.spec(2)
-    small = smc.smc_run_batch([(spec, 0, smc.SmcConfig(T=1 << 17, n=8, seed=s)) for s in (1, 2, 3)], [w.data])
-    big = smc.smc_run_batch([(spec, 0, smc.SmcConfig(T=(1 << 17) + 1024, n=8, seed=s)) for s in (1, 2, 3)], [w.data])
+    small = smc.smc_run_batch([(spec, 0, smc.SmcConfig(T=1 << 15, n=8, seed=s)) for s in (1, 2, 3)], [w.data])
+    big = smc.smc_run_batch([(spec, 0, smc.SmcConfig(T=(1 << 15) + 1024, n=8, seed=s)) for s in (1, 2, 3)], [w.data])
     fs, fb = np.array([r.F for r in small]), np.array([r.F for r in big])
     assert abs(fs.mean() - fb.mean()) < 0.5, (fs, fb)
 
