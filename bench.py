@@ -127,6 +127,15 @@ def dist_init():
     return ws, rank, local
 
 
+# BASELINE.json config text per workload (synthetic data, see synthetic.config)
+WORKLOAD_TEXT = {
+    "C1": "synthetic XPS-like spectrum, 3 Gaussian peaks (flat background as a known offset)",
+    "C2": "synthetic XRD-like spectrum, 6 pseudo-Voigt peaks + Shirley",
+    "C3": "large-population single spectrum, 8 Lorentzian peaks (eta = 0) + Shirley",
+    "C5": "Kmax sweep stress test, 20 pseudo-Voigt peaks + Shirley",
+}
+
+
 def cpu_reference_sample(workload, seed, T):
     """Reference smc_run (oracle/_ref, unchanged reference sources) for K = 1..Kmax
     at T particles, workers = 0.  Returns (evals, seconds, cores, kind)."""
@@ -287,8 +296,8 @@ def run_ours(args, ws, rank, local):
         "ms_per_step": elapsed / args.steps * 1e3, "time_to_evidence_s": elapsed / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32 point terms / f64 accumulation", "data": "synthetic",
-        "config": {"workload": f"{args.config}: synthetic XRD-like spectrum N={N}, 6 pseudo-Voigt peaks + Shirley,"
-                               f" xps family K={ks[0]}..{ks[-1]}, T={w.T}, n={w.n}, ess 0.5; 1 trial per GPU",
+        "config": {"workload": f"{args.config}: {WORKLOAD_TEXT.get(args.config, 'synthetic spectrum')}, N={N},"
+                               f" {w.family} family K={ks[0]}..{ks[-1]}, T={w.T}, n={w.n}, ess 0.5; 1 trial per GPU",
                    "N": N, "K_range": [ks[0], ks[-1]], "T": w.T, "n": w.n, "trials_per_gpu": 1,
                    "l2": "flushed between steps (256 MiB write)", "parallelism": f"trials x{ws} (weak)"},
         "K_selected": k_sel, "trials_per_step": trials_step, "point_evals_per_s_move": pe_rate,
