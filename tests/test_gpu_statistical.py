@@ -304,3 +304,37 @@ def test_xrd_block_limit(smc):
     phases = [syn.TIO2_PHASES[0]] * 64  # 64 phases + the background block > 64
     with pytest.raises(ValueError):
         smc.smc_run(M.xrd_model(phases, xr), xr, smc.SmcConfig(T=256, n=8, seed=1))
+
+
+def test_staged_results_equal_session_fetch(smc):
+    # run_batch copies finished runs' results out while the others still step
+    # (pinned staging on a copy stream); a session fetch copies them at the end.
+    # Same seeds, same device code: identical posteriors, energies and ladders.
+    w = syn.config("C2", 2048)
+    probs = [(w.spec(k), 0, smc.SmcConfig(T=2048, n=8, seed=21)) for k in (1, 3, 5)]
+    staged = smc.smc_run_batch(probs, [w.data])
+    sess = smc.Session(probs, [w.data])
+    sess.run()
+    fetched = sess.fetch()
+    sess.close()
+    for a, b in zip(staged, fetched):
+        assert a.F == b.F
+        assert np.array_equal(a.posterior, b.posterior) and np.array_equal(a.energies, b.energies)
+        assert np.array_equal(a.arrays["ladder"], b.arrays["ladder"])
+        assert np.array_equal(a.arrays["level_acc_rate"], b.arrays["level_acc_rate"])
+
+
+def test_staged_batch_with_a_failing_run(smc):
+    # one run exceeds max_levels (runtime error), the others finish: the staging
+    # skips the failed run and the finished ones still come back complete
+    w = syn.config("C2", 2048)
+    probs = [(w.spec(2), 0, smc.SmcConfig(T=2048, n=8, seed=5)),
+             (w.spec(4), 0, smc.SmcConfig(T=2048, n=8, seed=5, max_levels=2)),
+             (w.spec(6), 0, smc.SmcConfig(T=2048, n=8, seed=5))]
+    out = smc.smc_run_batch(probs, [w.data], raise_on_error=False)
+    assert isinstance(out[1], RuntimeError)
+    for r, K in ((out[0], 2), (out[2], 6)):
+        assert np.isfinite(r.F) and r.posterior.shape == (4 * K + 2, 2048)
+        assert np.all(np.isfinite(r.posterior)) and r.arrays["ladder"][-1] == 1.0
+    alone = smc.smc_run_batch([probs[2]], [w.data])[0]
+    assert alone.F == out[2].F and np.array_equal(alone.posterior, out[2].posterior)
