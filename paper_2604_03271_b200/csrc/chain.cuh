@@ -110,8 +110,8 @@ struct Xch {  // per-unit cross-warp exchange, double-buffered by parity
 // committed peak signal P: shared memory for W = 2 and 4 (one trial signal in
 // registers leaves the allocator room: no spills at 128 registers), registers
 // for W = 1 and 8; see chain_p_in_smem (launch.h)
-template <int W>
-__host__ __device__ constexpr bool p_in_smem() { return chain_p_in_smem(W); }
+template <int W, int PPL>
+__host__ __device__ constexpr bool p_in_smem() { return chain_p_in_smem(W, PPL); }
 
 template <int PPL, int W>
 struct Smem {
@@ -130,7 +130,7 @@ struct Smem {
   __host__ __device__ static size_t bytes(int U, int dpad, int lay) {
     size_t b = off_w(lay) + (size_t)U * per_unit(dpad);
     b = (b + 15) & ~(size_t)15;
-    return b + (size_t)U * sizeof(Xch) + (size_t)U * NPT * (p_in_smem<W>() ? 8 : 4);  // + caches Q (and P)
+    return b + (size_t)U * sizeof(Xch) + (size_t)U * NPT * (p_in_smem<W, PPL>() ? 8 : 4);  // + caches Q (and P)
   }
 };
 
@@ -653,7 +653,7 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
   // Q[k] at Qs[k * L]: signal of every block except the one being swept (P - g_b)
   float* Qs = gcache + (size_t)unit * SM::NPT + u.lg;
   // committed peak signal: registers, or shared memory (Ps[k * L]) when p_in_smem<W>()
-  constexpr bool kPsm = p_in_smem<W>();
+  constexpr bool kPsm = p_in_smem<W, PPL>();
   float* Ps = pcache + (size_t)unit * SM::NPT + u.lg;
   constexpr int L = SM::L;
   if (kPsm) {
@@ -934,7 +934,7 @@ cudaError_t launch_chain_t(int U, int lay, int dmax, const GroupDesc* gds, const
 // (W, PPL) pairs compiled (see pick_shape in kernels.cu): W = 1 for N <= 512,
 // W = 2 for N <= 2048, W = 4 for N <= 4096, W = 8 for N <= 8192
 #define SMC_FOR_EACH_SHAPE(X)                                                                          \
-  X(1, 2) X(1, 4) X(1, 6) X(1, 8) X(1, 10) X(1, 12) X(1, 14) X(1, 16)                                 \
+  X(1, 2) X(1, 4) X(1, 6) X(1, 8) X(1, 10) X(1, 12) X(1, 14) X(1, 16) X(1, 20) X(1, 24) X(1, 28) X(1, 32) \
   X(2, 10) X(2, 12) X(2, 14) X(2, 16) X(2, 20) X(2, 24) X(2, 28) X(2, 32)                             \
   X(4, 20) X(4, 24) X(4, 28) X(4, 32) X(8, 20) X(8, 24) X(8, 28) X(8, 32)
 

@@ -899,6 +899,8 @@ Shape pick_shape(int64_t N, int dmax) {
   int nl;
   if (N <= 512) {
     s.W = 1, list = w1, nl = 8;
+  } else if (N <= 1024) {  // one warp per chain with wide lanes (no cross-warp exchange per evaluation)
+    s.W = 1, list = w48, nl = 4;
   } else if (N <= 2048) {
     s.W = 2, list = w2, nl = 8;
   } else if (N <= 4096) {
@@ -913,9 +915,9 @@ Shape pick_shape(int64_t N, int dmax) {
       break;
     }
   s.U = chain_threads(s.W) / (32 * s.W);
-  // W = 2 keeps 8 units' P and Q caches in shared memory: a large model that
+  // W = 2 (and wide-lane W = 1) keep 8 units' P and Q caches in shared memory: a large model that
   // does not fit takes the W = 4 shape (2 units per CTA) instead
-  if (s.W == 2 && chain_smem_bytes(s, dmax) > kChainSmemMax) {
+  if (s.W <= 2 && s.PPL >= 10 && chain_smem_bytes(s, dmax) > kChainSmemMax) {
     s.W = 4;
     s.PPL = w48[0];
     for (int i = 0; i < 4; ++i)
@@ -935,7 +937,7 @@ size_t chain_smem_bytes(const Shape& s, int dmax) {  // must match Smem<PPL, W>:
   const size_t spec = 4 + ((lay & kLayWeights) ? 8 : 0) + ((lay & kLayY4) ? 4 : 8);  // bytes per point
   size_t b = 16 + npt * spec + (size_t)s.U * dpad * (8 + 8 + 4 + 8 + 8 + 4 + 4 + 4 + 4);
   b = (b + 15) & ~(size_t)15;
-  return b + (size_t)s.U * sizeof(Xch) + (size_t)s.U * npt * (chain_p_in_smem(s.W) ? 8 : 4);  // Q (and P)
+  return b + (size_t)s.U * sizeof(Xch) + (size_t)s.U * npt * (chain_p_in_smem(s.W, s.PPL) ? 8 : 4);  // Q (and P)
 }
 
 cudaError_t launch_energy(int family, const Shape& s, int dmax, const GroupDesc* gds, const int* list,

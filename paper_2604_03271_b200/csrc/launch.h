@@ -30,7 +30,8 @@ struct Shape {
 // W = 2 runs 8 units per 512-thread CTA, one CTA per SM, so the spectrum is
 // staged once per SM and the 8 units' P and Q caches fit in shared memory
 __host__ __device__ constexpr int chain_threads(int W) { return W >= 8 ? 32 * W : (W == 2 ? 512 : 256); }
-__host__ __device__ constexpr bool chain_p_in_smem(int W) { return W == 2 || W == 4; }
+// (and W = 1 with wide lanes, PPL >= 20: 512 < N <= 1024)
+__host__ __device__ constexpr bool chain_p_in_smem(int W, int PPL) { return W == 2 || W == 4 || (W == 1 && PPL >= 20); }
 
 constexpr size_t kChainSmemMax = 227 * 1024;  // dynamic shared memory per CTA
 Shape pick_shape(int64_t N, int dmax);

@@ -74,7 +74,7 @@ def test_invalid_config_is_reported_before_touching_the_device():
 
 
 def test_launch_shapes_cover_the_configs():
-    for n, (W, P) in {301: (1, 10), 840: (2, 14), 2000: (2, 32), 4096: (4, 32), 8192: (8, 32), 50: (1, 2)}.items():
+    for n, (W, P) in {301: (1, 10), 840: (1, 28), 2000: (2, 32), 4096: (4, 32), 8192: (8, 32), 50: (1, 2)}.items():
         w, p, u = S.launch_shape(n)
         assert (w, p) == (W, P) and 32 * w * p >= n and u >= 1
 
