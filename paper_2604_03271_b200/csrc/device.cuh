@@ -48,6 +48,10 @@ struct GroupState {  // mutable per-group scalars; read back by the host every r
 // bisection state machine of next_beta, slice partial sums and the slice
 // offsets of the grid-level CDF scan.
 constexpr int kMaxSlices = 512;
+// next_beta bisection steps per k_tp_ess_tree launch, and its delta slots
+// (slot 0: the full step; 1 .. 2^D - 1: the heap of bisection midpoints)
+constexpr int kEssDepth = 3;
+constexpr int kEssSlots = 1 << kEssDepth;
 struct TemperScratch {
   double emin, lo, hi, full, beta_next;
   double m, lse, u;
@@ -57,6 +61,7 @@ struct TemperScratch {
   unsigned int counter, pad2;
   double part[kMaxSlices][2];
   double offs[kMaxSlices + 1];
+  double tpart[kMaxSlices][2 * kEssSlots];  // k_tp_ess_tree: (sum w, sum w^2) per slice and slot
 };
 
 struct GroupDesc {  // immutable per group

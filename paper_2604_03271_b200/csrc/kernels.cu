@@ -569,6 +569,101 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_ess(const GroupDesc* __rest
   }
 }
 
+// kEssDepth steps of the next_beta bisection (smc.cpp:68-93) per launch.  One
+// pass over E evaluates every delta the next kEssDepth steps can visit: the
+// heap of interval midpoints below the current (lo, hi) (node j has children
+// 2j = (lo_j, m_j) and 2j + 1 = (m_j, hi_j)), plus the full step while it < 0.
+// The last slice block then replays the bisection through those slots with
+// fin_ess.  Deltas, per-slot sums (same per-thread order, same reduction
+// trees, slices summed in order) and control flow are those of one k_tp_ess
+// launch per step, so beta_next is bitwise the same.
+__global__ void __launch_bounds__(kGridThreads) k_tp_ess_tree(const GroupDesc* __restrict__ gds,
+                                                              const int* __restrict__ list) {
+  __shared__ double shp[2 * kEssSlots][kGridThreads / 32];
+  SliceCtx c;
+  if (!slice_ctx(gds, list, c)) return;
+  const GroupDesc& g = *c.g;
+  TemperScratch* ts = c.ts;
+  if (ts->done || ts->err) return;
+  GroupState* st = g.st;
+  const bool first = ts->it < 0;
+  double dl[kEssSlots], lo[kEssSlots], hi[kEssSlots];
+  dl[0] = ts->full;
+  lo[1] = ts->lo;
+  hi[1] = ts->hi;
+#pragma unroll
+  for (int j = 1; j < kEssSlots; ++j) {
+    dl[j] = 0.5 * (lo[j] + hi[j]);
+    if (2 * j + 1 < kEssSlots) {
+      lo[2 * j] = lo[j];
+      hi[2 * j] = dl[j];
+      lo[2 * j + 1] = dl[j];
+      hi[2 * j + 1] = hi[j];
+    }
+  }
+  double cc[kEssSlots];
+#pragma unroll
+  for (int s = 0; s < kEssSlots; ++s) cc[s] = -dl[s] * g.n_data;
+  const double emin = ts->emin;
+  const double* E = g.E[st->cur];
+  double a1[kEssSlots], a2[kEssSlots];
+#pragma unroll
+  for (int s = 0; s < kEssSlots; ++s) a1[s] = a2[s] = 0.0;
+  for (int64_t i = c.i0 + threadIdx.x; i < c.i1; i += blockDim.x) {
+    const double x = E[i] - emin;
+#pragma unroll
+    for (int s = 0; s < kEssSlots; ++s) {
+      if (s == 0 && !first) continue;
+      const double w = exp_neg_split(cc[s] * x);
+      a1[s] += w;
+      a2[s] += w * w;
+    }
+  }
+  // block_reduce's trees for all 2 kEssSlots values at once: xor tree within
+  // each warp, then warp v reduces value v over the warps' partials
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int s = 0; s < kEssSlots; ++s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a1[s] += __shfl_xor_sync(0xffffffffu, a1[s], o);
+      a2[s] += __shfl_xor_sync(0xffffffffu, a2[s], o);
+    }
+    if (lane == 0) {
+      shp[2 * s][warp] = a1[s];
+      shp[2 * s + 1][warp] = a2[s];
+    }
+  }
+  __syncthreads();
+  if (warp < 2 * kEssSlots) {
+    double v = lane < nw ? shp[warp][lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) {
+      ts->tpart[blockIdx.x][warp] = v;
+      __threadfence();  // written by 16 threads: each publishes before last_block's count
+    }
+  }
+  if (last_block(&ts->counter, g.nslices) && threadIdx.x == 0) {
+    ts->counter = 0;
+    auto step = [&](int s) {  // one bisection step with slot s; true = continue
+      double s1 = 0.0, s2 = 0.0;
+      for (int sl = 0; sl < g.nslices; ++sl) {
+        s1 += ts->tpart[sl][2 * s];
+        s2 += ts->tpart[sl][2 * s + 1];
+      }
+      fin_ess(g, ts, s1, s2);
+      if (ts->done || ts->err) return -1;
+      return (s1 * s1 / s2) / (double)g.T > g.ess_target ? 1 : 0;
+    };
+    int go = first ? step(0) : 0;
+    for (int j = 1, k = 0; go >= 0 && k < kEssDepth; ++k) {
+      go = step(j);
+      j = 2 * j + (go > 0 ? 1 : 0);
+    }
+  }
+}
+
 // max of the incremental log-weights (smc.cpp:55-59, math.hpp:20-24)
 __global__ void __launch_bounds__(kGridThreads) k_tp_wmax(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
   __shared__ TemperShared sh;
@@ -982,7 +1077,7 @@ cudaError_t prime_level_kernels(int family, int noise, const Shape& s, int dmax)
   e = launch_move(family, noise, s, dmax, nullptr, nullptr, nullptr, 0, 0, nullptr);
   if (e != cudaSuccess) return e;
   const void* ks[] = {(const void*)k_init_draw, (const void*)k_temper,      (const void*)k_tp_emin,
-                      (const void*)k_tp_ess,    (const void*)k_tp_wmax,     (const void*)k_tp_wsum,
+                      (const void*)k_tp_ess,    (const void*)k_tp_ess_tree, (const void*)k_tp_wmax,     (const void*)k_tp_wsum,
                       (const void*)k_tp_offsets, (const void*)k_tp_resample, (const void*)k_stats_grid,
                       (const void*)k_stats_final};
   for (const void* k : ks) {
@@ -1018,17 +1113,19 @@ cudaError_t launch_temper(const GroupDesc* gds, const int* list, int n_list, cud
   k_temper<<<n_list, kTemperThreads, 0, st>>>(gds, list);
   return cudaGetLastError();
 }
+constexpr int kEssLaunches = (60 + kEssDepth - 1) / kEssDepth;  // first launch: + the full step
 cudaError_t launch_temper_grid(const GroupDesc* gds, const int* list, int n_list, int max_slices, cudaStream_t st) {
   const dim3 grid(max_slices, n_list);
   k_tp_emin<<<grid, kGridThreads, 0, st>>>(gds, list);
-  for (int it = 0; it < 61; ++it) k_tp_ess<<<grid, kGridThreads, 0, st>>>(gds, list);
+  // the full step + at most 60 bisection steps (fin_ess), kEssDepth per launch
+  for (int it = 0; it < kEssLaunches; ++it) k_tp_ess_tree<<<grid, kGridThreads, 0, st>>>(gds, list);
   k_tp_wmax<<<grid, kGridThreads, 0, st>>>(gds, list);
   k_tp_wsum<<<grid, kGridThreads, 0, st>>>(gds, list);
   k_tp_offsets<<<grid, kGridThreads, 0, st>>>(gds, list);
   k_tp_resample<<<grid, kGridThreads, 0, st>>>(gds, list);
   return cudaGetLastError();
 }
-int temper_grid_launches() { return 66; }
+int temper_grid_launches() { return 5 + kEssLaunches; }
 
 cudaError_t launch_temper_sharded(const GroupDesc* gds, const int* list, int n_list, int max_slices, Exchange& x,
                                   cudaStream_t st) {
