@@ -76,7 +76,7 @@ struct GroupDesc {  // immutable per group
   int sharded;
   int pbase;
   int shard, nshards;  // this shard's index and the shard count of the run
-  double* xbuf;        // [2] cross-shard exchange of the tempering phases
+  double* xbuf;        // [2 kEssSlots] cross-shard exchange of the tempering phases
   double* xgat;        // [nshards][2] gathered (weight total, particle count) per shard
   // energy: E = e_a0 + e_a1 * sum(l_k); device noise parameters
   double e_a0, e_a1;

@@ -791,7 +791,7 @@ struct ClassRun {
       bytes += Arena::al(T * 8) + Arena::al(kHist * (1 + 2 * d) * 8);
       bytes += Arena::al((size_t)R.cfg.max_levels * 4 * 8);
       bytes += Arena::al(2 * d * 8) + Arena::al(d * 8);                         // stat_acc, out_shift
-      bytes += Arena::al(2 * 8) + Arena::al(2 * 8 * (size_t)R.nshards);        // xbuf, xgat
+      bytes += Arena::al(2 * kEssSlots * 8) + Arena::al(2 * 8 * (size_t)R.nshards);  // xbuf, xgat
       bytes += Arena::al(R.refl.size() * 4 + 8) + Arena::al(R.refl_off.size() * 4 + 4);  // xrd reflections
       if (T > grid_temper_t() || xch) bytes += Arena::al(sizeof(TemperScratch));  // grid tempering
     }
@@ -901,7 +901,7 @@ struct ClassRun {
       g.shard = R.shard;
       g.nshards = R.nshards;
       g.pbase = (int)R.pbase;
-      g.xbuf = ar.take<double>(2);
+      g.xbuf = ar.take<double>(2 * kEssSlots);
       g.xgat = ar.take<double>(2 * (size_t)R.nshards);
       if (!R.refl.empty()) {
         float2* rf = ar.take<float2>(R.refl.size() / 2);

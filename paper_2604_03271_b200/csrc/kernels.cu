@@ -530,42 +530,19 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_emin(const GroupDesc* __res
   }
 }
 
-__global__ void __launch_bounds__(kGridThreads) k_tp_ess(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
-  __shared__ TemperShared sh;
-  SliceCtx c;
-  if (!slice_ctx(gds, list, c)) return;
-  const GroupDesc& g = *c.g;
-  TemperScratch* ts = c.ts;
-  if (ts->done || ts->err) return;
-  GroupState* st = g.st;
-  const double delta = ts->it < 0 ? ts->full : 0.5 * (ts->lo + ts->hi);
-  const double cc = -delta * g.n_data, emin = ts->emin;
-  const double* E = g.E[st->cur];
-  double a1 = 0.0, a2 = 0.0;
-  for (int64_t i = c.i0 + threadIdx.x; i < c.i1; i += blockDim.x) {
-    const double w = exp_neg_split(cc * (E[i] - emin));
-    a1 += w;
-    a2 += w * w;
-  }
-  a1 = block_reduce(a1, sh.red, OpAdd(), 0.0);
-  a2 = block_reduce(a2, sh.red, OpAdd(), 0.0);
-  if (threadIdx.x == 0) {
-    ts->part[blockIdx.x][0] = a1;
-    ts->part[blockIdx.x][1] = a2;
-  }
-  if (last_block(&ts->counter, g.nslices) && threadIdx.x == 0) {
-    double s1 = 0.0, s2 = 0.0;
-    for (int s = 0; s < g.nslices; ++s) {
-      s1 += ts->part[s][0];
-      s2 += ts->part[s][1];
-    }
-    ts->counter = 0;
-    if (g.sharded) {
-      g.xbuf[0] = s1;
-      g.xbuf[1] = s2;
-    } else {
-      fin_ess(g, ts, s1, s2);
-    }
+// the bisection steps of one k_tp_ess_tree pass from its per-slot totals
+// sums[2 s] = sum w, sums[2 s + 1] = sum w^2 (slot layout: k_tp_ess_tree)
+__device__ void ess_replay(const GroupDesc& g, TemperScratch* ts, const double* sums) {
+  auto step = [&](int s) {  // one fin_ess step with slot s: -1 = finished, else 1 = went right (lo = delta)
+    const double s1 = sums[2 * s], s2 = sums[2 * s + 1];
+    fin_ess(g, ts, s1, s2);
+    if (ts->done || ts->err) return -1;
+    return (s1 * s1 / s2) / (double)g.T > g.ess_target ? 1 : 0;
+  };
+  int go = ts->it < 0 ? step(0) : 0;
+  for (int j = 1, k = 0; go >= 0 && k < kEssDepth; ++k) {
+    go = step(j);
+    j = 2 * j + (go > 0 ? 1 : 0);
   }
 }
 
@@ -575,8 +552,8 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_ess(const GroupDesc* __rest
 // 2j = (lo_j, m_j) and 2j + 1 = (m_j, hi_j)), plus the full step while it < 0.
 // The last slice block then replays the bisection through those slots with
 // fin_ess.  Deltas, per-slot sums (same per-thread order, same reduction
-// trees, slices summed in order) and control flow are those of one k_tp_ess
-// launch per step, so beta_next is bitwise the same.
+// trees, slices summed in order) and control flow are those of one single-delta
+// pass per step, so beta_next is bitwise the same.
 __global__ void __launch_bounds__(kGridThreads) k_tp_ess_tree(const GroupDesc* __restrict__ gds,
                                                               const int* __restrict__ list) {
   __shared__ double shp[2 * kEssSlots][kGridThreads / 32];
@@ -646,20 +623,16 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_ess_tree(const GroupDesc* _
   }
   if (last_block(&ts->counter, g.nslices) && threadIdx.x == 0) {
     ts->counter = 0;
-    auto step = [&](int s) {  // one bisection step with slot s; true = continue
-      double s1 = 0.0, s2 = 0.0;
-      for (int sl = 0; sl < g.nslices; ++sl) {
-        s1 += ts->tpart[sl][2 * s];
-        s2 += ts->tpart[sl][2 * s + 1];
-      }
-      fin_ess(g, ts, s1, s2);
-      if (ts->done || ts->err) return -1;
-      return (s1 * s1 / s2) / (double)g.T > g.ess_target ? 1 : 0;
-    };
-    int go = first ? step(0) : 0;
-    for (int j = 1, k = 0; go >= 0 && k < kEssDepth; ++k) {
-      go = step(j);
-      j = 2 * j + (go > 0 ? 1 : 0);
+    double sums[2 * kEssSlots];
+    for (int v = 0; v < 2 * kEssSlots; ++v) {
+      double a = 0.0;
+      for (int sl = 0; sl < g.nslices; ++sl) a += ts->tpart[sl][v];
+      sums[v] = a;
+    }
+    if (g.sharded) {
+      for (int v = 0; v < 2 * kEssSlots; ++v) g.xbuf[v] = sums[v];
+    } else {
+      ess_replay(g, ts, sums);
     }
   }
 }
@@ -813,9 +786,9 @@ __global__ void k_tpf_emin(const GroupDesc* __restrict__ gds, const int* __restr
   const GroupDesc& g = gds[list[blockIdx.x]];
   if (threadIdx.x == 0 && !g.ts->err) fin_emin(g, g.ts, g.xbuf[0]);
 }
-__global__ void k_tpf_ess(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
+__global__ void k_tpf_ess_tree(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
   const GroupDesc& g = gds[list[blockIdx.x]];
-  if (threadIdx.x == 0 && !g.ts->done && !g.ts->err) fin_ess(g, g.ts, g.xbuf[0], g.xbuf[1]);
+  if (threadIdx.x == 0 && !g.ts->done && !g.ts->err) ess_replay(g, g.ts, g.xbuf);
 }
 __global__ void k_tpf_wmax(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
   const GroupDesc& g = gds[list[blockIdx.x]];
@@ -1077,7 +1050,7 @@ cudaError_t prime_level_kernels(int family, int noise, const Shape& s, int dmax)
   e = launch_move(family, noise, s, dmax, nullptr, nullptr, nullptr, 0, 0, nullptr);
   if (e != cudaSuccess) return e;
   const void* ks[] = {(const void*)k_init_draw, (const void*)k_temper,      (const void*)k_tp_emin,
-                      (const void*)k_tp_ess,    (const void*)k_tp_ess_tree, (const void*)k_tp_wmax,     (const void*)k_tp_wsum,
+                      (const void*)k_tp_ess_tree, (const void*)k_tp_wmax,     (const void*)k_tp_wsum,
                       (const void*)k_tp_offsets, (const void*)k_tp_resample, (const void*)k_stats_grid,
                       (const void*)k_stats_final};
   for (const void* k : ks) {
@@ -1136,10 +1109,10 @@ cudaError_t launch_temper_sharded(const GroupDesc* gds, const int* list, int n_l
   k_tp_emin<<<grid, kGridThreads, 0, st>>>(gds, list);
   SMC_X(x.reduce(0, 1, XOP_MIN, st));
   k_tpf_emin<<<n_list, 32, 0, st>>>(gds, list);
-  for (int it = 0; it < 61; ++it) {
-    k_tp_ess<<<grid, kGridThreads, 0, st>>>(gds, list);
-    SMC_X(x.reduce(0, 2, XOP_SUM, st));
-    k_tpf_ess<<<n_list, 32, 0, st>>>(gds, list);
+  for (int it = 0; it < kEssLaunches; ++it) {  // (sum w, sum w^2) of every slot in one exchange
+    k_tp_ess_tree<<<grid, kGridThreads, 0, st>>>(gds, list);
+    SMC_X(x.reduce(0, 2 * kEssSlots, XOP_SUM, st));
+    k_tpf_ess_tree<<<n_list, 32, 0, st>>>(gds, list);
   }
   k_tp_wmax<<<grid, kGridThreads, 0, st>>>(gds, list);
   SMC_X(x.reduce(0, 1, XOP_MAX, st));
@@ -1154,7 +1127,7 @@ cudaError_t launch_temper_sharded(const GroupDesc* gds, const int* list, int n_l
 #undef SMC_X
   return cudaGetLastError();
 }
-int temper_sharded_launches() { return 2 * 66 - 1; }  // + one exchange per phase (kernels or NCCL)
+int temper_sharded_launches() { return 2 * temper_grid_launches() - 1; }  // + one exchange per phase (kernels or NCCL)
 
 cudaError_t launch_stats_sharded(const GroupDesc* gds, const int* list, int n_list, int dmax, Exchange& x,
                                  cudaStream_t st) {
