@@ -532,6 +532,7 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_emin(const GroupDesc* __res
 
 // the bisection steps of one k_tp_ess_tree pass from its per-slot totals
 // sums[2 s] = sum w, sums[2 s + 1] = sum w^2 (slot layout: k_tp_ess_tree)
+template <int D>
 __device__ void ess_replay(const GroupDesc& g, TemperScratch* ts, const double* sums) {
   auto step = [&](int s) {  // one fin_ess step with slot s: -1 = finished, else 1 = went right (lo = delta)
     const double s1 = sums[2 * s], s2 = sums[2 * s + 1];
@@ -540,23 +541,27 @@ __device__ void ess_replay(const GroupDesc& g, TemperScratch* ts, const double* 
     return (s1 * s1 / s2) / (double)g.T > g.ess_target ? 1 : 0;
   };
   int go = ts->it < 0 ? step(0) : 0;
-  for (int j = 1, k = 0; go >= 0 && k < kEssDepth; ++k) {
+  for (int j = 1, k = 0; go >= 0 && k < D; ++k) {
     go = step(j);
     j = 2 * j + (go > 0 ? 1 : 0);
   }
 }
 
-// kEssDepth steps of the next_beta bisection (smc.cpp:68-93) per launch.  One
-// pass over E evaluates every delta the next kEssDepth steps can visit: the
+// D steps of the next_beta bisection (smc.cpp:68-93) per launch (D = 3 by
+// default; SPECMC_ESS_DEPTH=1 gives one step per launch, the parity check).  One
+// pass over E evaluates every delta the next D steps can visit: the
 // heap of interval midpoints below the current (lo, hi) (node j has children
 // 2j = (lo_j, m_j) and 2j + 1 = (m_j, hi_j)), plus the full step while it < 0.
 // The last slice block then replays the bisection through those slots with
 // fin_ess.  Deltas, per-slot sums (same per-thread order, same reduction
 // trees, slices summed in order) and control flow are those of one single-delta
 // pass per step, so beta_next is bitwise the same.
+template <int D>
 __global__ void __launch_bounds__(kGridThreads) k_tp_ess_tree(const GroupDesc* __restrict__ gds,
                                                               const int* __restrict__ list) {
-  __shared__ double shp[2 * kEssSlots][kGridThreads / 32];
+  constexpr int S = 1 << D;  // slots: full step + 2^D - 1 heap nodes
+  static_assert(2 * S <= kGridThreads / 32, "one warp per reduced value");
+  __shared__ double shp[2 * S][kGridThreads / 32];
   SliceCtx c;
   if (!slice_ctx(gds, list, c)) return;
   const GroupDesc& g = *c.g;
@@ -564,43 +569,43 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_ess_tree(const GroupDesc* _
   if (ts->done || ts->err) return;
   GroupState* st = g.st;
   const bool first = ts->it < 0;
-  double dl[kEssSlots], lo[kEssSlots], hi[kEssSlots];
+  double dl[S], lo[S], hi[S];
   dl[0] = ts->full;
   lo[1] = ts->lo;
   hi[1] = ts->hi;
 #pragma unroll
-  for (int j = 1; j < kEssSlots; ++j) {
+  for (int j = 1; j < S; ++j) {
     dl[j] = 0.5 * (lo[j] + hi[j]);
-    if (2 * j + 1 < kEssSlots) {
+    if (2 * j + 1 < S) {
       lo[2 * j] = lo[j];
       hi[2 * j] = dl[j];
       lo[2 * j + 1] = dl[j];
       hi[2 * j + 1] = hi[j];
     }
   }
-  double cc[kEssSlots];
+  double cc[S];
 #pragma unroll
-  for (int s = 0; s < kEssSlots; ++s) cc[s] = -dl[s] * g.n_data;
+  for (int s = 0; s < S; ++s) cc[s] = -dl[s] * g.n_data;
   const double emin = ts->emin;
   const double* E = g.E[st->cur];
-  double a1[kEssSlots], a2[kEssSlots];
+  double a1[S], a2[S];
 #pragma unroll
-  for (int s = 0; s < kEssSlots; ++s) a1[s] = a2[s] = 0.0;
+  for (int s = 0; s < S; ++s) a1[s] = a2[s] = 0.0;
   for (int64_t i = c.i0 + threadIdx.x; i < c.i1; i += blockDim.x) {
     const double x = E[i] - emin;
 #pragma unroll
-    for (int s = 0; s < kEssSlots; ++s) {
+    for (int s = 0; s < S; ++s) {
       if (s == 0 && !first) continue;
       const double w = exp_neg_split(cc[s] * x);
       a1[s] += w;
       a2[s] += w * w;
     }
   }
-  // block_reduce's trees for all 2 kEssSlots values at once: xor tree within
+  // block_reduce's trees for all 2 S values at once: xor tree within
   // each warp, then warp v reduces value v over the warps' partials
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
-  for (int s = 0; s < kEssSlots; ++s) {
+  for (int s = 0; s < S; ++s) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       a1[s] += __shfl_xor_sync(0xffffffffu, a1[s], o);
@@ -612,7 +617,7 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_ess_tree(const GroupDesc* _
     }
   }
   __syncthreads();
-  if (warp < 2 * kEssSlots) {
+  if (warp < 2 * S) {
     double v = lane < nw ? shp[warp][lane] : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -623,16 +628,16 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_ess_tree(const GroupDesc* _
   }
   if (last_block(&ts->counter, g.nslices) && threadIdx.x == 0) {
     ts->counter = 0;
-    double sums[2 * kEssSlots];
-    for (int v = 0; v < 2 * kEssSlots; ++v) {
+    double sums[2 * S];
+    for (int v = 0; v < 2 * S; ++v) {
       double a = 0.0;
       for (int sl = 0; sl < g.nslices; ++sl) a += ts->tpart[sl][v];
       sums[v] = a;
     }
     if (g.sharded) {
-      for (int v = 0; v < 2 * kEssSlots; ++v) g.xbuf[v] = sums[v];
+      for (int v = 0; v < 2 * S; ++v) g.xbuf[v] = sums[v];
     } else {
-      ess_replay(g, ts, sums);
+      ess_replay<D>(g, ts, sums);
     }
   }
 }
@@ -786,9 +791,10 @@ __global__ void k_tpf_emin(const GroupDesc* __restrict__ gds, const int* __restr
   const GroupDesc& g = gds[list[blockIdx.x]];
   if (threadIdx.x == 0 && !g.ts->err) fin_emin(g, g.ts, g.xbuf[0]);
 }
+template <int D>
 __global__ void k_tpf_ess_tree(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
   const GroupDesc& g = gds[list[blockIdx.x]];
-  if (threadIdx.x == 0 && !g.ts->done && !g.ts->err) ess_replay(g, g.ts, g.xbuf);
+  if (threadIdx.x == 0 && !g.ts->done && !g.ts->err) ess_replay<D>(g, g.ts, g.xbuf);
 }
 __global__ void k_tpf_wmax(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
   const GroupDesc& g = gds[list[blockIdx.x]];
@@ -1050,7 +1056,7 @@ cudaError_t prime_level_kernels(int family, int noise, const Shape& s, int dmax)
   e = launch_move(family, noise, s, dmax, nullptr, nullptr, nullptr, 0, 0, nullptr);
   if (e != cudaSuccess) return e;
   const void* ks[] = {(const void*)k_init_draw, (const void*)k_temper,      (const void*)k_tp_emin,
-                      (const void*)k_tp_ess_tree, (const void*)k_tp_wmax,     (const void*)k_tp_wsum,
+                      (const void*)k_tp_ess_tree<1>, (const void*)k_tp_ess_tree<kEssDepth>, (const void*)k_tp_wmax,     (const void*)k_tp_wsum,
                       (const void*)k_tp_offsets, (const void*)k_tp_resample, (const void*)k_stats_grid,
                       (const void*)k_stats_final};
   for (const void* k : ks) {
@@ -1086,19 +1092,30 @@ cudaError_t launch_temper(const GroupDesc* gds, const int* list, int n_list, cud
   k_temper<<<n_list, kTemperThreads, 0, st>>>(gds, list);
   return cudaGetLastError();
 }
-constexpr int kEssLaunches = (60 + kEssDepth - 1) / kEssDepth;  // first launch: + the full step
+// bisection steps per ESS pass: kEssDepth, or SPECMC_ESS_DEPTH=1 (one step per
+// pass, the order of the reference's loop; tests compare the two bitwise)
+static int ess_depth() {
+  static const int v = std::getenv("SPECMC_ESS_DEPTH") && std::atoi(std::getenv("SPECMC_ESS_DEPTH")) == 1 ? 1 : kEssDepth;
+  return v;
+}
+// the full step + at most 60 bisection steps (fin_ess), D per pass (the first also takes the full step)
+static int ess_launches() { return (60 + ess_depth() - 1) / ess_depth(); }
+template <int D>
+static void launch_ess_pass(dim3 grid, const GroupDesc* gds, const int* list, cudaStream_t st) {
+  k_tp_ess_tree<D><<<grid, kGridThreads, 0, st>>>(gds, list);
+}
 cudaError_t launch_temper_grid(const GroupDesc* gds, const int* list, int n_list, int max_slices, cudaStream_t st) {
   const dim3 grid(max_slices, n_list);
   k_tp_emin<<<grid, kGridThreads, 0, st>>>(gds, list);
-  // the full step + at most 60 bisection steps (fin_ess), kEssDepth per launch
-  for (int it = 0; it < kEssLaunches; ++it) k_tp_ess_tree<<<grid, kGridThreads, 0, st>>>(gds, list);
+  for (int it = 0; it < ess_launches(); ++it)
+    ess_depth() == 1 ? launch_ess_pass<1>(grid, gds, list, st) : launch_ess_pass<kEssDepth>(grid, gds, list, st);
   k_tp_wmax<<<grid, kGridThreads, 0, st>>>(gds, list);
   k_tp_wsum<<<grid, kGridThreads, 0, st>>>(gds, list);
   k_tp_offsets<<<grid, kGridThreads, 0, st>>>(gds, list);
   k_tp_resample<<<grid, kGridThreads, 0, st>>>(gds, list);
   return cudaGetLastError();
 }
-int temper_grid_launches() { return 5 + kEssLaunches; }
+int temper_grid_launches() { return 5 + ess_launches(); }
 
 cudaError_t launch_temper_sharded(const GroupDesc* gds, const int* list, int n_list, int max_slices, Exchange& x,
                                   cudaStream_t st) {
@@ -1109,10 +1126,16 @@ cudaError_t launch_temper_sharded(const GroupDesc* gds, const int* list, int n_l
   k_tp_emin<<<grid, kGridThreads, 0, st>>>(gds, list);
   SMC_X(x.reduce(0, 1, XOP_MIN, st));
   k_tpf_emin<<<n_list, 32, 0, st>>>(gds, list);
-  for (int it = 0; it < kEssLaunches; ++it) {  // (sum w, sum w^2) of every slot in one exchange
-    k_tp_ess_tree<<<grid, kGridThreads, 0, st>>>(gds, list);
-    SMC_X(x.reduce(0, 2 * kEssSlots, XOP_SUM, st));
-    k_tpf_ess_tree<<<n_list, 32, 0, st>>>(gds, list);
+  for (int it = 0; it < ess_launches(); ++it) {  // (sum w, sum w^2) of every slot in one exchange
+    if (ess_depth() == 1) {
+      launch_ess_pass<1>(grid, gds, list, st);
+      SMC_X(x.reduce(0, 2 * 2, XOP_SUM, st));
+      k_tpf_ess_tree<1><<<n_list, 32, 0, st>>>(gds, list);
+    } else {
+      launch_ess_pass<kEssDepth>(grid, gds, list, st);
+      SMC_X(x.reduce(0, 2 * kEssSlots, XOP_SUM, st));
+      k_tpf_ess_tree<kEssDepth><<<n_list, 32, 0, st>>>(gds, list);
+    }
   }
   k_tp_wmax<<<grid, kGridThreads, 0, st>>>(gds, list);
   SMC_X(x.reduce(0, 1, XOP_MAX, st));

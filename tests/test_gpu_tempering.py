@@ -1,0 +1,58 @@
+"""Grid-level tempering (T > 2^15): the tree ESS passes (k_tp_ess_tree, three
+next_beta bisection steps per pass over E) against one bisection step per
+pass (SPECMC_ESS_DEPTH=1, the order of the reference's loop, smc.cpp:68-93).
+
+Tolerance: bitwise.  Every delta, per-slot sum and fin_ess step is the same in
+both schedules, so F, the tempering ladder and the posterior must be equal bit
+for bit — for an unsharded run and for a run split over 2 in-process shards
+(one exchange of all slots per pass vs one per step).
+"""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+_SCRIPT = r"""
+import hashlib, json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2604_03271_b200 as S
+from paper_2604_03271_b200 import model as M
+from paper_2604_03271_b200 import synthetic as syn
+sp, _ = syn.gen_xps(3, 5)
+spec = M.xps_model(2, sp)
+cfg = S.SmcConfig(T=1 << 16, n=4, seed=11)
+out = {}
+S.stats_reset()
+for name, r in (("grid", S.smc_run(spec, sp, cfg)), ("shard2", S.smc_run_sharded(spec, sp, cfg, n_virtual=2))):
+    out[name] = dict(F=r.F.hex(), levels=len(r.arrays["ladder"]),
+                     ladder=hashlib.sha256(np.ascontiguousarray(r.arrays["ladder"]).tobytes()).hexdigest(),
+                     post=hashlib.sha256(np.ascontiguousarray(r.posterior).tobytes()).hexdigest())
+out["launches"] = S.stats()["kernel_launches"]
+print(json.dumps(out))
+"""
+
+
+def _run(depth):
+    env = dict(os.environ)
+    env.pop("SPECMC_ESS_DEPTH", None)
+    if depth is not None:
+        env["SPECMC_ESS_DEPTH"] = str(depth)
+    cp = subprocess.run([sys.executable, "-c", _SCRIPT, str(ROOT)], env=env, capture_output=True, text=True, timeout=600)
+    assert cp.returncode == 0, cp.stderr[-3000:]
+    import json
+    return json.loads(cp.stdout.strip().splitlines()[-1])
+
+
+def test_tree_ess_passes_equal_single_steps_bitwise():
+    tree, single = _run(None), _run(1)
+    assert tree["grid"]["levels"] > 3
+    # the schedules differ (25 vs 65 tempering launches per unsharded level) ...
+    assert tree.pop("launches") < single.pop("launches")
+    # ... the results do not
+    assert tree == single, (tree, single)
