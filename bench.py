@@ -56,7 +56,9 @@ MUFU_NOISE = {"XpsHeteroNoise": 2.0, "GaussianApproxPoissonNoise": 2.0, "Poisson
               "GaussianFixedNoise": 0.0}
 MUFU_NOISE_EXECUTED = {"XpsHeteroNoise": 1.0, "GaussianApproxPoissonNoise": 1.0, "PoissonNoise": 1.0,
                        "GaussianFixedNoise": 0.0}
-CPU_SAMPLE_T = 256
+# reference-CPU sample size per config (bounded: a few seconds of CPU per step;
+# 64+ chains keep all host threads busy)
+CPU_SAMPLE_T = {"C1": 4096, "C2": 512, "C3": 512, "C5": 256}
 
 
 def parse():
@@ -136,13 +138,47 @@ WORKLOAD_TEXT = {
 }
 
 
-def cpu_reference_sample(workload, seed, T):
-    """Reference smc_run (oracle/_ref, unchanged reference sources) for K = 1..Kmax
-    at T particles, workers = 0.  Returns (evals, seconds, cores, kind)."""
+def inputs_module():
+    """The package's input synthesis (synthetic.py / model.py) WITHOUT importing
+    the package: the reference arm must not map libspecmc_b200.so.  A bare
+    namespace stands in for the package, so its __init__ (which loads the
+    library) never runs; model.py defers its library import to desc()."""
+    import importlib
+    import types
+    name = "paper_2604_03271_b200"
+    if name not in sys.modules:
+        stub = types.ModuleType(name)
+        stub.__path__ = [str(ROOT / name)]
+        sys.modules[name] = stub
+    return importlib.import_module(name + ".synthetic")
+
+
+def workload_config(args, w, ws):
+    """The `config` object of both arms' JSON lines (identical by construction)."""
+    ks = list(range(w.k_range[0], w.k_range[1] + 1))
+    N = len(w.data.xs)
+    return {"workload": f"{args.config}: {WORKLOAD_TEXT.get(args.config, 'synthetic spectrum')}, N={N},"
+                        f" {w.family} family K={ks[0]}..{ks[-1]}, T={w.T}, n={w.n}, ess 0.5; 1 trial per GPU",
+            "N": N, "K_range": [ks[0], ks[-1]], "T": w.T, "n": w.n, "trials_per_gpu": 1,
+            "l2": "flushed between steps (256 MiB write)", "parallelism": f"trials x{ws} (weak)"}
+
+
+def cpu_reference_sample(workload, seed, T, timing=True):
+    """Reference smc_run (oracle/_ref: the unchanged reference sources) for
+    K = 1..Kmax at T particles, workers = 0 (all host threads), the CLI's serial
+    K loop (specmc_main.cpp:147-170).  timing=True uses the Release-flag build
+    for this host's ISA (oracle/build_oracle.timing_ref_so).  Returns
+    (evals, seconds, cores, kind, build)."""
     from oracle.oracle import OracleModel, Port, Ref, ref_available
     ks = list(range(workload.k_range[0], workload.k_range[1] + 1))
     kind = "reference" if ref_available() else "port"
-    lib = Ref() if kind == "reference" else Port()
+    build = "oracle port (1 thread)"
+    if kind == "reference":
+        from oracle.build_oracle import timing_ref_so
+        so, build = timing_ref_so() if timing else (None, "parity build")
+        lib = Ref(so) if so is not None else Ref()
+    else:
+        lib = Port()
     evals, secs = 0, 0.0
     for K in ks:
         spec = workload.spec(K)
@@ -160,35 +196,48 @@ def cpu_reference_sample(workload, seed, T):
             secs += time.perf_counter() - t0
         evals += T * spec.d * r.levels
     cores = os.cpu_count() if kind == "reference" else 1
-    return evals, secs, cores, kind
+    return evals, secs, cores, kind, build
+
+
+def library_mapped():
+    try:
+        return "libspecmc_b200" in Path("/proc/self/maps").read_text()
+    except OSError:
+        return False
 
 
 def run_reference(args, ws, rank):
     if rank != 0:
         return
-    from paper_2604_03271_b200 import synthetic as syn
+    syn = inputs_module()
     w = syn.config(args.config)
-    T = CPU_SAMPLE_T
+    T = CPU_SAMPLE_T[args.config]
     seed = syn.trial_seed(4242, 0)
+    # warm-up: page the library and the spectrum in (one K at a small T: the
+    # CPU has no caches worth warming beyond that)
+    w_small = syn.config(args.config, 64)
+    w_small.k_range = (w.k_range[0], w.k_range[0])
     for _ in range(args.warmup):
-        cpu_reference_sample(w, seed, T)
+        cpu_reference_sample(w_small, seed, 64)
     ev, secs = 0, 0.0
     for _ in range(args.steps):
-        e, s, cores, kind = cpu_reference_sample(w, seed, T)
+        e, s_, cores, kind, build = cpu_reference_sample(w, seed, T)
         ev += e
-        secs += s
+        secs += s_
+    assert not library_mapped(), "reference arm mapped the product library"
     v = ev / secs
     line = {
         "metric": f"particle-likelihood evals/s (K=1..{w.k_range[1]} model selection, {args.config})",
         "value": v, "unit": "evals/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"{args.config} bounded sample: N={len(w.data.xs)}, K={w.k_range[0]}..{w.k_range[1]},"
-                               f" T={T}, n={w.n} (reference CPU path)", "N": len(w.data.xs), "T": T, "n": w.n,
-                   "K_range": list(w.k_range)},
+        "config": workload_config(args, w, ws),
         "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": kind,
-                         "sample": f"smc_run K={w.k_range[0]}..{w.k_range[1]} at T={T}, workers=0, per step"},
+                         "sample": f"each step: smc_run for K={w.k_range[0]}..{w.k_range[1]} (serial K loop, "
+                                   f"workers=0) on the same spectrum at T={T} particles instead of {w.T}; "
+                                   f"evals/s = sum T*d*levels / sum wall_seconds; build {build}"},
         "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "product_library_mapped": False,
     }
     print(json.dumps(line), flush=True)
 
@@ -296,10 +345,7 @@ def run_ours(args, ws, rank, local):
         "ms_per_step": elapsed / args.steps * 1e3, "time_to_evidence_s": elapsed / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32 point terms / f64 accumulation", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {WORKLOAD_TEXT.get(args.config, 'synthetic spectrum')}, N={N},"
-                               f" {w.family} family K={ks[0]}..{ks[-1]}, T={w.T}, n={w.n}, ess 0.5; 1 trial per GPU",
-                   "N": N, "K_range": [ks[0], ks[-1]], "T": w.T, "n": w.n, "trials_per_gpu": 1,
-                   "l2": "flushed between steps (256 MiB write)", "parallelism": f"trials x{ws} (weak)"},
+        "config": workload_config(args, w, ws),
         "K_selected": k_sel, "trials_per_step": trials_step, "point_evals_per_s_move": pe_rate,
         "gpu_launches": st["kernel_launches"],
         "roofline": {"bound": "sfu", "achieved": achieved / 1e9, "peak": peak_mufu / 1e9,
@@ -316,10 +362,11 @@ def run_ours(args, ws, rank, local):
         line["e2e"] = {"value": e2e["value"] / e2e["t"], "unit": "evals/s", "h2d_bytes_per_step": e2e["h2d"],
                        "d2h_bytes_per_step": e2e["d2h"], "step_seconds": e2e.get("steps")}
     if ws == 1 and not args.no_cpu_baseline:
-        ev, secs, cores, kind = cpu_reference_sample(w, seed, CPU_SAMPLE_T)
+        Tc = CPU_SAMPLE_T[args.config]
+        ev, secs, cores, kind, build = cpu_reference_sample(w, seed, Tc)
         line["cpu_baseline"] = {"value": ev / secs, "unit": "evals/s", "cores": cores, "kind": kind,
-                                "sample": f"smc_run K={ks[0]}..{ks[-1]} on the same spectrum at T={CPU_SAMPLE_T} "
-                                          f"(n={w.n}, workers=0), {secs:.1f} s"}
+                                "sample": f"smc_run K={ks[0]}..{ks[-1]} on the same spectrum at T={Tc} "
+                                          f"(n={w.n}, workers=0), {secs:.1f} s; build {build}"}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -29,6 +29,15 @@ REF_SOURCES = ["priors", "model", "energy", "mcmc", "smc", "spectrum", "report",
 
 COMMON = ["-O3", "-march=x86-64-v2", "-ffp-contract=off", "-fPIC", "-shared"]
 
+# Timing builds of the same reference sources (bench.py's reference arm and
+# cpu_baseline): the reference's own Release flags (proj/CMakeLists.txt:8-10,
+# :33-35: -O3 -DNDEBUG -march=native, gnu++20 with GCC's default FMA
+# contraction) for the two ISA levels a GPU box's host can have; bench.py picks
+# the one its CPU supports (the box cannot rebuild: /root/reference is absent
+# there).  The -ffp-contract=off build above stays the bit-exact parity target.
+NATIVE_VARIANTS = {"x86-64-v4": HERE / "_ref" / "libspecmc_ref_v4.so",
+                   "x86-64-v3": HERE / "_ref" / "libspecmc_ref_v3.so"}
+
 
 def _newer(out: Path, inputs) -> bool:
     if not out.exists():
@@ -60,7 +69,31 @@ def build_ref(force: bool = False) -> Path | None:
             *map(str, srcs), "-o", str(REF_SO),
         ]
         subprocess.run(cmd, check=True)
+    for march, out in NATIVE_VARIANTS.items():
+        if force or not _newer(out, srcs + [shim]):
+            cmd = ["g++", "-std=gnu++20", "-O3", "-DNDEBUG", f"-march={march}", "-fPIC", "-shared", "-pthread",
+                   f"-I{HERE / 'eigen_shim'}", f"-I{REF_ROOT / 'include'}",
+                   f'-DSPECMC_DATA_DIR="{REF_ROOT / "data"}"', *map(str, srcs), "-o", str(out)]
+            subprocess.run(cmd, check=True)
     return REF_SO
+
+
+def timing_ref_so() -> tuple[Path, str]:
+    """The reference timing build for this host's ISA (v4 needs AVX-512 F/BW/DQ/VL)."""
+    flags = set()
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("flags"):
+                flags = set(line.split(":", 1)[1].split())
+                break
+    except OSError:
+        pass
+    v4 = {"avx512f", "avx512bw", "avx512dq", "avx512vl"} <= flags
+    v3 = {"avx2", "fma", "bmi2"} <= flags
+    for march, ok in (("x86-64-v4", v4), ("x86-64-v3", v3)):
+        if ok and NATIVE_VARIANTS[march].exists():
+            return NATIVE_VARIANTS[march], march
+    return REF_SO, "x86-64-v2 (parity build)"
 
 
 if __name__ == "__main__":

@@ -670,7 +670,9 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
     // and step only change at its own proposal, so the proposal, its prior
     // check (mcmc.cpp:61-68) and the Philox draws are all fixed at sweep start.
     for (int i = lane; i < d; i += 32) {
-      const u32x4 o = philox(u32x4{cg, (uint32_t)level, (uint32_t)((t - 1) * d + i), ROLE_CHAIN}, g.key0, g.key1);
+      // counter (t-1) d + i < n d <= 2^32 (make_runspec rejects larger n d): unsigned, no wrap
+      const u32x4 o = philox(u32x4{cg, (uint32_t)level, (uint32_t)(t - 1) * (uint32_t)d + (uint32_t)i, ROLE_CHAIN},
+                             g.key0, g.key1);
       const double old_i = th[i];
       const double nv = old_i + (double)__expf((float)lsv[i]) * (double)normal_f32(o.x, o.y);
       double dlp = 0.0;

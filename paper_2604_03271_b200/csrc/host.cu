@@ -1139,6 +1139,9 @@ RunSpec make_runspec(const specmc_model_desc& m, int spectrum, const specmc_smc_
   validate_config(cfg);
   validate_model(m);
   validate_spectrum(sp.xs, sp.ys, sp.n, m.noise == SPECMC_NOISE_POISSON);
+  // the chain kernel's Philox counter (sweep - 1) d + component is 32-bit
+  if ((uint64_t)cfg.n * (uint64_t)m.d > ((uint64_t)1 << 32))
+    throw Error(SPECMC_EINVAL, "SmcConfig: n * d must not exceed 2^32 (device RNG counter range)");
   RunSpec R;
   R.m = m;
   R.spectrum = spectrum;
@@ -1467,6 +1470,56 @@ struct Scratch {
   T* alloc(size_t n) {
     bufs.emplace_back(sizeof(T) * std::max<size_t>(n, 1));
     return bufs.back().as<T>();
+  }
+};
+
+// One unsharded group holding a caller's array as its current energies, for
+// the parity units of the grid-level tempering (T > 2^15): the same slices and
+// k_tp_* launches as ClassRun::prepare / run give a production group.
+struct GridUnit {
+  Scratch sc;
+  GroupDesc* d_g = nullptr;
+  GroupState* d_st = nullptr;
+  TemperScratch* d_ts = nullptr;
+  int* d_list = nullptr;
+  int nslices = 0;
+  GroupDesc g;
+  GridUnit(const double* host_e, int64_t T, double n_data, double beta, double ess_target, int64_t S,
+           cudaStream_t st) {
+    std::memset(&g, 0, sizeof(g));
+    d_g = sc.alloc<GroupDesc>(1);
+    d_st = sc.alloc<GroupState>(1);
+    d_ts = sc.alloc<TemperScratch>(1);
+    d_list = sc.alloc<int>(1);
+    double* dE = sc.alloc<double>(T);
+    h2d(dE, host_e, T, st);
+    g.T = (int)T;
+    g.n = 1;
+    g.S = (int)S;
+    g.max_levels = 1;
+    g.ess_target = ess_target;
+    g.n_data = n_data;
+    g.E[0] = g.E[1] = dE;
+    g.wbuf = sc.alloc<double>(T);
+    g.anc = sc.alloc<int>(S);
+    g.diag = sc.alloc<double>(4);
+    g.st = d_st;
+    g.ts = d_ts;
+    size_t sl = std::max<size_t>(min_slice_len(), (T + kMaxSlices - 1) / kMaxSlices);
+    sl = (sl + 1023) & ~(size_t)1023;
+    g.slice_len = (int)sl;
+    g.nslices = nslices = (int)((T + sl - 1) / sl);
+    GroupState s;
+    std::memset(&s, 0, sizeof(s));
+    s.beta = beta;
+    s.active = 1;
+    s.T_loc = (int)T;
+    s.S_loc = (int)S;
+    h2d(d_st, &s, 1, st);
+    h2d(d_g, &g, 1, st);
+    const int zero = 0;
+    h2d(d_list, &zero, 1, st);
+    cuda_check(cudaMemsetAsync(d_ts, 0, sizeof(TemperScratch), st), "memset");
   }
 };
 
@@ -1805,6 +1858,18 @@ int specmc_next_beta(const double* E, int64_t n, double n_data, double beta_prev
     if (!E || !beta_out || n < 1) throw Error(SPECMC_EINVAL, "next_beta: empty input");
     if (!(beta_prev < 1.0)) throw Error(SPECMC_EINVAL, "next_beta: beta_prev must be < 1");
     Device dev(device);
+    if ((size_t)n > grid_temper_t()) {  // the production grid path (k_tp_emin + k_tp_ess_tree passes)
+      if (n > ((int64_t)1 << 31) - 1) throw Error(SPECMC_EINVAL, "next_beta: too many particles");
+      GridUnit gu(E, n, n_data, beta_prev, ess_target, 1, dev.stream);
+      cuda_check(launch_tp_next_beta(gu.d_g, gu.d_list, 1, gu.nslices, dev.stream), "k_tp_ess_tree");
+      count_launch(temper_grid_launches() - 4);
+      TemperScratch ts;
+      d2h(&ts, gu.d_ts, 1, dev.stream);
+      dev.sync();
+      if (ts.err) throw Error(SPECMC_ERUNTIME, "ess: total weight is zero");
+      *beta_out = ts.beta_next;
+      return SPECMC_OK;
+    }
     Scratch sc;
     double* d_E = sc.alloc<double>(n);
     double* d_out = sc.alloc<double>(1);
@@ -1828,6 +1893,26 @@ int specmc_systematic_resample(const double* lw, int64_t n, int64_t S, double u,
     if (!lw || !anc_out || n < 1 || S < 1) throw Error(SPECMC_EINVAL, "systematic_resample: empty input");
     if (n > ((int64_t)1 << 31) - 1) throw Error(SPECMC_EINVAL, "systematic_resample: too many weights");
     Device dev(device);
+    if ((size_t)n > grid_temper_t()) {
+      // the production grid path (k_tp_wmax, k_tp_wsum, k_tp_offsets, k_tp_resample) with the
+      // log-weights as energies: beta 0 -> -1 at n_data 1 gives lw_i = 1.0 * E_i exactly
+      if (S > ((int64_t)1 << 31) - 1) throw Error(SPECMC_EINVAL, "systematic_resample: too many targets");
+      GridUnit gu(lw, n, 1.0, 0.0, 0.5, S, dev.stream);
+      TemperScratch ts;
+      std::memset(&ts, 0, sizeof(ts));
+      ts.beta_next = -1.0;
+      ts.full = 1.0;
+      h2d(gu.d_ts, &ts, 1, dev.stream);
+      cuda_check(launch_tp_resample(gu.d_g, gu.d_list, 1, gu.nslices, &u, dev.stream), "k_tp_resample");
+      count_launch(5);
+      std::vector<int> a(S);
+      d2h(a.data(), gu.g.anc, S, dev.stream);
+      d2h(&ts, gu.d_ts, 1, dev.stream);
+      dev.sync();
+      if (ts.err) throw Error(SPECMC_ERUNTIME, "systematic_resample: total weight is zero");
+      for (int64_t j = 0; j < S; ++j) anc_out[j] = a[j];
+      return SPECMC_OK;
+    }
     Scratch sc;
     double* d_lw = sc.alloc<double>(n);
     double* d_w = sc.alloc<double>(n);

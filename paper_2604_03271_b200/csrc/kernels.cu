@@ -566,7 +566,12 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_ess_tree(const GroupDesc* _
   if (!slice_ctx(gds, list, c)) return;
   const GroupDesc& g = *c.g;
   TemperScratch* ts = c.ts;
-  if (ts->done || ts->err) return;
+  if (ts->done || ts->err) {
+    // a finished group still takes part in its run's exchange of this pass:
+    // it contributes zeros instead of re-summing the last pass's totals
+    if (g.sharded && blockIdx.x == 0 && threadIdx.x < 2 * S) g.xbuf[threadIdx.x] = 0.0;
+    return;
+  }
   GroupState* st = g.st;
   const bool first = ts->it < 0;
   double dl[S], lo[S], hi[S];
@@ -1104,16 +1109,36 @@ template <int D>
 static void launch_ess_pass(dim3 grid, const GroupDesc* gds, const int* list, cudaStream_t st) {
   k_tp_ess_tree<D><<<grid, kGridThreads, 0, st>>>(gds, list);
 }
-cudaError_t launch_temper_grid(const GroupDesc* gds, const int* list, int n_list, int max_slices, cudaStream_t st) {
+// the two halves of a grid-tempered level (launch_temper_grid); the parity
+// units specmc_next_beta / specmc_systematic_resample run them alone for
+// T > 2^15, i.e. exactly the production launches
+cudaError_t launch_tp_next_beta(const GroupDesc* gds, const int* list, int n_list, int max_slices, cudaStream_t st) {
   const dim3 grid(max_slices, n_list);
   k_tp_emin<<<grid, kGridThreads, 0, st>>>(gds, list);
   for (int it = 0; it < ess_launches(); ++it)
     ess_depth() == 1 ? launch_ess_pass<1>(grid, gds, list, st) : launch_ess_pass<kEssDepth>(grid, gds, list, st);
+  return cudaGetLastError();
+}
+// u_override != nullptr (parity unit): the level's uniform is the caller's, not
+// the Philox draw of fin_wsum
+__global__ void k_tp_set_u(const GroupDesc* __restrict__ gds, const int* __restrict__ list, double u) {
+  const GroupDesc& g = gds[list[blockIdx.x]];
+  if (threadIdx.x == 0) g.ts->u = u;
+}
+cudaError_t launch_tp_resample(const GroupDesc* gds, const int* list, int n_list, int max_slices,
+                               const double* u_override, cudaStream_t st) {
+  const dim3 grid(max_slices, n_list);
   k_tp_wmax<<<grid, kGridThreads, 0, st>>>(gds, list);
   k_tp_wsum<<<grid, kGridThreads, 0, st>>>(gds, list);
+  if (u_override) k_tp_set_u<<<n_list, 32, 0, st>>>(gds, list, *u_override);
   k_tp_offsets<<<grid, kGridThreads, 0, st>>>(gds, list);
   k_tp_resample<<<grid, kGridThreads, 0, st>>>(gds, list);
   return cudaGetLastError();
+}
+cudaError_t launch_temper_grid(const GroupDesc* gds, const int* list, int n_list, int max_slices, cudaStream_t st) {
+  cudaError_t e = launch_tp_next_beta(gds, list, n_list, max_slices, st);
+  if (e != cudaSuccess) return e;
+  return launch_tp_resample(gds, list, n_list, max_slices, nullptr, st);
 }
 int temper_grid_launches() { return 5 + ess_launches(); }
 

@@ -73,6 +73,12 @@ cudaError_t launch_temper(const GroupDesc* d_gds, const int* d_list, int n_list,
 // resampling + step prediction (66 launches, each over (slices x groups))
 cudaError_t launch_temper_grid(const GroupDesc* d_gds, const int* d_list, int n_list, int max_slices, cudaStream_t st);
 int temper_grid_launches();
+// its halves: emin + the ESS bisection passes (-> ts->beta_next), then weights,
+// evidence, CDF offsets and resampling (u_override: parity unit's explicit uniform)
+cudaError_t launch_tp_next_beta(const GroupDesc* d_gds, const int* d_list, int n_list, int max_slices,
+                                cudaStream_t st);
+cudaError_t launch_tp_resample(const GroupDesc* d_gds, const int* d_list, int n_list, int max_slices,
+                               const double* u_override, cudaStream_t st);
 // ---- particle sharding (shard.cu): one run's particles split over shards that
 // exchange a few scalars per tempering phase
 enum ExchangeOp : int { XOP_SUM = 0, XOP_MIN = 1, XOP_MAX = 2 };

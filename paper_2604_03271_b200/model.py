@@ -14,8 +14,6 @@ from typing import List, Union
 
 import numpy as np
 
-from . import _lib
-
 # ---------------------------------------------------------------- priors
 @dataclass(frozen=True)
 class NormalPrior:
@@ -149,6 +147,7 @@ class ModelSpec:
 
     def desc(self):
         """Flat C struct; the returned keep-alive tuple must outlive the struct."""
+        from . import _lib  # (deferred: describing a model needs no library)
         pk, pa, pb = self.arrays()
         n = self.noise
         sigma, s0, s1, s2, lit = 1.0, 1.0, 0.0, 0.0, 0
@@ -226,6 +225,27 @@ def xrd_model(phases: List[PhaseRef], data: Spectrum, noise: NoiseSpec = Poisson
     layout += [ScalarParam("bg_a", GammaPrior(2.0, 1.0 / ymax)), ScalarParam("bg_sigma", GammaPrior(2.0, 0.4)),
                ScalarParam("bg_r", UniformPrior(0.0, 1.0)), ScalarParam("bg_b", UniformPrior(ymin - half, ymin + half))]
     return ModelSpec("xrd", len(phases), layout, noise, list(phases))
+
+
+def apply_prior_overrides(spec: ModelSpec, overrides: dict) -> ModelSpec:
+    """Config-file prior overrides (config.cpp:204-222): ``prior.<name>`` by exact
+    parameter name first, then by the digit-stripped stem (``prior.eta``
+    applies to eta1..etaK); an override matching no parameter is an error."""
+    used = set()
+    layout = []
+    for p in spec.layout:
+        stem = p.name.rstrip("0123456789")
+        if p.name in overrides:
+            p = ScalarParam(p.name, overrides[p.name])
+            used.add(p.name)
+        elif stem != p.name and stem in overrides:
+            p = ScalarParam(p.name, overrides[stem])
+            used.add(stem)
+        layout.append(p)
+    unused = set(overrides) - used
+    if unused:
+        raise ValueError(f"prior override matches no parameter: prior.{sorted(unused)[0]}")
+    return ModelSpec(spec.family, spec.K, layout, spec.noise, list(spec.phases))
 
 
 def offset_model(sigma: float, m0: float = 0.0, v0: float = 4.0) -> ModelSpec:

@@ -17,8 +17,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .model import (GaussianFixedNoise, ModelSpec, PhaseRef, PoissonNoise, Reflection, Spectrum, XpsHeteroNoise,
-                    gm_model, xps_model)
+from .model import (GaussianFixedNoise, ModelSpec, PhaseRef, PoissonNoise, Reflection, Spectrum, UniformPrior,
+                    XpsHeteroNoise, apply_prior_overrides, gm_model, xps_model)
 
 _M = 0xFFFFFFFFFFFFFFFF
 
@@ -285,11 +285,16 @@ class Workload:
     n: int
     noise: object
     truth_k: int
+    prior_overrides: dict = None  # config-file prior overrides (config.cpp:204-222)
 
-    def spec(self, K: int) -> ModelSpec:
+    def spec(self, K: int, data: Spectrum | None = None) -> ModelSpec:
+        """The fitted model at K peaks (on ``data``, default the workload's spectrum)."""
+        data = self.data if data is None else data
         if self.family == "gm":
-            return gm_model(K, float(self.data.xs[0]), float(self.data.xs[-1]), self.noise.sigma, "uniform")
-        return xps_model(K, self.data, self.noise)
+            s = gm_model(K, float(data.xs[0]), float(data.xs[-1]), self.noise.sigma, "uniform")
+        else:
+            s = xps_model(K, data, self.noise)
+        return apply_prior_overrides(s, self.prior_overrides) if self.prior_overrides else s
 
 
 def config(name: str, T: int | None = None) -> Workload:
@@ -303,9 +308,12 @@ def config(name: str, T: int | None = None) -> Workload:
         data, _ = gen_xps_grid(6, 2, 2000, 5.0, 60.0, noise)
         return Workload("C2", data, "xps", (1, 10), T or 65536, 8, noise, 6)
     if name == "C3":
+        # 8 Lorentzian peaks; fitted with the xps family and the Lorentzian basis
+        # pinned by the config override prior.eta = uniform(0, 1e-9) (SURVEY.md
+        # Appendix A; config.cpp:204-222, lineshapes.hpp:51)
         noise = XpsHeteroNoise(1.0, 0.0, 0.0)
         data, _ = gen_xps_grid(8, 3, 4096, 5.0, 60.0, noise, eta_zero=True)
-        return Workload("C3", data, "xps", (1, 12), T or (1 << 22), 8, noise, 8)
+        return Workload("C3", data, "xps", (1, 12), T or (1 << 22), 8, noise, 8, {"eta": UniformPrior(0.0, 1e-9)})
     if name == "C5":
         noise = XpsHeteroNoise(1.0, 0.0, 0.0)
         data, _ = gen_xps_grid(20, 5, 8192, 5.0, 105.0, noise, margin=3.0)

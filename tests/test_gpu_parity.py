@@ -53,6 +53,17 @@ def _cases():
     xr, _ = syn.gen_xrd(600, 5)
     cases.append(("xrd3_poisson", M.xrd_model(syn.TIO2_PHASES, xr), xr))
     cases.append(("xrd3_gapprox", M.xrd_model(syn.TIO2_PHASES, xr, M.GaussianApproxPoissonNoise()), xr))
+    # the large-spectrum kernels: C3 (N = 4096, W = 4 warps per chain) and C5
+    # (N = 8192, W = 8), each on its uniform grid (weight-free Shirley scan,
+    # 4 B/point y layout) and on a jittered grid (trapezoid weights staged), at
+    # K = 1, 6 and Kmax
+    for cname in ("C3", "C5"):
+        wc = syn.config(cname)
+        xjc = np.sort(wc.data.xs + rng.uniform(-0.004, 0.004, len(wc.data.xs)))
+        wj = M.Spectrum(xjc, wc.data.ys.copy())
+        for K in (1, 6, wc.k_range[1]):
+            cases.append((f"{cname.lower()}_K{K}", wc.spec(K), wc.data))
+            cases.append((f"{cname.lower()}_K{K}_jittered", wc.spec(K, wj), wj))
     return cases
 
 
@@ -125,8 +136,11 @@ def test_next_beta_two_atom(smc):
 
 
 def test_next_beta_matches_oracle(smc, port):
+    # T <= 2^15: the single-CTA k_temper bisection; T > 2^15: the production
+    # grid path (k_tp_emin + k_tp_ess_tree passes, 3 bisection steps per pass)
+    # that C2/C3/C5 run
     rng = np.random.default_rng(1)
-    for T, nd in ((1000, 300.0), (65536, 2000.0), (4096, 301.0)):
+    for T, nd in ((1000, 300.0), (4096, 301.0), (65536, 2000.0), (1 << 18, 8192.0), (100003, 4096.0)):
         E = 5.0 + np.abs(rng.normal(size=T)) * 3
         E[::97] = np.inf
         for beta_prev in (0.0, 1e-4, 0.3):
@@ -147,7 +161,10 @@ def test_resample_exact_counts(smc, port):
 
 def test_resample_matches_oracle(smc, port):
     rng = np.random.default_rng(2)
-    for T, S in ((10, 3), (1000, 125), (65536, 8192), (100003, 777)):
+    # T > 2^15 runs the production grid path (k_tp_wmax, k_tp_wsum,
+    # k_tp_offsets, k_tp_resample: slice CDF offsets + per-slice target ranges)
+    for T, S in ((10, 3), (1000, 125), (32768, 4096), (65536, 8192), (100003, 777), (1 << 18, 1 << 15),
+                 (1 << 18, 300001)):
         lw = rng.normal(size=T) * 2
         lw[::13] = -np.inf
         u = rng.uniform()

@@ -1,0 +1,106 @@
+"""Model selection and posterior moments against the reference itself.
+
+Golden files tests/golden/selection_{C1,C2}.json hold, for 10 seeds
+trial_seed(4242, t), the reference's F per K, its per-seed selected K and
+modal K, and the posterior mean/std at the true K (peak blocks sorted by
+centre per particle); tests/golden/make_selection_golden.py made them by
+running the unchanged reference sources (oracle/_ref) through smc_run as
+cmd_model_select does (proj/tools/specmc_main.cpp:147-170).
+
+The B200 sampler runs the same K range, T, n and seeds (its own Philox
+streams: parity is statistical) and must
+
+  * select the same modal K (north_star: "the selected K is identical";
+    acceptance select_k_once / criterion 4,
+    proj/tests/acceptance/acceptance_main.cpp:227-262),
+  * match the reference's mean F per K within 4 standard errors of the
+    difference of the two 10-seed means (+ 0.05 nats),
+  * match the posterior mean of every component within 4 standard errors of
+    the seed-to-seed spread (floored at 5% of the posterior std) and the
+    posterior std within a factor 1.25.
+"""
+import json
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2604_03271_b200 import synthetic as syn
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def _canonical(th, family, K):
+    stride = 3 if family == "gm" else 4
+    out = th.copy()
+    blocks = th[:, :stride * K].reshape(len(th), K, stride)
+    order = np.argsort(blocks[:, :, 1], axis=1, kind="stable")
+    out[:, :stride * K] = np.take_along_axis(blocks, order[:, :, None], axis=1).reshape(len(th), stride * K)
+    return out
+
+
+def _load(cfg):
+    p = GOLDEN / f"selection_{cfg}.json"
+    if not p.exists():
+        pytest.skip(f"{p.name} not generated")
+    return json.loads(p.read_text())
+
+
+@pytest.fixture(scope="module", params=["C1", "C2"])
+def runs(request, smc):
+    g = _load(request.param)
+    w = syn.config(g["config"], g["T"])
+    ks = list(range(g["K_range"][0], g["K_range"][1] + 1))
+    seeds = [int(s) for s in g["seeds"]]
+    probs = [(w.spec(K), 0, smc.SmcConfig(T=g["T"], n=g["n"], ess_target=g["ess_target"], seed=s))
+             for s in seeds for K in ks]
+    reps = smc.smc_run_batch(probs, [w.data])
+    F = np.array([r.F for r in reps]).reshape(len(seeds), len(ks))
+    post = {}
+    for si in range(len(seeds)):
+        r = reps[si * len(ks) + ks.index(w.truth_k)]
+        post[si] = _canonical(np.ascontiguousarray(r.posterior.T), w.family, w.truth_k)
+    return g, w, ks, F, reps, post
+
+
+def test_selected_k_identical_to_reference(smc, runs):
+    g, w, ks, F, reps, _ = runs
+    sel = []
+    for si in range(F.shape[0]):
+        rows = [(K, reps[si * len(ks) + j]) for j, K in enumerate(ks)]
+        sel.append(smc.model_select(rows).K_best)
+    modal = max(set(sel), key=lambda k: (sel.count(k), -k))
+    assert modal == g["modal_K"] == w.truth_k, (sel, g["selected"])
+    # model_select over every seed at once (the CLI's --trials table)
+    rows = [(K, reps[si * len(ks) + j]) for si in range(F.shape[0]) for j, K in enumerate(ks)]
+    assert smc.model_select(rows).K_best == g["modal_K"]
+
+
+def test_free_energy_per_k_matches_reference(runs):
+    g, w, ks, F, _, _ = runs
+    Fr = np.array(g["F"])
+    n = F.shape[0]
+    for j, K in enumerate(ks):
+        se = math.sqrt(F[:, j].var(ddof=1) / n + Fr[:, j].var(ddof=1) / n)
+        d = abs(F[:, j].mean() - Fr[:, j].mean())
+        assert d <= 4 * se + 0.05, (g["config"], K, F[:, j].mean(), Fr[:, j].mean(), se)
+
+
+def test_posterior_moments_match_reference(runs):
+    g, w, ks, F, _, post = runs
+    m_gpu = np.array([p.mean(axis=0) for p in post.values()])
+    s_gpu = np.array([p.std(axis=0) for p in post.values()])
+    m_ref = np.array(g["posterior_mean"])
+    s_ref = np.array(g["posterior_std"])
+    n = len(m_gpu)
+    se = np.sqrt(m_gpu.var(axis=0, ddof=1) / n + m_ref.var(axis=0, ddof=1) / n)
+    floor = 0.05 * s_ref.mean(axis=0)
+    dm = np.abs(m_gpu.mean(axis=0) - m_ref.mean(axis=0))
+    assert np.all(dm <= 4 * np.maximum(se, floor)), (g["config"], np.nonzero(dm > 4 * np.maximum(se, floor))[0])
+    ratio = s_gpu.mean(axis=0) / s_ref.mean(axis=0)
+    # (components the prior pins to a point, e.g. a degenerate width, have ~0 spread on both)
+    ok = (s_ref.mean(axis=0) < 1e-12) | ((ratio > 0.8) & (ratio < 1.25))
+    assert np.all(ok), (g["config"], ratio)
