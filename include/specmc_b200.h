@@ -236,6 +236,8 @@ typedef struct {
   double move_kernel_ms;    /* CUDA-event time summed over move-kernel launches */
   int64_t move_launches;
   double point_evals;       /* trials x N summed over move launches */
+  double move_mufu_ops;     /* MUFU lane-ops the move kernel executed (shape evaluations and noise
+                               terms over the padded point slots; the SFU roofline numerator) */
 } specmc_stats;
 
 int specmc_stats_get(specmc_stats* out);

@@ -50,7 +50,7 @@ class SpectrumC(C.Structure):
 
 class StatsC(C.Structure):
     _fields_ = [("kernel_launches", C.c_int64), ("move_kernel_ms", C.c_double), ("move_launches", C.c_int64),
-                ("point_evals", C.c_double)]
+                ("point_evals", C.c_double), ("move_mufu_ops", C.c_double)]
 
 
 # every symbol include/specmc_b200.h declares (tests/test_abi.py checks the header agrees)

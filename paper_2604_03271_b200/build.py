@@ -15,7 +15,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 ROOT = PKG.parent
-LIB = PKG / "libspecmc_b200.so"
+LIB = Path(os.environ["SPECMC_OUT"]) if os.environ.get("SPECMC_OUT") else PKG / "libspecmc_b200.so"
+DEFS = os.environ.get("SPECMC_DEFS", "").split()  # -D... tuning variants (A/B builds)
 SOURCES = sorted(CSRC.glob("*.cu"))
 HEADERS = [CSRC / "device.cuh", CSRC / "chain.cuh", CSRC / "launch.h", ROOT / "include" / "specmc_b200.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -37,8 +38,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs = []
     procs = []
     for src in SOURCES:
-        obj = CSRC / (src.stem + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+        obj = CSRC / (src.stem + (".v" + str(abs(hash(tuple(DEFS)))) if DEFS else "") + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *DEFS, "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append((subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True), src))

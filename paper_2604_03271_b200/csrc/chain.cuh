@@ -9,18 +9,27 @@
 // Reference paths are relative to the reference root (proj/...).
 //
 // A chain unit is W warps (L = 32 W lanes, compile-time).  Lane l owns the PPL
-// consecutive points [l*PPL, (l+1)*PPL) of the spectrum and keeps, in
-// registers,
+// consecutive points [l*PPL, (l+1)*PPL) of the spectrum.
+//
+// Packed fp32 pairs.  The lane's points are held as PH = PPL/2 float2 "pair
+// slots": slot k pairs the lane's point k (.x, first half) with its point
+// k + PH (.y, second half).  Every per-point step of an evaluation is then one
+// sm_100 packed instruction (FFMA2 / FADD2 / FMUL2) for two independent points:
+// the two halves run as separate running sums through the Shirley scans and
+// are joined once per lane, and the paired noise terms combine slot k with
+// slot k+1 component-wise (two points of the first half and two of the second
+// half per packed instruction).  Only the MUFU ops (ex2, rcp, lg2) stay scalar.
+//
 //   P[k]  committed peak signal  sum_b g_b(x)      (combine, model.cpp:287-288)
-//   Q[k]  P minus g_b(x) of the block being swept (shared memory, lane-transposed)
+//   Q[k]  P minus g_b(x) of the block being swept (shared memory)
 // A proposal changes one block: the trial signal is Pn = Q + g_new, and an
 // amplitude proposal needs no transcendental at all (Pn = P + (A'/A - 1)(P - Q)).
 // The Shirley background (lineshapes.hpp:65-83) needs the cumulative
 // trapezoid of Pn: C_k = sum_{j<=k} c_j Pn_j - h_{k+1} Pn_k with
 // c_j = h_j + h_{j+1}, h_j = (x_j - x_{j-1})/2, i.e. a lane-local scan and one
-// warp (and cross-warp) scan per proposal.  Energy terms are O(1)-centred,
-// summed per lane in fp32 and across lanes in fp64.  Padding points replicate
-// the last real point with weight 0, so no per-point masks are needed; a
+// warp (and cross-warp) scan per proposal.  Energy terms are summed per lane in
+// fp32 and across lanes exactly (fixed point).  Padding points replicate the
+// last real point with weight 0, so no per-point masks are needed; a
 // forward/noise fault shows up as a non-finite sum (=> E = +inf, the
 // reference's rejection sentinel).
 #pragma once
@@ -36,6 +45,27 @@ __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000
 constexpr float kHalfLn2 = 0.34657359027997264f;
 constexpr float kLn2 = 0.6931471805599453f;
 
+// ---- packed fp32 pair helpers (sm_100a FFMA2 / FADD2 / FMUL2) -------------
+using f2 = float2;
+__device__ __forceinline__ f2 F2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ f2 add2(f2 a, f2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ f2 neg2(f2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ f2 ex2f2(f2 a) { return make_float2(ex2f(a.x), ex2f(a.y)); }
+__device__ __forceinline__ f2 rcpf2(f2 a) { return make_float2(rcpf(a.x), rcpf(a.y)); }
+__device__ __forceinline__ f2 lg2f2(f2 a) { return make_float2(lg2f(a.x), lg2f(a.y)); }
+__device__ __forceinline__ float comp(f2 a, int h) { return h ? a.y : a.x; }
+
+// xps with the Lorentzian basis pinned (every eta prior Uniform(0, <= 1e-7):
+// the config override prior.eta = uniform(0, 1e-9) of SURVEY.md Appendix A,
+// config.cpp:204-222): the move kernel drops the Gaussian term, whose weight
+// A eta <= 1e-7 A lies below the fp32 rounding of the signal (device-only
+// family code; the energy kernel and every other path treat it as xps)
+constexpr int FAM_XPSL = 4;
+template <int FAM>
+__host__ __device__ constexpr bool is_xps() { return FAM == FAM_XPS || FAM == FAM_XPSL; }
+
 struct BlockC {
   float mu, c1, c2, c3;
   bool ok;
@@ -43,18 +73,19 @@ struct BlockC {
 
 template <int FAM>
 __device__ __forceinline__ constexpr int block_stride() {
-  return FAM == FAM_GM ? 3 : (FAM == FAM_XPS ? 4 : (FAM == FAM_XRD ? 9 : 1));
+  return FAM == FAM_GM ? 3 : (is_xps<FAM>() ? 4 : (FAM == FAM_XRD ? 9 : 1));
 }
 
-// gm:  g = A exp(-b/2 (x-mu)^2) = c1 2^(c2 d^2)                   (model.cpp:216-220)
-// xps: g = c1 2^(-u) + 1 / (c2 (1 + u)), u = t^2, t = x/sigma - mu/sigma = fma(x, c3, mu'),
+// Block constants from the fp32 shadow p of the block's parameters:
+// gm:  g = A exp(-b/2 (x-mu)^2) = c1 2^(c2 d^2), d = x - mu             (model.cpp:216-220)
+// xps: g = c1 2^(-u) + 1 / (c2 (1 + u)), u = t^2, t = x/sigma - mu/sigma,
 //      c1 = A eta, c2 = 1 / (A (1-eta)) (the Lorentzian amplitude folded into its
-//      reciprocal: one FMUL less per point; a zero Lorentzian amplitude becomes
-//      c2 = 1e30, i.e. a contribution <= 1e-30)
+//      reciprocal; a zero Lorentzian amplitude becomes c2 = 1e30, i.e. a
+//      contribution <= 1e-30)
 //      (= A [eta exp(-ln2 d^2/s^2) + (1-eta) s^2/(s^2+d^2)], model.cpp:269-280)
 // offset: g = theta_0                              (conjugate_oracle.hpp:22-26)
 template <int FAM>
-__device__ __forceinline__ BlockC block_consts(const float* p) {  // p: fp32 shadow of the block's parameters
+__device__ __forceinline__ BlockC block_consts(const float* p) {
   BlockC c;
   c.ok = true;
   c.c3 = 0.f;
@@ -62,13 +93,13 @@ __device__ __forceinline__ BlockC block_consts(const float* p) {  // p: fp32 sha
     c.c1 = p[0];
     c.mu = p[1];
     c.c2 = p[2] * -0.72134752044448170f;  // -b/2 * log2(e)
-  } else if (FAM == FAM_XPS) {
+  } else if (is_xps<FAM>()) {
     const float A = p[0], sig = p[2], eta = p[3];
     c.ok = sig > 0.f;
     c.c3 = rcpf(sig);
     c.mu = -p[1] * c.c3;
     c.c1 = A * eta;
-    const float aL = A - c.c1;
+    const float aL = FAM == FAM_XPSL ? A : A - c.c1;
     c.c2 = aL != 0.f ? rcpf(aL) : 1e30f;
   } else {
     c.c1 = p[0];
@@ -78,17 +109,20 @@ __device__ __forceinline__ BlockC block_consts(const float* p) {  // p: fp32 sha
   return c;
 }
 
+// acc + g(x) for one pair slot (two points)
 template <int FAM>
-__device__ __forceinline__ float shape(const BlockC& b, float x) {
+__device__ __forceinline__ f2 shape_add2(const BlockC& b, f2 x, f2 acc) {
   if (FAM == FAM_GM) {
-    const float d = x - b.mu;
-    return b.c1 * ex2f(b.c2 * (d * d));
-  } else if (FAM == FAM_XPS) {
-    const float t = fmaf(x, b.c3, b.mu);
-    const float nu = t * -t;  // -u: the negation rides on the FMUL (MUFU.EX2 takes no negate)
-    return fmaf(b.c1, ex2f(nu), rcpf(fmaf(nu, -b.c2, b.c2)));
+    const f2 dx = add2(x, F2(-b.mu));  // exact near the centre (the d^2 c2 form keeps full relative precision)
+    return fma2(F2(b.c1), ex2f2(mul2(F2(b.c2), mul2(dx, dx))), acc);
+  } else if (is_xps<FAM>()) {
+    const f2 t = fma2(x, F2(b.c3), F2(b.mu));
+    const f2 nu = mul2(t, neg2(t));  // -u: the negation rides on the FMUL2 (MUFU.EX2 takes no negate)
+    const f2 r = rcpf2(fma2(nu, F2(-b.c2), F2(b.c2)));
+    if (FAM == FAM_XPSL) return add2(acc, r);
+    return add2(fma2(F2(b.c1), ex2f2(nu), acc), r);
   } else {
-    return b.c1;
+    return add2(acc, F2(b.c1));
   }
 }
 
@@ -99,17 +133,19 @@ struct Xch {  // per-unit cross-warp exchange, double-buffered by parity
 
 // Per-CTA shared memory (dynamic):
 //   [0,16)     mbarrier of the spectrum bulk copy
-//   sx  float  [PPL][L]   shifted abscissa
-//   sc  float2 [PPL][L]   (c_k, h_{k+1})
-//   sy  float2 [PPL][L]   (y_k, 1/s_k)   (20 B per point: N = 8192 fits)
+//   sx  float2 [PH][L]   shifted abscissa of the pair slots (4 B per point)
+//   sc  float4 [PH][L]   (c_a, c_b, h_a, h_b): trapezoid weights of the two points
+//                        of a slot (non-uniform xps grids only, launch layout)
+//   sy  float2 [PH][L]   (-y_a, -y_b) (kLayY4: gauss and the paired hetero models), or
+//       float4 [PH][L]   (y_a, y_b, 1/s_a, 1/s_b) (poisson)
 //   per unit: th f64, ls f64, acc i32, proposal f64, dlp f64, log u f32, flags i32,
 //             fp32 shadows of th and of the proposal  (x dpad); every warp of the
 //             unit computes and writes identical values (idempotent), one unit
 //             barrier per sweep orders the sweep-level rewrites
-//   per unit: Xch, then G float [PPL][L] (cached g_b(x) of the block being swept)
+//   per unit: Xch, then Q float2 [PH][L] (signal of every block but the swept one)
 // committed peak signal P: shared memory for W = 2 and 4 (one trial signal in
-// registers leaves the allocator room: no spills at 128 registers), registers
-// for W = 1 and 8; see chain_p_in_smem (launch.h)
+// registers leaves the allocator room), registers for W = 1 and 8; see
+// chain_p_in_smem (launch.h)
 template <int W, int PPL>
 __host__ __device__ constexpr bool p_in_smem() { return chain_p_in_smem(W, PPL); }
 
@@ -138,20 +174,20 @@ template <int PPL, int W>
 struct Unit {
   static constexpr int L = 32 * W;
   static constexpr int NPT = PPL * L;
-  const float* sx;
-  const float2* sc;
-  const float2* sy;
+  static constexpr int PH = PPL / 2;
+  const f2* sx;
+  const float4* sc;
+  const void* sy;
   int nv;      // leading real (non-padding) points of this lane
   float npad;  // padding points of this lane
-  bool tail;   // uniform xps layout: this lane's last slot holds the last real point
+  bool tail;   // uniform xps layout: this lane's last point holds the last real point
   Xch* xc;
   int lg, wiu, lane, bar_id;
   int par;
-  __device__ __forceinline__ float x(int k) const { return sx[k * L + lg]; }
-  __device__ __forceinline__ float2 c(int k) const { return sc[k * L + lg]; }
-  __device__ __forceinline__ float2 y(int k) const { return sy[k * L + lg]; }
-  // paired noise layout (nz_pairs): (y_2p, y_2p+1) per point pair p
-  __device__ __forceinline__ float2 y2(int p) const { return sy[p * L + lg]; }
+  __device__ __forceinline__ f2 x2(int k) const { return sx[k * L + lg]; }
+  __device__ __forceinline__ float4 c4(int k) const { return sc[k * L + lg]; }
+  __device__ __forceinline__ f2 y2(int k) const { return static_cast<const f2*>(sy)[k * L + lg]; }
+  __device__ __forceinline__ float4 y4(int k) const { return static_cast<const float4*>(sy)[k * L + lg]; }
   __device__ __forceinline__ void sync() const {
     if (W > 1) named_bar(bar_id, L);
   }
@@ -195,7 +231,7 @@ __device__ __forceinline__ int block_off(const GroupDesc& g, int b) {
   return FAM == FAM_XRD ? 9 * b : b * block_stride<FAM>();
 }
 
-// acc_k += sign * g_b(x_k) for block b with (fp32) parameters p.  Returns false
+// acc += sign * g_b(x) for block b with (fp32) parameters p.  Returns false
 // on an evaluation fault (model.cpp:226-258, :272-275): the block then adds nothing.
 //   xrd phase b (model.cpp:235-267): sum over its reflections of
 //     A ri [(1-r) 2^(-(2 dx/wg)^2) + r / (1 + (2 dx/wl)^2)],  c = mu_ref + d2t,
@@ -203,7 +239,8 @@ __device__ __forceinline__ int block_off(const GroupDesc& g, int b) {
 //   xrd background (model.cpp:223-234): a [(1-r) 2^(-(2x/s)^2) + r / (1 + (2x/s)^2)] + b
 template <int FAM, int PPL, int W>
 __device__ __forceinline__ bool add_block(const GroupDesc& g, int b, const float* p, const Unit<PPL, W>& u,
-                                          float (&acc)[PPL], float sign) {
+                                          f2 (&acc)[PPL / 2], float sign) {
+  constexpr int PH = PPL / 2;
   if (FAM == FAM_XRD) {
     if (b < g.K) {
       const float A = p[0], d2t = p[1], r = p[2], alpha = p[3], uu = p[4], vv = p[5], ww = p[6], ss = p[7],
@@ -224,12 +261,12 @@ __device__ __forceinline__ bool add_block(const GroupDesc& g, int b, const float
         const float amp = sign * A * rf.y;
         const float ag = amp * (1.f - r), al = amp * r;
 #pragma unroll
-        for (int k = 0; k < PPL; ++k) {
-          const float dx = u.x(k) - c;
-          const bool pos = dx >= 0.f;
-          const float tg = dx * (pos ? ig_hi : ig_lo);
-          const float tl = dx * (pos ? il_hi : il_lo);
-          acc[k] += fmaf(ag, ex2f(tg * -tg), al * rcpf(fmaf(tl, tl, 1.f)));
+        for (int k = 0; k < PH; ++k) {
+          const f2 dx = add2(u.x2(k), F2(-c));
+          const f2 tg = make_float2(dx.x * (dx.x >= 0.f ? ig_hi : ig_lo), dx.y * (dx.y >= 0.f ? ig_hi : ig_lo));
+          const f2 tl = make_float2(dx.x * (dx.x >= 0.f ? il_hi : il_lo), dx.y * (dx.y >= 0.f ? il_hi : il_lo));
+          const f2 lz = rcpf2(fma2(tl, tl, F2(1.f)));
+          acc[k] = add2(acc[k], fma2(F2(ag), ex2f2(mul2(tg, neg2(tg))), mul2(F2(al), lz)));
         }
       }
       return true;
@@ -238,18 +275,20 @@ __device__ __forceinline__ bool add_block(const GroupDesc& g, int b, const float
     const float is = 2.f / p[1];
     const float ag = sign * p[0] * (1.f - p[2]), al = sign * p[0] * p[2], off = sign * p[3];
 #pragma unroll
-    for (int k = 0; k < PPL; ++k) {
-      const float t = u.x(k) * is;
-      acc[k] += fmaf(ag, ex2f(t * -t), fmaf(al, rcpf(fmaf(t, t, 1.f)), off));
+    for (int k = 0; k < PH; ++k) {
+      const f2 t = mul2(u.x2(k), F2(is));
+      const f2 tt2 = mul2(t, t);
+      const f2 lz = rcpf2(add2(tt2, F2(1.f)));
+      acc[k] = add2(acc[k], fma2(F2(ag), ex2f2(neg2(tt2)), fma2(F2(al), lz, F2(off))));
     }
     return true;
   } else {
     BlockC c = block_consts<FAM>(p);
     if (!c.ok) return false;
-    c.c1 *= sign;                      // amplitudes: gm c1; xps c1, 1/c2 (gm c2 is the exponent)
-    if (FAM == FAM_XPS) c.c2 *= sign;
+    c.c1 *= sign;                      // amplitudes: gm c1; xps c1, 1/c2
+    if (is_xps<FAM>()) c.c2 *= sign;
 #pragma unroll
-    for (int k = 0; k < PPL; ++k) acc[k] += shape<FAM>(c, u.x(k));
+    for (int k = 0; k < PH; ++k) acc[k] = shape_add2<FAM>(c, u.x2(k), acc[k]);
     return true;
   }
 }
@@ -259,9 +298,9 @@ __device__ __forceinline__ bool add_block(const GroupDesc& g, int b, const float
 // returning false, model.cpp:272-275): any set bit means E = +inf.
 template <int FAM, int PPL, int W>
 __device__ __forceinline__ unsigned long long full_signal(const GroupDesc& g, const float* th,
-                                                          const Unit<PPL, W>& u, float (&P)[PPL]) {
+                                                          const Unit<PPL, W>& u, f2 (&P)[PPL / 2]) {
 #pragma unroll
-  for (int k = 0; k < PPL; ++k) P[k] = 0.f;
+  for (int k = 0; k < PPL / 2; ++k) P[k] = F2(0.f);
   const int nb = n_blocks<FAM>(g);
   unsigned long long fmask = 0ull;
   for (int b = 0; b < nb; ++b)
@@ -312,6 +351,7 @@ __device__ __forceinline__ double unit_sum(Unit<PPL, W>& u, float acc) {
 //   hetero:  lg2(var/s) + q' r^2/var, q' = q / (ln2/2)  E = a0 + a1 (ln2/2) sum
 //            (hlin: the same with var linear in f)
 //   poisson: f - y - y ln(f/y)                          E = a0 + a1 * sum
+// (scalar form: the padding correction and the poisson terms; yq = (y, 1/s))
 template <int NZ>
 __device__ __forceinline__ float noise_term(const GroupDesc& g, float f, float2 yq) {
   const float r = yq.x - f;
@@ -338,67 +378,104 @@ __device__ __forceinline__ float noise_term(const GroupDesc& g, float f, float2 
 // ops per point with the peak shape):
 //   lg2(va/sa) + lg2(vb/sb) = lg2((va/sa)(vb/sb)),
 //   ra^2/va + rb^2/vb = (ra^2 vb + rb^2 va) / (va vb).
-// The var <= 0 sentinel survives: the lg2 argument takes the sign of min(va, vb)
-// (NaN for a negative variance, energy.cpp:20), va vb = 0 gives inf.  Products
-// leave the fp32 range only for states whose per-point fp32 terms already
-// overflow (E >~ 1e19): those read as +inf as before.
+// The partners are slots k and k+1 of the same half (component-wise), so one
+// packed step combines two point pairs.  The var <= 0 sentinel survives: the
+// lane keeps min over the variances (NaN => E = +inf unless every variance is
+// > 0, energy.cpp:20), va vb = 0 gives inf.  Products leave the fp32 range only
+// for states whose per-point fp32 terms already overflow (E >~ 1e19): those
+// read as +inf as before.  The lg2 terms are not centred (~25 each at C2
+// counts; the host moves the per-point scales into e_a0): a lane's fp32 sum of
+// 16 of them carries ~1e-4 of rounding, ~1e-4 nats in N E.
 template <int NZ>
 __host__ __device__ constexpr bool nz_pairs() { return NZ == NZ_HETERO || NZ == NZ_HLIN || NZ == NZ_HPROP; }
+template <int NZ>
+__device__ __forceinline__ f2 nz_var2(const GroupDesc& g, f2 f) {
+  if (NZ == NZ_HETERO) return fma2(fma2(F2(g.nz_a1), f, F2(g.nz_a0)), f, F2(g.nz_a2));
+  if (NZ == NZ_HLIN) return fma2(F2(g.nz_a0), f, F2(g.nz_a2));
+  return f;  // NZ_HPROP
+}
 template <int NZ>
 __device__ __forceinline__ float nz_var(const GroupDesc& g, float f) {
   if (NZ == NZ_HETERO) return fmaf(fmaf(g.nz_a1, f, g.nz_a0), f, g.nz_a2);
   if (NZ == NZ_HLIN) return fmaf(g.nz_a0, f, g.nz_a2);
   return f;  // NZ_HPROP
 }
-// (ya, yb) = the pair's observations (host, paired layout).  The lane keeps
-// three partials: quad += (ra^2 vb + rb^2 va) / (va vb), lg += lg2(va vb),
-// mn = min over the variances; its noise sum is q' quad + lg, and NaN
-// (E = +inf) unless every variance is > 0.  The lg2 terms are not centred
-// (~25 each at C2 counts; the host moves the per-point scales into e_a0): a
-// lane's fp32 sum of 16 of them carries ~1e-4 of rounding, ~1e-4 nats in N E.
-struct PairAcc {
-  float quad, lg, mn;
+// lane partials of the noise sum: packed quadratic parts and lg2 parts (one
+// lane per half), min over the variances (paired models); the packed term sums
+// in quad (other models)
+struct NoiseAcc {
+  f2 quad, lg;
+  float mn;
 };
 template <int NZ>
-__device__ __forceinline__ void noise_pair(const GroupDesc& g, float fa, float fb, float2 yab, PairAcc& a) {
-  const float ra = yab.x - fa, rb = yab.y - fb;
-  const float va = nz_var<NZ>(g, fa), vb = nz_var<NZ>(g, fb);
+__device__ __forceinline__ void noise_quad(const GroupDesc& g, f2 fa, f2 fb, f2 ya, f2 yb, NoiseAcc& a) {
+  const f2 ra = add2(fa, ya), rb = add2(fb, yb);  // (f - y): the layout stores -y (only r^2 enters)
+  const f2 va = nz_var2<NZ>(g, fa), vb = nz_var2<NZ>(g, fb);
+  const f2 num = fma2(mul2(ra, ra), vb, mul2(mul2(rb, rb), va));
+  const f2 vv = mul2(va, vb);
+  a.quad = fma2(num, rcpf2(vv), a.quad);
+  a.lg = add2(a.lg, lg2f2(vv));
+  a.mn = fminf(a.mn, fminf(fminf(va.x, va.y), fminf(vb.x, vb.y)));  // two FMNMX3
+}
+// the odd last slot of a lane with PH odd: its two points pair with each other
+template <int NZ>
+__device__ __forceinline__ void noise_pair_h(const GroupDesc& g, f2 f, f2 y, NoiseAcc& a) {
+  const float ra = f.x + y.x, rb = f.y + y.y;  // f - y (the layout stores -y)
+  const float va = nz_var<NZ>(g, f.x), vb = nz_var<NZ>(g, f.y);
   const float num = fmaf(ra * ra, vb, (rb * rb) * va);
   const float vv = va * vb;
-  a.quad = fmaf(num, rcpf(vv), a.quad);
-  a.lg += lg2f(vv);
-  a.mn = fminf(a.mn, fminf(va, vb));  // one FMNMX3
+  a.quad.x = fmaf(num, rcpf(vv), a.quad.x);
+  a.lg.x += lg2f(vv);
+  a.mn = fminf(a.mn, fminf(va, vb));
 }
-template <int NZ>
-__device__ __forceinline__ float pair_total(const GroupDesc& g, const PairAcc& a) {
-  const float t = fmaf(g.nz_q, a.quad, a.lg);
-  return a.mn > 0.f ? t : __int_as_float(0x7fc00000);
-}
-// f(k) -> sum of the noise terms of this lane's PPL points, and (CORR) the
-// padding correction: padding points (k >= nv) replicate the lane's last point,
-// so npad copies of its term are removed at once.  Without CORR the caller
-// removes the padding terms (uniform xps layout, eval_shirley_nz).
+// f(k) -> f2 for pair slot k, called in slot order: the sum of the noise terms
+// of the lane's PPL points, and (CORR) the padding correction: padding points
+// (the lane's points >= nv) replicate the spectrum's last point, so npad copies
+// of the term at the lane's last point are removed at once.  Without CORR the
+// caller removes the padding terms (uniform xps layout, eval_shirley_uniform).
 template <int NZ, int PPL, int W, bool CORR = true, class F>
 __device__ __forceinline__ float lane_noise_sum(const GroupDesc& g, const Unit<PPL, W>& u, F&& fk) {
-  float acc = 0.f, tl = 0.f, fprev = 0.f, flast = 0.f;
-  PairAcc pa{0.f, 0.f, FLT_MAX};
+  constexpr int PH = PPL / 2;
+  NoiseAcc a{F2(0.f), F2(0.f), FLT_MAX};
+  float flast = 0.f;
+  if (nz_pairs<NZ>()) {
 #pragma unroll
-  for (int k = 0; k < PPL; ++k) {
-    const float f = fk(k);
-    if (nz_pairs<NZ>()) {
-      if (k & 1)
-        noise_pair<NZ>(g, fprev, f, u.y2(k >> 1), pa);
-      else
-        fprev = f;
-      flast = f;
-    } else {
-      tl = noise_term<NZ>(g, f, u.y(k));
-      acc += tl;
+    for (int k = 0; k + 1 < PH; k += 2) {
+      const f2 fa = fk(k), fb = fk(k + 1);
+      noise_quad<NZ>(g, fa, fb, u.y2(k), u.y2(k + 1), a);
+      flast = fb.y;
+    }
+    if (PH & 1) {
+      const f2 f = fk(PH - 1);
+      noise_pair_h<NZ>(g, f, u.y2(PH - 1), a);
+      flast = f.y;
+    }
+  } else if (NZ == NZ_GAUSS) {
+#pragma unroll
+    for (int k = 0; k < PH; ++k) {
+      const f2 f = fk(k);
+      const f2 r = add2(f, u.y2(k));  // f - y (the layout stores -y)
+      a.quad = fma2(r, r, a.quad);
+      flast = f.y;
+    }
+  } else {  // poisson: scalar terms (lg2 of the model value under y > 0 guards)
+#pragma unroll
+    for (int k = 0; k < PH; ++k) {
+      const f2 f = fk(k);
+      const float4 y = u.y4(k);  // (y_a, y_b, 1/s_a, 1/s_b)
+      a.quad.x += noise_term<NZ>(g, f.x, make_float2(y.x, y.z));
+      a.quad.y += noise_term<NZ>(g, f.y, make_float2(y.y, y.w));
+      flast = f.y;
     }
   }
-  if (nz_pairs<NZ>()) acc = pair_total<NZ>(g, pa);
+  float acc;
+  if (nz_pairs<NZ>()) {
+    const float t = fmaf(g.nz_q, a.quad.x + a.quad.y, a.lg.x + a.lg.y);
+    acc = a.mn > 0.f ? t : __int_as_float(0x7fc00000);
+  } else {
+    acc = a.quad.x + a.quad.y;
+  }
   if (!CORR) return acc;
-  if (!nz_pairs<NZ>()) return fmaf(-u.npad, tl, acc);
   if (u.npad > 0.f) acc = fmaf(-u.npad, noise_term<NZ>(g, flast, make_float2(g.y_last, g.s_last)), acc);
   return acc;
 }
@@ -410,14 +487,11 @@ __device__ __forceinline__ double finish_energy(const GroupDesc& g, double s) {
 }
 
 template <int PPL, int W, int NZ>
-__device__ __forceinline__ double eval_plain_nz(const GroupDesc& g, Unit<PPL, W>& u, const float (&Pn)[PPL]) {
+__device__ __forceinline__ double eval_plain_nz(const GroupDesc& g, Unit<PPL, W>& u, const f2 (&Pn)[PPL / 2]) {
   const float acc = lane_noise_sum<NZ>(g, u, [&](int k) { return Pn[k]; });
   return finish_energy<NZ>(g, unit_sum(u, acc));
 }
 
-// Shirley background + energy (lineshapes.hpp:65-83, model.cpp:289-292).
-// amp_bound >= max_k |P_k| (sum of |amplitudes|) decides the degenerate-signal
-// test without a max reduction unless it is inconclusive.
 // scan of the lane values v over the unit: exclusive prefix and total (every
 // lane of every warp gets the same total)
 template <int PPL, int W>
@@ -443,12 +517,15 @@ __device__ __forceinline__ void unit_scan(Unit<PPL, W>& u, float v, float& prefi
 // inconclusive degenerate-signal bound: exact max of Pn over the real points
 // of the unit (rare)
 template <int PPL, int W>
-__device__ __forceinline__ float unit_max_real(Unit<PPL, W>& u, const float (&Pn)[PPL]) {
+__device__ __forceinline__ float unit_max_real(Unit<PPL, W>& u, const f2 (&Pn)[PPL / 2]) {
+  constexpr int PH = PPL / 2;
   float mx = -FLT_MAX;
 #pragma unroll
-  for (int k = 0; k < PPL; ++k)
-    if (k < u.nv) mx = fmaxf(mx, Pn[k]);
-  if (u.tail) mx = fmaxf(mx, Pn[PPL - 1]);
+  for (int k = 0; k < PH; ++k) {
+    if (k < u.nv) mx = fmaxf(mx, Pn[k].x);
+    if (k + PH < u.nv) mx = fmaxf(mx, Pn[k].y);
+  }
+  if (u.tail) mx = fmaxf(mx, Pn[PH - 1].y);
   mx = warp_max_f(mx);
   if (W > 1) {
     u.sync();  // everyone has consumed scan[par] above
@@ -465,16 +542,19 @@ __device__ __forceinline__ float unit_max_real(Unit<PPL, W>& u, const float (&Pn
 // and D cancels in C/C_{N-1}: the scan sums Pn alone, with -P_0/2 seeded on
 // lane 0 and -P_{N-1}/2 taken off the last lane's contribution (the layout
 // keeps both endpoints at fixed slots; padding has Pn = 0, so it adds nothing
-// and all padding points of a lane share one f).  Per point: one FADD in each
-// pass and two FFMA for f, no weight loads.
+// and all padding points of a lane share one f).  Per pair slot: one FADD2 in
+// the first pass and two FFMA2 for f, no weight loads; the lane's two halves
+// run their own sums, the second starting where the first ends.
 template <int PPL, int W, int NZ>
-__device__ __forceinline__ double eval_shirley_uniform(const GroupDesc& g, Unit<PPL, W>& u, const float (&Pn)[PPL],
+__device__ __forceinline__ double eval_shirley_uniform(const GroupDesc& g, Unit<PPL, W>& u, const f2 (&Pn)[PPL / 2],
                                                        float bga, float bgb, float amp_bound) {
-  const float init = u.lg == 0 ? -0.5f * Pn[0] : 0.f;
-  float run = init;
+  constexpr int PH = PPL / 2;
+  const float init = u.lg == 0 ? -0.5f * Pn[0].x : 0.f;
+  f2 run = make_float2(init, 0.f);
 #pragma unroll
-  for (int k = 0; k < PPL; ++k) run += Pn[k];
-  const float v = u.tail ? fmaf(-0.5f, Pn[PPL - 1], run) : run;
+  for (int k = 0; k < PH; ++k) run = add2(run, Pn[k]);
+  const float lane_sum = run.x + run.y;
+  const float v = u.tail ? fmaf(-0.5f, Pn[PH - 1].y, lane_sum) : lane_sum;
   float prefix, total;
   unit_scan(u, v, prefix, total);
   const float ba = bgb - bga;
@@ -484,19 +564,22 @@ __device__ __forceinline__ double eval_shirley_uniform(const GroupDesc& g, Unit<
   float acc, fpad;
   if (!degen) {
     const float scale = ba * rcpf(total);
-    const float m = fmaf(-0.5f, scale, 1.f);
+    const f2 m = F2(fmaf(-0.5f, scale, 1.f));
     // f_k = Pn_k + a + scale (R_k - P_0/2 - Pn_k/2) = B_k + m Pn_k with the
-    // running background B_k = a + scale (R_k - P_0/2): two FFMA per point
-    float B = fmaf(scale, prefix + init, bga);
+    // running background B_k = a + scale (R_k - P_0/2): two FFMA2 per slot
+    f2 B = make_float2(fmaf(scale, prefix + init, bga), fmaf(scale, prefix + run.x, bga));
+    const f2 S = F2(scale);
     acc = lane_noise_sum<NZ, PPL, W, false>(g, u, [&](int k) {
-      B = fmaf(scale, Pn[k], B);
-      return fmaf(m, Pn[k], B);
+      B = fma2(S, Pn[k], B);
+      return fma2(m, Pn[k], B);
     });
-    fpad = u.tail ? fmaf(-scale, Pn[PPL - 1], B) : B;
+    fpad = u.tail ? fmaf(-scale, Pn[PH - 1].y, B.y) : B.y;
   } else {  // linear ramp a -> b (padding sits at x = 1e30: clamp to the last point)
     const float sl = ba * g.inv_range;
     acc = lane_noise_sum<NZ, PPL, W, false>(g, u, [&](int k) {
-      return Pn[k] + fmaf(sl, fminf(u.x(k), g.x1s) - g.x0s, bga);
+      const f2 x = u.x2(k);
+      const f2 xc = make_float2(fminf(x.x, g.x1s), fminf(x.y, g.x1s));
+      return add2(Pn[k], fma2(F2(sl), add2(xc, F2(-g.x0s)), F2(bga)));
     });
     fpad = fmaf(sl, g.x1s - g.x0s, bga);
   }
@@ -504,54 +587,61 @@ __device__ __forceinline__ double eval_shirley_uniform(const GroupDesc& g, Unit<
   return finish_energy<NZ>(g, unit_sum(u, acc));
 }
 
+// Shirley background + energy (lineshapes.hpp:65-83, model.cpp:289-292) on a
+// general grid.  amp_bound >= max_k |P_k| (sum of |amplitudes|) decides the
+// degenerate-signal test without a max reduction unless it is inconclusive.
 template <int PPL, int W, int NZ>
-__device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, W>& u, const float (&Pn)[PPL],
+__device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, W>& u, const f2 (&Pn)[PPL / 2],
                                                   float bga, float bgb, float amp_bound) {
   if (g.sh_uniform) return eval_shirley_uniform<PPL, W, NZ>(g, u, Pn, bga, bgb, amp_bound);
-  // pass 1: lane-local inclusive scan of c_k Pn_k; C_k is kept for PPL <= 16 and
-  // recomputed in pass 2 for longer lanes (register budget)
+  constexpr int PH = PPL / 2;
+  // pass 1: lane-local inclusive scan of c_k Pn_k per half; C_k is kept for
+  // PPL <= 16 and recomputed in pass 2 for longer lanes (register budget)
   constexpr bool kKeepC = PPL <= 16;
-  float Cn[kKeepC ? PPL : 1];
-  float run = 0.f;
+  f2 Cn[kKeepC ? PH : 1];
+  f2 run = F2(0.f);
 #pragma unroll
-  for (int k = 0; k < PPL; ++k) {
-    const float2 c = u.c(k);
-    run = fmaf(c.x, Pn[k], run);
-    if (kKeepC) Cn[k] = fmaf(-c.y, Pn[k], run);
+  for (int k = 0; k < PH; ++k) {
+    const float4 c = u.c4(k);  // (c_a, c_b, h_a, h_b)
+    run = fma2(make_float2(c.x, c.y), Pn[k], run);
+    if (kKeepC) Cn[k] = fma2(make_float2(-c.z, -c.w), Pn[k], run);
   }
   float prefix, total;
-  unit_scan(u, run, prefix, total);
+  unit_scan(u, run.x + run.y, prefix, total);
   const float ba = bgb - bga;
   bool degen = !(total > 1e-12f * amp_bound * g.range);
   if (degen) degen = !(total > 1e-12f * unit_max_real(u, Pn) * g.range);  // inconclusive bound
   float acc;
   if (!degen) {
     const float scale = ba * rcpf(total);
-    const float base = fmaf(scale, prefix, bga);
-    float run2 = 0.f;
+    const f2 base = make_float2(fmaf(scale, prefix, bga), fmaf(scale, prefix + run.x, bga));
+    const f2 S = F2(scale);
+    f2 run2 = F2(0.f);
     acc = lane_noise_sum<NZ>(g, u, [&](int k) {
-      float Ck;  // C_k = sum_{j<=k} c_j Pn_j - h_{k+1} Pn_k (lane-local part)
+      f2 Ck;  // C_k = sum_{j<=k} c_j Pn_j - h_{k+1} Pn_k (lane-local part of each half)
       if (kKeepC) {
         Ck = Cn[kKeepC ? k : 0];
       } else {
-        const float2 c = u.c(k);
-        run2 = fmaf(c.x, Pn[k], run2);
-        Ck = fmaf(-c.y, Pn[k], run2);
+        const float4 c = u.c4(k);
+        run2 = fma2(make_float2(c.x, c.y), Pn[k], run2);
+        Ck = fma2(make_float2(-c.z, -c.w), Pn[k], run2);
       }
-      return Pn[k] + fmaf(scale, Ck, base);
+      return add2(Pn[k], fma2(S, Ck, base));
     });
   } else {  // linear ramp a -> b
-    acc = lane_noise_sum<NZ>(g, u, [&](int k) { return Pn[k] + fmaf(ba, (u.x(k) - g.x0s) * g.inv_range, bga); });
+    acc = lane_noise_sum<NZ>(g, u, [&](int k) {
+      return add2(Pn[k], fma2(F2(ba), mul2(add2(u.x2(k), F2(-g.x0s)), F2(g.inv_range)), F2(bga)));
+    });
   }
-  // padding points (k >= nv, c = h = 0) replicate the lane's last point exactly
+  // padding points (c = h = 0) replicate the spectrum's last point exactly
   return finish_energy<NZ>(g, unit_sum(u, acc));
 }
 
 // NZ is the device noise model, or NZ_DYN to switch on g.noise per evaluation
 // (energy kernels and the offset test family: one instantiation for all noises)
 template <int FAM, int PPL, int W, int NZ>
-__device__ __forceinline__ double evaluate_nz(const GroupDesc& g, Unit<PPL, W>& u, const float (&Pn)[PPL], float bga,
-                                              float bgb, float amp_bound) {
+__device__ __forceinline__ double evaluate_nz(const GroupDesc& g, Unit<PPL, W>& u, const f2 (&Pn)[PPL / 2],
+                                              float bga, float bgb, float amp_bound) {
   if (NZ == NZ_DYN) {
     switch (g.noise) {
       case NZ_GAUSS: return evaluate_nz<FAM, PPL, W, NZ_GAUSS>(g, u, Pn, bga, bgb, amp_bound);
@@ -562,7 +652,7 @@ __device__ __forceinline__ double evaluate_nz(const GroupDesc& g, Unit<PPL, W>& 
     }
   }
   constexpr int nz = NZ == NZ_DYN ? NZ_GAUSS : NZ;  // (the NZ_DYN branch above returned)
-  if (FAM == FAM_XPS) return eval_shirley_nz<PPL, W, nz>(g, u, Pn, bga, bgb, amp_bound);
+  if (is_xps<FAM>()) return eval_shirley_nz<PPL, W, nz>(g, u, Pn, bga, bgb, amp_bound);
   return eval_plain_nz<PPL, W, nz>(g, u, Pn);
 }
 
@@ -601,7 +691,7 @@ __device__ __forceinline__ int find_group(const int* prefix, int n, int x) {
 
 template <int FAM>
 __device__ __forceinline__ float amp_sum(const GroupDesc& g, const float* thf) {
-  if (FAM != FAM_XPS) return 0.f;
+  if (!is_xps<FAM>()) return 0.f;
   float s = 0.f;
   for (int b = 0; b < g.K; ++b) s += fabsf(thf[4 * b]);
   return s;
@@ -623,16 +713,17 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
                                            const int wiu, const int lane, const GroupState* st, const int cur,
                                            const int d, const int T, double* th, double* lsv, int* acc, double* nvb,
                                            double* dlpb, float* lub, int* flg, float* thf, float* nvf,
-                                           float* gcache, float* pcache) {
+                                           f2* gcache, f2* pcache) {
   using SM = Smem<PPL, W>;
+  constexpr int PH = PPL / 2;
   constexpr int stride = block_stride<FAM>();
   const int ibg = 4 * g.K;  // xps Shirley endpoints (a, b) at ibg, ibg + 1
-  float P[PPL];
+  f2 P[PH];
   unsigned long long fmask = full_signal<FAM, PPL, W>(g, thf, u, P);
   float asum = amp_sum<FAM>(g, thf);
   double e = fmask ? dinf()
-                   : evaluate_nz<FAM, PPL, W, NZ>(g, u, P, FAM == FAM_XPS ? thf[ibg] : 0.f,
-                                           FAM == FAM_XPS ? thf[ibg + 1] : 0.f, asum);
+                   : evaluate_nz<FAM, PPL, W, NZ>(g, u, P, is_xps<FAM>() ? thf[ibg] : 0.f,
+                                           is_xps<FAM>() ? thf[ibg + 1] : 0.f, asum);
   if (ENERGY) {
     if (wiu == 0 && lane == 0) g.E[cur][c] = e;
     return;
@@ -649,16 +740,16 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
   double* En = g.E[cur ^ 1];
   // components inside a block (everything but the xps Shirley endpoints and the offset family)
   const int npeak = FAM == FAM_OFFSET ? 0 : (FAM == FAM_XRD ? g.d : stride * g.K);
-  unsigned trials = 0;
+  unsigned trials = 0, shape_evals = 0;  // shape_evals: block-entry and trial shape evaluations (MUFU count)
+  constexpr int L = SM::L;
   // Q[k] at Qs[k * L]: signal of every block except the one being swept (P - g_b)
-  float* Qs = gcache + (size_t)unit * SM::NPT + u.lg;
+  f2* Qs = gcache + (size_t)unit * (SM::NPT / 2) + u.lg;
   // committed peak signal: registers, or shared memory (Ps[k * L]) when p_in_smem<W>()
   constexpr bool kPsm = p_in_smem<W, PPL>();
-  float* Ps = pcache + (size_t)unit * SM::NPT + u.lg;
-  constexpr int L = SM::L;
+  f2* Ps = pcache + (size_t)unit * (SM::NPT / 2) + u.lg;
   if (kPsm) {
 #pragma unroll
-    for (int k = 0; k < PPL; ++k) Ps[k * L] = P[k];
+    for (int k = 0; k < PH; ++k) Ps[k * L] = P[k];
   }
 #define SMC_P(k) (kPsm ? Ps[(k) * L] : P[k])
 
@@ -692,39 +783,41 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
       const int b = bi.b, j = bi.j;
       const bool peak = i < npeak;
       if (FAM != FAM_OFFSET && peak && j == 0) {  // entering block b: Q = P - g_b(x)
-        float Qn[PPL];
+        f2 Qn[PH];
 #pragma unroll
-        for (int k = 0; k < PPL; ++k) Qn[k] = SMC_P(k);
-        if (!((fmask >> b) & 1ull)) add_block<FAM, PPL, W>(g, b, thf + bi.off, u, Qn, -1.f);
+        for (int k = 0; k < PH; ++k) Qn[k] = SMC_P(k);
+        if (!((fmask >> b) & 1ull)) {
+          add_block<FAM, PPL, W>(g, b, thf + bi.off, u, Qn, -1.f);
+          ++shape_evals;
+        }
 #pragma unroll
-        for (int k = 0; k < PPL; ++k) Qs[k * L] = Qn[k];
+        for (int k = 0; k < PH; ++k) Qs[k * L] = Qn[k];
       }
       if (!(flg[i] & 1)) continue;  // outside the prior support: no trial (mcmc.cpp:68)
       const float oldf = thf[i], newf = nvf[i];
       // ---- trial signal Pn = P + (g_new - G) (the reference's BlockEvaluator::trial, energy.cpp:57-84)
-      float Pn[PPL];
+      f2 Pn[PH];
       unsigned long long fnew = fmask;
       float dA = 0.f;
       // Shirley endpoint: enters combine() only (block -1), the peak signal is
       // unchanged and (registers) evaluated in place: no copy, no commit
-      const bool endpoint = FAM == FAM_XPS && !peak;  // (gm, xrd: every component is in a block)
+      const bool endpoint = is_xps<FAM>() && !peak;  // (gm, xrd: every component is in a block)
       if (FAM == FAM_OFFSET) {
-        const float dv = newf - oldf;
+        const f2 dv = F2(newf - oldf);
 #pragma unroll
-        for (int k = 0; k < PPL; ++k) Pn[k] = SMC_P(k) + dv;
+        for (int k = 0; k < PH; ++k) Pn[k] = add2(SMC_P(k), dv);
       } else if (endpoint) {
         if (kPsm) {
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) Pn[k] = SMC_P(k);
+          for (int k = 0; k < PH; ++k) Pn[k] = SMC_P(k);
         }
       } else if (j == 0 && oldf != 0.f && !((fmask >> b) & 1ull) &&
                  (FAM != FAM_XRD || b < g.K)) {  // amplitude: g' = (A'/A) g
+        // Pn = P + r (P - Q) = (1 + r) P - r Q, r = A'/A - 1
         const float r = (newf - oldf) * rcpf(oldf);
+        const f2 r1 = F2(1.f + r), mr = F2(-r);
 #pragma unroll
-        for (int k = 0; k < PPL; ++k) {
-          const float pk = SMC_P(k);
-          Pn[k] = fmaf(r, pk - Qs[k * L], pk);
-        }
+        for (int k = 0; k < PH; ++k) Pn[k] = fma2(mr, Qs[k * L], mul2(r1, SMC_P(k)));
         dA = fabsf(newf) - fabsf(oldf);
       } else {
         constexpr int kMaxNp = FAM == FAM_XRD ? 9 : block_stride<FAM>();
@@ -732,15 +825,16 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
 #pragma unroll
         for (int q = 0; q < kMaxNp; ++q) pn[q] = (q == j) ? newf : (q < bi.np ? thf[bi.off + q] : 0.f);
 #pragma unroll
-        for (int k = 0; k < PPL; ++k) Pn[k] = Qs[k * L];
+        for (int k = 0; k < PH; ++k) Pn[k] = Qs[k * L];
         if (add_block<FAM, PPL, W>(g, b, pn, u, Pn, 1.f))
           fnew &= ~(1ull << b);
         else
           fnew |= 1ull << b;
         if (j == 0) dA = fabsf(newf) - fabsf(oldf);
+        ++shape_evals;
       }
       float bga = 0.f, bgb = 0.f;
-      if (FAM == FAM_XPS) {
+      if (is_xps<FAM>()) {
         bga = i == ibg ? newf : thf[ibg];
         bgb = i == ibg + 1 ? newf : thf[ibg + 1];
       }
@@ -769,12 +863,12 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
       // commit: Q (other blocks) is unchanged; P updated in place (select) or in shared memory
       if (!kPsm && !endpoint) {
 #pragma unroll
-        for (int k = 0; k < PPL; ++k) P[k] = accept ? Pn[k] : P[k];
+        for (int k = 0; k < PH; ++k) P[k] = accept ? Pn[k] : P[k];
       }
       if (accept) {
         if (kPsm && !endpoint) {
 #pragma unroll
-          for (int k = 0; k < PPL; ++k) Ps[k * L] = Pn[k];
+          for (int k = 0; k < PH; ++k) Ps[k * L] = Pn[k];
         }
         fmask = fnew;
         asum += dA;
@@ -817,8 +911,13 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
     }
   }
 #undef SMC_P
+  // trials: each lane counted its own components; shape_evals: every lane
+  // walked the same proposals (lane 0 of warp 0 reports)
   trials = __reduce_add_sync(0xffffffffu, trials);
-  if (wiu == 0 && lane == 0) atomicAdd(&g.st->trials, (unsigned long long)trials);
+  if (wiu == 0 && lane == 0) {
+    atomicAdd(&g.st->trials, (unsigned long long)trials);
+    atomicAdd(&g.st->shape_evals, (unsigned long long)shape_evals);
+  }
 }
 
 template <int FAM, int PPL, int W, bool ENERGY, int NZ>
@@ -839,9 +938,9 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   const int cta_in_group = blockIdx.x - cta_prefix[gi];
 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  float* sx = reinterpret_cast<float*>(smem + SM::off_x);
-  float2* sc = reinterpret_cast<float2*>(smem + SM::off_c);
-  float2* sy = reinterpret_cast<float2*>(smem + SM::off_y(lay));
+  f2* sx = reinterpret_cast<f2*>(smem + SM::off_x);
+  float4* sc = reinterpret_cast<float4*>(smem + SM::off_c);
+  void* sy = reinterpret_cast<void*>(smem + SM::off_y(lay));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int unit = warp / W, wiu = warp - unit * W;
   unsigned char* wb = smem + SM::off_w(lay) + (size_t)unit * SM::per_unit(dpad);
@@ -856,15 +955,15 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   float* nvf = thf + dpad;                            // fp32 shadow of the proposals
   const size_t xoff = ((SM::off_w(lay) + (size_t)U * SM::per_unit(dpad)) + 15) & ~(size_t)15;
   Xch* xcs = reinterpret_cast<Xch*>(smem + xoff);
-  float* gcache = reinterpret_cast<float*>(smem + xoff + (size_t)U * sizeof(Xch));
-  float* pcache = gcache + (size_t)U * SM::NPT;
+  f2* gcache = reinterpret_cast<f2*>(smem + xoff + (size_t)U * sizeof(Xch));
+  f2* pcache = gcache + (size_t)U * (SM::NPT / 2);
 
   // ---- stage the spectrum: cp.async.bulk (UBLKCP) completing on an mbarrier
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     const uint32_t bx = SM::NPT * 4u, bc = SM::NPT * 8u, by = SM::NPT * (uint32_t)SM::y_bytes(lay);
     // trapezoid weights: non-uniform grids only (the launch layout stages them then)
-    const bool wc = FAM == FAM_XPS && !g.sh_uniform && (SM::layout(lay) & kLayWeights);
+    const bool wc = is_xps<FAM>() && !g.sh_uniform && (SM::layout(lay) & kLayWeights);
     mbar_expect_tx(bar, bx + (wc ? bc : 0u) + by);
     bulk_g2s(sx, g.spec_x, bx, bar);
     if (wc) bulk_g2s(sc, g.spec_c, bc, bar);
@@ -887,7 +986,7 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   u.lane = lane;
   u.bar_id = 1 + unit;
   u.par = 0;
-  if (FAM == FAM_XPS && g.sh_uniform) {  // points 0..N-2 lead, point N-1 in the last slot
+  if (is_xps<FAM>() && g.sh_uniform) {  // points 0..N-2 lead, point N-1 in the last slot
     u.nv = min(max(g.N - 1 - u.lg * PPL, 0), PPL);
     u.tail = u.lg == Unit<PPL, W>::L - 1;
     u.npad = (float)(PPL - u.nv - (u.tail ? 1 : 0));

@@ -10,10 +10,11 @@
 //   wbuf       fp64 [T]           normalised weights (CDF scan input)
 //   hist       fp64 [5][1+2d]     step-size history ring (beta, acc[d], step[d])
 //   diag       fp64 [max_levels][4] (beta, ess_ratio, log_mean_w, acc_rate)
-// The observed spectrum is prepared on the host per launch shape as two
-// arrays in lane-transposed order (point p = lane * PPL + k stored at
-// k * L + lane, L = 32 * W lanes per chain) so that the per-point shared
-// memory reads of a warp are conflict-free.
+// The observed spectrum is prepared on the host per launch shape in
+// lane-transposed pair-slot order: lane l's points l*PPL + k and
+// l*PPL + k + PPL/2 share slot k, stored at [k * L + l] (L = 32 W lanes per
+// chain; chain.cuh), so a warp's shared-memory reads of a slot are
+// conflict-free 8- or 16-byte accesses.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -42,6 +43,7 @@ struct GroupState {  // mutable per-group scalars; read back by the host every r
   int S_loc;     // chains of the current level held by this group
   int chain_lo;  // global index of its first chain (Philox stream: chain_base + chain_lo + c)
   unsigned long long trials;
+  unsigned long long shape_evals;  // move kernel: block shape evaluations (block entries + non-amplitude trials)
 };
 
 // Grid-level tempering state of one group (multi-CTA path, k_tp_*): the

@@ -49,7 +49,7 @@ inline void cuda_check(cudaError_t e, const char* what) {
 
 // ------------------------------------------------------------ instrumentation
 std::mutex g_stats_mu;
-specmc_stats g_stats{0, 0.0, 0, 0.0};
+specmc_stats g_stats{0, 0.0, 0, 0.0, 0.0};
 
 void count_launch(int64_t n = 1) {
   std::lock_guard<std::mutex> lk(g_stats_mu);
@@ -409,6 +409,14 @@ int dev_noise(const specmc_model_desc& m) {
   }
 }
 
+struct RunSpec;
+// MUFU lane-ops per point slot of one block shape evaluation (move kernel):
+// gm ex2, xps ex2 + rcp, Lorentzian rcp, xrd (ex2 + rcp) per reflection
+double mufu_per_shape(int kfam, const RunSpec& R);
+// ... and of one evaluation's noise terms: the paired hetero models share one
+// rcp and one lg2 per two points, poisson one lg2, gauss none
+double mufu_per_noise(int nz) { return nz == NZ_GAUSS ? 0.0 : 1.0; }
+
 PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, const double* ys, int64_t N,
                                   const Shape& s, double x_shift) {
   PreparedSpectrum ps;
@@ -499,22 +507,27 @@ PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, 
     if (ps.uniform) return p + 1 < (size_t)N ? (int64_t)p : N - 1;
     return p < (size_t)N ? (int64_t)p : N - 1;
   };
+  // pair-slot layout (chain.cuh): lane point k of lane l sits in slot
+  // k mod PH, component k / PH; x float2, weights float4 (c_a, c_b, h_a, h_b),
+  // y float2 (-y_a, -y_b) or, for poisson, float4 (y_a, y_b, 1/s_a, 1/s_b)
+  const int PH = s.PPL / 2;
+  const bool y4 = ps.nz != NZ_POISSON;
   for (size_t p = 0; p < npt; ++p) {
     const int64_t q = src(p);
     const bool real = ps.uniform ? (p + 1 < (size_t)N || p + 1 == npt) : p < (size_t)N;
     const int lane = (int)(p / s.PPL), k = (int)(p % s.PPL);
-    const size_t idx = (size_t)k * L + lane;
+    const int slot = k % PH, h = k / PH;
+    const size_t sidx = (size_t)slot * L + lane;
     const double hk = q > 0 ? 0.5 * (xs[q] - xs[q - 1]) : 0.0;
     const double hk1 = q + 1 < N ? 0.5 * (xs[q + 1] - xs[q]) : 0.0;
-    ps.x[idx] = (ps.uniform && !real) ? 1e30f : (float)(xs[q] - x_shift);
-    ps.c[2 * idx] = real ? (float)(hk + hk1) : 0.f;
-    ps.c[2 * idx + 1] = real ? (float)hk1 : 0.f;
-    if (paired) {  // (y_2p, y_2p+1) at pair slot (k/2) * L + lane
-      const size_t pidx = (size_t)(k >> 1) * L + lane;
-      ps.y[2 * pidx + (k & 1)] = (float)ys[q];
+    ps.x[2 * sidx + h] = (ps.uniform && !real) ? 1e30f : (float)(xs[q] - x_shift);
+    ps.c[4 * sidx + h] = real ? (float)(hk + hk1) : 0.f;
+    ps.c[4 * sidx + 2 + h] = real ? (float)hk1 : 0.f;
+    if (y4) {  // negated: the kernel forms f - y with one FADD2 (only (f - y)^2 enters)
+      ps.y[2 * sidx + h] = (float)-ys[q];
     } else {
-      ps.y[2 * idx] = (float)ys[q];
-      ps.y[2 * idx + 1] = (float)inv_s[q];
+      ps.y[4 * sidx + h] = (float)ys[q];
+      ps.y[4 * sidx + 2 + h] = (float)inv_s[q];
     }
   }
   ps.y_last = (float)ys[N - 1];
@@ -524,13 +537,12 @@ PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, 
 
 // shared-memory spectrum layout of a class (launch.h kLay*): the trapezoid
 // weights only when an xps spectrum of the class is on a non-uniform grid, y
-// at 4 B/point for the paired noise models
+// at 4 B/point for every noise model but poisson
 template <class M>
 int spectrum_layout(int family, int noise, const M& prep) {
   bool weights = false;
   for (const auto& kv : prep) weights = weights || (family == SPECMC_FAMILY_XPS && !kv.second.uniform);
-  const bool paired = noise == NZ_HETERO || noise == NZ_HLIN || noise == NZ_HPROP;
-  return (weights ? kLayWeights : 0) | (paired ? kLayY4 : 0);
+  return (weights ? kLayWeights : 0) | (noise != NZ_POISSON ? kLayY4 : 0);
 }
 
 double pick_shift(const specmc_model_desc& m, const double* xs, int64_t N) {
@@ -557,6 +569,29 @@ struct RunSpec {
   int64_t T_loc0 = 0, pbase = 0;
   int problem = 0;  // index of the run in the caller's batch
 };
+
+// kernel family of a run: the model family, or kFamXpsLorentz for an xps
+// model whose every eta prior is Uniform(lo >= 0, hi <= 1e-7) -- the Lorentzian
+// basis of SURVEY.md Appendix A (prior.eta = uniform(0, 1e-9), config.cpp:204-222)
+int kernel_family(const RunSpec& R) {
+  const auto& m = R.m;
+  if (m.family != SPECMC_FAMILY_XPS || m.K < 1) return m.family;
+  for (int k = 0; k < m.K; ++k) {
+    const int i = 4 * k + 3;
+    if (R.pk[i] != SPECMC_PRIOR_UNIFORM || !(R.pa[i] >= 0.0) || !(R.pb[i] <= 1e-7)) return m.family;
+  }
+  return kFamXpsLorentz;
+}
+
+double mufu_per_shape(int kfam, const RunSpec& R) {
+  switch (kfam) {
+    case SPECMC_FAMILY_GM: return 1.0;
+    case SPECMC_FAMILY_XPS: return 2.0;
+    case kFamXpsLorentz: return 1.0;
+    case SPECMC_FAMILY_XRD: return R.m.K > 0 ? 2.0 * (double)(R.refl.size() / 2) / (double)R.m.K : 2.0;
+    default: return 0.0;
+  }
+}
 
 using SpecKey = std::tuple<int, double, int, int, double, double, double, double, int>;
 SpecKey spec_key(const RunSpec& R) {
@@ -613,6 +648,8 @@ struct ClassRun {
   std::vector<int> idx;  // indices into the session's runs
   Shape shape{};
   int dmax = 1, Tmax = 0, family = 0, noise = 0, G = 0;
+  int kfam = 0;                     // kernel family of the move kernel (kernel_family)
+  std::vector<double> mufu_shape;   // per group: MUFU lane-ops per slot of one shape evaluation
   Arena ar;
   GroupDesc* d_gds = nullptr;
   GroupState* d_st = nullptr;
@@ -752,6 +789,7 @@ struct ClassRun {
   void prepare(Device& dev, const std::vector<RunSpec>& runs, const std::vector<specmc_spectrum>& spectra) {
     G = (int)idx.size();
     family = runs[idx[0]].m.family;
+    kfam = kernel_family(runs[idx[0]]);
     noise = dev_noise(runs[idx[0]].m);
     int64_t Nmax = 0;
     for (int r : idx) {
@@ -765,7 +803,7 @@ struct ClassRun {
     if (chain_smem_bytes(shape, dmax) > kChainSmemMax)
       throw Error(SPECMC_EINVAL, "model too large for the device path (shared memory)");
     // module load of this class's kernels happens here, outside the timed level loop
-    cuda_check(prime_level_kernels(family, noise, shape, dmax), "loading the level kernels");
+    cuda_check(prime_level_kernels(kfam, noise, shape, dmax), "loading the level kernels");
 
     // one prepared copy per (spectrum, shift, noise parameters): the inverse
     // noise scales and the centring constants depend on the noise model
@@ -825,6 +863,8 @@ struct ClassRun {
     }
     gds.resize(G);
     runs_T0.resize(G);
+    mufu_shape.resize(G);
+    for (int gi = 0; gi < G; ++gi) mufu_shape[gi] = mufu_per_shape(kfam, runs[idx[gi]]);
     out_shift.resize(G);
     for (int gi = 0; gi < G; ++gi) {
       const RunSpec& R = runs[idx[gi]];
@@ -1001,7 +1041,7 @@ struct ClassRun {
       h2d(d_prefix, h_list + (G + 1), na + 1, st);
       cuda_check(cudaEventRecord(mv.a, st), "event");
       if (total > 0)
-        cuda_check(launch_move(family, noise, shape, dmax, d_gds, d_list, d_prefix, na, total, st), "k_chain<move>");
+        cuda_check(launch_move(kfam, noise, shape, dmax, d_gds, d_list, d_prefix, na, total, st), "k_chain<move>");
       cuda_check(cudaEventRecord(mv.b, st), "event");
       cuda_check(launch_stats_sharded(d_gds, d_list, na, dmax, *xch, st), "k_stats (sharded)");
       count_launch(4);
@@ -1037,7 +1077,7 @@ struct ClassRun {
         count_launch(temper_grid_launches());
       }
       cuda_check(cudaEventRecord(mv.a, st), "event");
-      cuda_check(launch_move(family, noise, shape, dmax, d_gds, d_list, d_prefix, na, total, st), "k_chain<move>");
+      cuda_check(launch_move(kfam, noise, shape, dmax, d_gds, d_list, d_prefix, na, total, st), "k_chain<move>");
       cuda_check(cudaEventRecord(mv.b, st), "event");
       cuda_check(launch_stats_grid(d_gds, d_list, na, dmax, st), "k_stats_grid");
       count_launch(3);
@@ -1061,9 +1101,14 @@ struct ClassRun {
     std::lock_guard<std::mutex> lk(g_stats_mu);
     g_stats.move_kernel_ms += move_ms;
     g_stats.move_launches += move_launches;
-    double pe = 0.0;
-    for (int gi = 0; gi < G; ++gi) pe += (double)h_st[gi].trials * (double)gds[gi].N;
+    double pe = 0.0, mo = 0.0;
+    const double slots = (double)shape.PPL * 32.0 * shape.W;  // every lane evaluates its padded slots
+    for (int gi = 0; gi < G; ++gi) {
+      pe += (double)h_st[gi].trials * (double)gds[gi].N;
+      mo += slots * ((double)h_st[gi].shape_evals * mufu_shape[gi] + (double)h_st[gi].trials * mufu_per_noise(noise));
+    }
     g_stats.point_evals += pe;
+    g_stats.move_mufu_ops += mo;
   }
 
   // D2H of diagnostics, posterior and energies (report fields of smc.cpp:221-247)
@@ -1205,7 +1250,7 @@ struct Session {
     std::map<std::tuple<int, int, int>, std::vector<int>> cls;
     for (int i = 0; i < n_problems; ++i) {
       const Shape s = pick_shape(runs[i].N, runs[i].m.d);
-      cls[{runs[i].m.family, dev_noise(runs[i].m), s.W * 100 + s.PPL}].push_back(i);
+      cls[{kernel_family(runs[i]), dev_noise(runs[i].m), s.W * 100 + s.PPL}].push_back(i);
     }
     for (auto& kv : cls) {
       classes.push_back(std::make_unique<ClassRun>());
@@ -1391,7 +1436,7 @@ int run_sharded_batch(int n_problems, const specmc_problem* problems, int n_spec
   std::map<std::tuple<int, int, int>, std::vector<int>> cls;
   for (int i = 0; i < (int)runs.size(); ++i) {
     const Shape s = pick_shape(runs[i].N, runs[i].m.d);
-    cls[{runs[i].m.family, dev_noise(runs[i].m), s.W * 100 + s.PPL}].push_back(i);
+    cls[{kernel_family(runs[i]), dev_noise(runs[i].m), s.W * 100 + s.PPL}].push_back(i);
   }
   std::vector<specmc_smc_result> res(runs.size());
   for (auto& r : res) std::memset(&r, 0, sizeof(r));
@@ -1976,7 +2021,7 @@ int specmc_stats_get(specmc_stats* out) {
 
 void specmc_stats_reset(void) {
   std::lock_guard<std::mutex> lk(g_stats_mu);
-  g_stats = specmc_stats{0, 0.0, 0, 0.0};
+  g_stats = specmc_stats{0, 0.0, 0, 0.0, 0.0};
 }
 
 int specmc_launch_shape(int64_t n_points, int32_t* W, int32_t* PPL, int32_t* U) {

@@ -1043,6 +1043,7 @@ cudaError_t launch_move(int family, int noise, const Shape& s, int dmax, const G
   switch (family) {
     case FAM_GM: SMC_MOVE_NZ(gm)
     case FAM_XPS: SMC_MOVE_NZ(xps)
+    case FAM_XPSL: SMC_MOVE_NZ(xpsl)
     case FAM_XRD: SMC_MOVE_NZ(xrd)
     case FAM_OFFSET: return launch_chain_offset_move_dyn(s, dmax, gds, list, prefix, n_list, total_ctas, st);
   }
@@ -1056,7 +1057,7 @@ cudaError_t launch_move(int family, int noise, const Shape& s, int dmax, const G
 // that first-launch loading is paid when a session is prepared and not inside
 // its timed level loop (CUDA_MODULE_LOADING=LAZY is the runtime default).
 cudaError_t prime_level_kernels(int family, int noise, const Shape& s, int dmax) {
-  cudaError_t e = launch_energy(family, s, dmax, nullptr, nullptr, nullptr, 0, 0, nullptr);
+  cudaError_t e = launch_energy(family == FAM_XPSL ? FAM_XPS : family, s, dmax, nullptr, nullptr, nullptr, 0, 0, nullptr);
   if (e != cudaSuccess) return e;
   e = launch_move(family, noise, s, dmax, nullptr, nullptr, nullptr, 0, 0, nullptr);
   if (e != cudaSuccess) return e;

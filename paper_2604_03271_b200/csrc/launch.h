@@ -12,12 +12,17 @@ namespace smc {
 // points in registers, U units share one CTA (and its staged spectrum).
 // Spectrum layout in the chain kernels' shared memory (bit flags): bit 0 = the
 // trapezoid weights are staged (xps on a non-uniform grid), bit 1 = y at 4 B
-// per point (paired noise models).  W <= 2 kernels use the fixed full layout
+// per point (every noise model but poisson).  W <= 2 kernels use the fixed full layout
 // (weights + 8 B y: 20 B/point, compile-time offsets); W >= 4 kernels size
 // it per launch, which halves the footprint of the large spectra (C3, C5) and
 // lets two CTAs share an SM.
 constexpr int kLayWeights = 1, kLayY4 = 2, kLayFull = kLayWeights;
-__host__ __device__ constexpr bool chain_dyn_layout(int W) { return W >= 4; }
+// units per CTA of the W = 2 kernels (N <= 2048): 8 (512 threads) or 10 (640
+// threads; needs the per-launch layout to fit the units' caches)
+#ifndef SPECMC_W2_UNITS
+#define SPECMC_W2_UNITS 8
+#endif
+__host__ __device__ constexpr bool chain_dyn_layout(int W) { return W >= 4 || (W == 2 && SPECMC_W2_UNITS > 8); }
 
 struct Shape {
   int W;
@@ -29,7 +34,7 @@ struct Shape {
 // chain-kernel CTA size per unit width W (units per CTA = threads / 32 W):
 // W = 2 runs 8 units per 512-thread CTA, one CTA per SM, so the spectrum is
 // staged once per SM and the 8 units' P and Q caches fit in shared memory
-__host__ __device__ constexpr int chain_threads(int W) { return W >= 8 ? 32 * W : (W == 2 ? 512 : 256); }
+__host__ __device__ constexpr int chain_threads(int W) { return W >= 8 ? 32 * W : (W == 2 ? 64 * SPECMC_W2_UNITS : 256); }
 // (and W = 1 with wide lanes, PPL >= 20: 512 < N <= 1024)
 __host__ __device__ constexpr bool chain_p_in_smem(int W, int PPL) { return W == 2 || W == 4 || (W == 1 && PPL >= 20); }
 
@@ -60,11 +65,14 @@ SMC_DECL_CHAIN(launch_chain_offset_move_dyn)
   SMC_DECL_CHAIN(launch_chain_##FAM##_move_hprop)
 SMC_DECL_MOVE(gm)
 SMC_DECL_MOVE(xps)
+SMC_DECL_MOVE(xpsl)
 SMC_DECL_MOVE(xrd)
 #undef SMC_DECL_MOVE
 #undef SMC_DECL_CHAIN
 // fused waste-free chain move (wastefree_level chain loop x cw_mh_sweep, smc.cpp:142-156, mcmc.cpp:55-96)
-// (one instantiation per family x device noise model, NoiseDev in device.cuh)
+// (one instantiation per kernel family x device noise model, NoiseDev in device.cuh; kernel
+// family = the model family, or kFamXpsLorentz for xps with the Lorentzian basis pinned)
+constexpr int kFamXpsLorentz = 4;  // == FAM_XPSL (chain.cuh)
 cudaError_t launch_move(int family, int noise, const Shape& s, int dmax, const GroupDesc* d_gds, const int* d_list,
                         const int* d_cta_prefix, int n_list, int total_ctas, cudaStream_t st);
 // next_beta + weights + evidence + systematic resampling + predict_step_size (one CTA per group)

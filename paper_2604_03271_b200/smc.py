@@ -455,7 +455,7 @@ def stats():
     s = _lib.StatsC()
     lib.specmc_stats_get(C.byref(s))
     return {"kernel_launches": s.kernel_launches, "move_kernel_ms": s.move_kernel_ms,
-            "move_launches": s.move_launches, "point_evals": s.point_evals}
+            "move_launches": s.move_launches, "point_evals": s.point_evals, "move_mufu_ops": s.move_mufu_ops}
 
 
 def stats_reset():

@@ -15,10 +15,12 @@ for r in range(reps):
         for line in out.splitlines():
             if line.startswith("{"):
                 d = json.loads(line)
-                res.setdefault((lib, d["cfg"]), []).append((d["dev"], d["pt_evals_per_s_move"] / 1e9))
+                res.setdefault((lib, d["cfg"]), []).append((d["dev"], d["pt_evals_per_s_move"] / 1e9,
+                                                            d.get("mufu_ops_per_s", 0.0) / 1e9))
             elif line.startswith("clocks"):
                 print(lib, line, flush=True)
 for (lib, cfg), v in sorted(res.items(), key=lambda kv: (kv[0][1], kv[0][0])):
     devs = sorted(x[0] for x in v); pe = sorted(x[1] for x in v)
+    mu = sorted(x[2] for x in v)
     print(f"{cfg:4s} {lib:45s} dev_med={devs[len(devs)//2]:.3f} dev_min={devs[0]:.3f}  Gpe/s_med={pe[len(pe)//2]:.1f} max={pe[-1]:.1f}"
-          f"  reps={[round(x[1] / 1e0, 1) for x in v]}")
+          f"  mufu_Gop/s_med={mu[len(mu)//2]:.0f}  reps={[round(x[1] / 1e0, 1) for x in v]}")

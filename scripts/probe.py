@@ -23,6 +23,7 @@ def run(name, T=None, kmax=None, seed=7):
                K_best=choice.K_best, proposals=props, trials=trials,
                evals_per_s=props / reps[0].device_seconds, move_ms=round(st["move_kernel_ms"], 1),
                pt_evals_per_s_move=st["point_evals"] / (st["move_kernel_ms"] * 1e-3),
+               mufu_ops_per_s=st.get("move_mufu_ops", 0.0) / (st["move_kernel_ms"] * 1e-3),
                launches=st["kernel_launches"])
     print(json.dumps(out), flush=True)
 
