@@ -190,6 +190,28 @@ int specmc_comm_init_nccl(int32_t rank, int32_t world, const uint8_t* id, int32_
                           char* err, size_t errlen);
 void specmc_comm_destroy(specmc_comm* c);
 
+/* ---- multi-GPU model selection ------------------
+ * The reference runs the K range of a model selection serially
+ * (cmd_model_select, proj/tools/specmc_main.cpp:147-170).  Here one batch of
+ * runs (e.g. every K) is split over the ranks of comm (one GPU each):
+ * cost-aware placement (specmc_plan), runs larger than a rank's share
+ * particle-sharded over an aligned block of ranks (sub-communicators split
+ * from comm with ncclCommSplit and cached in it), everything else one batch per
+ * rank; then one all-reduce of the per-run scalars.  Every rank passes the
+ * same problem list.  out[i] on every rank: status, F, diverged, levels, d,
+ * proposals, trials (summed over shards), device_seconds (CUDA events around
+ * this rank's whole call); posterior/energies/diagnostics only on the ranks
+ * that ran run i (a shard's particles for a sharded run), NULL elsewhere.
+ * plan_rank0 / plan_shards (optional, n_problems each): the placement. */
+int specmc_smc_run_distributed(int32_t n_problems, const specmc_problem* problems, int32_t n_spectra,
+                               const specmc_spectrum* spectra, specmc_comm* comm, int32_t* plan_rank0,
+                               int32_t* plan_shards, specmc_smc_result* out, char* err, size_t errlen);
+/* The placement alone (host only, no device): costs[i] (T d N for the
+ * distributed entry), T[i] and n[i] (shards keep whole chains) on `world`
+ * ranks -> first rank and shard count per run, per-rank load, max load. */
+int specmc_plan(int32_t n_runs, const double* costs, const int64_t* T, const int32_t* n_sweeps, int32_t world,
+                int32_t* rank0, int32_t* shards, double* rank_load, double* makespan);
+
 /* ---- parity units (each runs the same device code as the sampler) ------ */
 
 /* Batched full energies E(theta) for fixed parameters: the K2 kernel.

@@ -61,7 +61,7 @@ EXPORTS = [
     "specmc_launch_shape", "specmc_device_count", "specmc_version", "specmc_session_create", "specmc_session_run",
     "specmc_session_fetch", "specmc_session_destroy", "specmc_probe_mufu", "specmc_smc_run_sharded",
     "specmc_nccl_unique_id", "specmc_comm_init_nccl", "specmc_comm_destroy", "specmc_init_ensemble",
-    "specmc_smc_run_sharded_batch",
+    "specmc_smc_run_sharded_batch", "specmc_smc_run_distributed", "specmc_plan",
 ]
 SPECMC_COMM_ID_BYTES = 128
 
@@ -98,6 +98,10 @@ def _load():
                                               E, Z]
         lib.specmc_comm_destroy.argtypes = [C.c_void_p]
         lib.specmc_comm_destroy.restype = None
+    if hasattr(lib, "specmc_plan"):
+        lib.specmc_smc_run_distributed.argtypes = [C.c_int32, C.POINTER(ProblemC), C.c_int32, C.POINTER(SpectrumC),
+                                                   C.c_void_p, _ip, _ip, C.POINTER(SmcResultC), E, Z]
+        lib.specmc_plan.argtypes = [C.c_int32, _dp, _lp, _ip, C.c_int32, _ip, _ip, _dp, _dp]
     lib.specmc_result_free.argtypes = [C.POINTER(SmcResultC)]
     lib.specmc_result_free.restype = None
     lib.specmc_free.argtypes = [C.c_void_p]

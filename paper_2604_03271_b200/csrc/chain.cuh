@@ -936,6 +936,9 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   const int gi = find_group(cta_prefix, n_list, blockIdx.x);
   const GroupDesc& g = gds[list[gi]];
   const int cta_in_group = blockIdx.x - cta_prefix[gi];
+  // a move launch covers every group of the class; finished or failed groups'
+  // CTAs leave at once (levels are enqueued ahead of the host's check)
+  if (!ENERGY && !g.st->active) return;
 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   f2* sx = reinterpret_cast<f2*>(smem + SM::off_x);

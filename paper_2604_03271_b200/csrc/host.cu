@@ -1054,46 +1054,89 @@ struct ClassRun {
         if (h_st[gi].active) next.push_back(gi);
       active.swap(next);
     }
-    while (!active.empty() && !xch) {
-      total = build_list(active, false, list, prefix);
+    if (!active.empty() && !xch) {
+      // Unsharded class: every level is the same launch sequence over every
+      // group of the class (the kernels skip finished or failed groups), so
+      // the host enqueues levels ahead without waiting for them: after each
+      // level the small GroupState array is copied into a pinned ring slot and
+      // an event recorded; the host keeps up to kAhead levels in flight and
+      // retires / stages runs as their levels' copies land.  Once every run is
+      // seen inactive no further level is enqueued (at most kAhead levels of
+      // empty launches run past the end).
+      constexpr int kAhead = 3, kRing = kAhead + 1;
+      total = build_list(order, false, list, prefix);  // every group, its S chains (static)
       const int na = (int)list.size();
+      dev.sync();  // h_list's pinned bytes of the init launches may still be in flight
       std::vector<int> small, big;
-      for (int gi : active) (gds[gi].nslices > 0 ? big : small).push_back(gi);
-      dev.sync();  // h_list is reused: the previous round's copies must be done
+      for (int gi : order) (gds[gi].nslices > 0 ? big : small).push_back(gi);
       std::memcpy(h_list, list.data(), sizeof(int) * na);
       std::memcpy(h_list + (G + 1), prefix.data(), sizeof(int) * (na + 1));
       std::copy(small.begin(), small.end(), h_list + 2 * (G + 1));
       std::copy(big.begin(), big.end(), h_list + 3 * (G + 1));
       h2d(d_list, h_list, na, st);
       h2d(d_prefix, h_list + (G + 1), na + 1, st);
-      if (!small.empty()) {
-        h2d(d_list_small, h_list + 2 * (G + 1), small.size(), st);
-        cuda_check(launch_temper(d_gds, d_list_small, (int)small.size(), st), "k_temper");
-        count_launch(1);
+      if (!small.empty()) h2d(d_list_small, h_list + 2 * (G + 1), small.size(), st);
+      if (!big.empty()) h2d(d_list_big, h_list + 3 * (G + 1), big.size(), st);
+      size_t ring_bytes = 0;
+      GroupState* ring = static_cast<GroupState*>(pinned_cache().get(sizeof(GroupState) * G * kRing, ring_bytes));
+      std::vector<cudaEvent_t> lev(kRing), ma(kRing), mb(kRing);
+      for (int k = 0; k < kRing; ++k) {
+        cuda_check(cudaEventCreateWithFlags(&lev[k], cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&ma[k]), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&mb[k]), "cudaEventCreate");
       }
-      if (!big.empty()) {
-        h2d(d_list_big, h_list + 3 * (G + 1), big.size(), st);
-        cuda_check(launch_temper_grid(d_gds, d_list_big, (int)big.size(), max_slices, st), "k_tp_*");
-        count_launch(temper_grid_launches());
+      std::vector<char> seen_done(G, 0);
+      int n_live = (int)active.size();
+      int64_t enq = 0, obs = 0;
+      bool live_before = true;  // some run was active when the observed level started
+      while (true) {
+        while (n_live > 0 && enq - obs < kAhead) {  // enqueue one level
+          const int k = (int)(enq % kRing);
+          if (!small.empty()) {
+            cuda_check(launch_temper(d_gds, d_list_small, (int)small.size(), st), "k_temper");
+            count_launch(1);
+          }
+          if (!big.empty()) {
+            cuda_check(launch_temper_grid(d_gds, d_list_big, (int)big.size(), max_slices, st), "k_tp_*");
+            count_launch(temper_grid_launches());
+          }
+          cuda_check(cudaEventRecord(ma[k], st), "event");
+          cuda_check(launch_move(kfam, noise, shape, dmax, d_gds, d_list, d_prefix, na, total, st), "k_chain<move>");
+          cuda_check(cudaEventRecord(mb[k], st), "event");
+          cuda_check(launch_stats_grid(d_gds, d_list, na, dmax, st), "k_stats_grid");
+          count_launch(3);
+          d2h(ring + (size_t)k * G, d_st, G, st);
+          cuda_check(cudaEventRecord(lev[k], st), "event");
+          ++enq;
+        }
+        if (obs == enq) break;
+        const int k = (int)(obs % kRing);
+        if (stage_early) drain(false);  // host copies of finished runs while the levels run
+        cuda_check(cudaEventSynchronize(lev[k]), "cudaEventSynchronize");
+        const GroupState* hs = ring + (size_t)k * G;
+        if (live_before) {  // (a level past the end of every run moves nothing: not counted)
+          float ms = 0.f;
+          cuda_check(cudaEventElapsedTime(&ms, ma[k], mb[k]), "cudaEventElapsedTime");
+          move_ms += ms;
+          ++move_launches;
+        }
+        live_before = false;
+        for (int gi = 0; gi < G; ++gi) live_before = live_before || hs[gi].active;
+        std::memcpy(h_st, hs, sizeof(GroupState) * G);
+        for (int gi = 0; gi < G; ++gi)
+          if (!h_st[gi].active && !seen_done[gi]) {
+            seen_done[gi] = 1;
+            --n_live;
+            if (stage_early) stage_group(gi, st);
+          }
+        ++obs;
       }
-      cuda_check(cudaEventRecord(mv.a, st), "event");
-      cuda_check(launch_move(kfam, noise, shape, dmax, d_gds, d_list, d_prefix, na, total, st), "k_chain<move>");
-      cuda_check(cudaEventRecord(mv.b, st), "event");
-      cuda_check(launch_stats_grid(d_gds, d_list, na, dmax, st), "k_stats_grid");
-      count_launch(3);
-      if (stage_early) drain(false);  // host copies of finished runs while this level runs
-      d2h(h_st, d_st, G, st);
-      dev.sync();
-      move_ms += mv.ms();
-      ++move_launches;
-      std::vector<int> next;
-      for (int gi : active) {
-        if (h_st[gi].active)
-          next.push_back(gi);
-        else if (stage_early)
-          stage_group(gi, st);
+      for (int k = 0; k < kRing; ++k) {
+        cudaEventDestroy(lev[k]);
+        cudaEventDestroy(ma[k]);
+        cudaEventDestroy(mb[k]);
       }
-      active.swap(next);
+      pinned_cache().put(ring, ring_bytes);
     }
     cuda_check(cudaEventRecord(whole.b, st), "event");
     dev.sync();
@@ -1333,6 +1376,7 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;  // NCCL >= 2.18
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*ErrorString)(ncclResult_t) = nullptr;
@@ -1348,6 +1392,7 @@ struct NcclApi {
       a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(a.h, "ncclAllReduce"));
       a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(a.h, "ncclAllGather"));
       a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(a.h, "ncclCommDestroy"));
+      a.CommSplit = reinterpret_cast<decltype(a.CommSplit)>(dlsym(a.h, "ncclCommSplit"));
       a.ErrorString = reinterpret_cast<decltype(a.ErrorString)>(dlsym(a.h, "ncclGetErrorString"));
       a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(a.h, "ncclGroupStart"));
       a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(a.h, "ncclGroupEnd"));
@@ -1367,6 +1412,9 @@ struct NcclApi {
 struct CommImpl {
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1, device = 0;
+  // sub-communicators of the distributed entry (one per rank block that shares
+  // a particle-sharded run), split once from comm and kept for later calls
+  std::map<std::pair<int, int>, ncclComm_t> subs;
 };
 
 // One shard of every run per rank: the exchanges are NCCL collectives on the
@@ -1487,6 +1535,192 @@ int run_sharded_batch(int n_problems, const specmc_problem* problems, int n_spec
       }
       for (int r = 1; r < count; ++r) specmc_result_free(&res[i0 + r]);
     }
+    if (o.status != SPECMC_OK && first_bad == SPECMC_OK) first_bad = o.status;
+  }
+  return first_bad;
+}
+
+// ------------------------------------------------- multi-GPU model selection
+// Placement of a batch of runs (the K range of a model selection, SURVEY.md
+// 8e-1/8e-3) on `world` ranks.  Cost of a run = T d N (its proposals per level
+// times points; the level count grows only weakly with K).  A run costing more
+// than a rank's share L = sum / world is particle-sharded over s ranks (the
+// smallest power of two >= cost / L that divides T), placed on the aligned
+// block of s ranks with the least load; every other run goes to the least
+// loaded rank, longest first (LPT).  Deterministic: every rank computes the
+// same plan from the same inputs.
+struct Plan {
+  std::vector<int> rank0, shards;
+  std::vector<double> load;
+  double makespan = 0.0;
+};
+Plan make_plan(int n, const double* cost, const int64_t* T, const int32_t* n_sweeps, int world) {
+  Plan p;
+  p.rank0.assign(n, 0);
+  p.shards.assign(n, 1);
+  p.load.assign(world, 0.0);
+  double total = 0.0;
+  for (int i = 0; i < n; ++i) total += cost[i];
+  const double share = total / world;
+  std::vector<int> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  int wpow = 1;
+  while (wpow * 2 <= world) wpow *= 2;
+  for (int i : order) {
+    int s = 1;
+    if (world > 1 && cost[i] > share * (1.0 + 1e-9)) {
+      while (s < wpow && s * share < cost[i]) s *= 2;
+      // every shard keeps whole chains: T / s divisible by n with >= 2 chains
+      while (s > 1 && (T[i] % s != 0 || (T[i] / s) % n_sweeps[i] != 0 || T[i] / s / n_sweeps[i] < 2)) s /= 2;
+    }
+    int best = 0;
+    if (s > 1) {
+      double bl = 1e300;
+      for (int b = 0; b + s <= world; b += s) {
+        double m = 0.0;
+        for (int r = b; r < b + s; ++r) m = std::max(m, p.load[r]);
+        if (m < bl) {
+          bl = m;
+          best = b;
+        }
+      }
+      for (int r = best; r < best + s; ++r) p.load[r] += cost[i] / s;
+    } else {
+      for (int r = 1; r < world; ++r)
+        if (p.load[r] < p.load[best]) best = r;
+      p.load[best] += cost[i];
+    }
+    p.rank0[i] = best;
+    p.shards[i] = s;
+  }
+  p.makespan = *std::max_element(p.load.begin(), p.load.end());
+  return p;
+}
+
+double run_cost(const specmc_problem& pr, const specmc_spectrum* sps) {
+  return (double)pr.cfg.T * (double)pr.model.d * (double)sps[pr.spectrum].n;
+}
+
+// The batch split over the ranks of `world` by make_plan: first the sharded
+// runs, block by block in (first rank, shards) order on sub-communicators split
+// from world (every rank takes part in every split, in the same order), then
+// this rank's own runs in one batch, then one all-reduce of the per-run
+// scalars (F, levels, status, ... from the run's first rank; trials summed over
+// its shards) so that every rank can select K.  Arrays (posterior, energies,
+// ladder, diagnostics) stay with the ranks that ran the run.
+int run_distributed(int n_problems, const specmc_problem* problems, int n_spectra, const specmc_spectrum* sps,
+                    CommImpl* world, int32_t* plan_rank0, int32_t* plan_shards, specmc_smc_result* out) {
+  if (n_problems < 1 || !problems) throw Error(SPECMC_EINVAL, "distributed: no problems");
+  if (n_spectra < 1 || !sps) throw Error(SPECMC_EINVAL, "distributed: no spectra");
+  if (!world) throw Error(SPECMC_EINVAL, "distributed: null communicator");
+  for (int i = 0; i < n_problems; ++i) {
+    if (problems[i].spectrum < 0 || problems[i].spectrum >= n_spectra)
+      throw Error(SPECMC_EINVAL, "batch: spectrum index out of range");
+    validate_config(problems[i].cfg);
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<double> cost(n_problems);
+  std::vector<int64_t> Ts(n_problems);
+  std::vector<int32_t> ns(n_problems);
+  for (int i = 0; i < n_problems; ++i) {
+    cost[i] = run_cost(problems[i], sps);
+    Ts[i] = problems[i].cfg.T;
+    ns[i] = problems[i].cfg.n;
+  }
+  const Plan plan = make_plan(n_problems, cost.data(), Ts.data(), ns.data(), world->world);
+  if (plan_rank0) std::copy(plan.rank0.begin(), plan.rank0.end(), plan_rank0);
+  if (plan_shards) std::copy(plan.shards.begin(), plan.shards.end(), plan_shards);
+  const int me = world->rank;
+  Device dev(world->device);
+  Timer whole;
+  cuda_check(cudaEventRecord(whole.a, dev.stream), "event");
+  NcclApi& api = NcclApi::get();
+  std::vector<specmc_problem> probs(problems, problems + n_problems);
+  for (auto& p : probs) p.cfg.device = world->device;
+  // 1) particle-sharded runs, one rank block at a time
+  std::map<std::pair<int, int>, std::vector<int>> blocks;
+  for (int i = 0; i < n_problems; ++i)
+    if (plan.shards[i] > 1) blocks[{plan.rank0[i], plan.shards[i]}].push_back(i);
+  int first_bad = SPECMC_OK;
+  for (auto& kv : blocks) {
+    const int b0 = kv.first.first, s = kv.first.second;
+    const bool in = me >= b0 && me < b0 + s;
+    auto it = world->subs.find(kv.first);
+    if (it == world->subs.end()) {
+      if (!api.CommSplit) throw Error(SPECMC_ECOMM, "NCCL without ncclCommSplit (needs >= 2.18)");
+      ncclComm_t sub = nullptr;
+      api.check(api.CommSplit(world->comm, in ? b0 * 4096 + s : NCCL_SPLIT_NOCOLOR, me, &sub, nullptr),
+                "ncclCommSplit");
+      it = world->subs.emplace(kv.first, sub).first;
+    }
+    if (!in) continue;
+    CommImpl sc;
+    sc.comm = it->second;
+    sc.rank = me - b0;
+    sc.world = s;
+    sc.device = world->device;
+    std::vector<specmc_problem> bp;
+    for (int i : kv.second) bp.push_back(probs[i]);
+    std::vector<specmc_smc_result> br(bp.size());
+    for (auto& r : br) std::memset(&r, 0, sizeof(r));
+    const int rc = run_sharded_batch((int)bp.size(), bp.data(), n_spectra, sps, 1, &sc, br.data());
+    if (rc != SPECMC_OK && first_bad == SPECMC_OK) first_bad = rc;
+    for (size_t j = 0; j < kv.second.size(); ++j) out[kv.second[j]] = br[j];
+  }
+  // 2) this rank's own runs
+  std::vector<int> mine;
+  for (int i = 0; i < n_problems; ++i)
+    if (plan.shards[i] == 1 && plan.rank0[i] == me) mine.push_back(i);
+  if (!mine.empty()) {
+    std::vector<specmc_problem> bp;
+    for (int i : mine) bp.push_back(probs[i]);
+    std::vector<specmc_smc_result> br(bp.size());
+    for (auto& r : br) std::memset(&r, 0, sizeof(r));
+    char e2[256];
+    const int rc = run_batch((int)bp.size(), bp.data(), n_spectra, sps, br.data(), e2, sizeof(e2));
+    if (rc != SPECMC_OK && first_bad == SPECMC_OK) first_bad = rc;
+    for (size_t j = 0; j < mine.size(); ++j) out[mine[j]] = br[j];
+  }
+  // 3) every run's scalars on every rank (one all-reduce, sum; zeros from non-owners)
+  constexpr int kF = 7;
+  std::vector<double> h((size_t)kF * n_problems, 0.0);
+  for (int i = 0; i < n_problems; ++i) {
+    const bool ran = plan.shards[i] > 1 ? (me >= plan.rank0[i] && me < plan.rank0[i] + plan.shards[i])
+                                        : me == plan.rank0[i];
+    if (!ran) continue;
+    double* r = h.data() + (size_t)kF * i;
+    r[5] = (double)out[i].trials;  // local share of a sharded run
+    if (me != plan.rank0[i]) continue;
+    r[0] = out[i].F;
+    r[1] = out[i].diverged;
+    r[2] = out[i].levels;
+    r[3] = out[i].status;
+    r[4] = (double)((int64_t)problems[i].cfg.T * problems[i].model.d * out[i].levels);
+    r[6] = out[i].d;
+  }
+  double* dbuf = nullptr;
+  cuda_check(cudaMalloc(&dbuf, sizeof(double) * h.size()), "cudaMalloc");
+  h2d(dbuf, h.data(), h.size(), dev.stream);
+  api.check(api.AllReduce(dbuf, dbuf, h.size(), ncclFloat64, ncclSum, world->comm, dev.stream), "ncclAllReduce");
+  d2h(h.data(), dbuf, h.size(), dev.stream);
+  cuda_check(cudaEventRecord(whole.b, dev.stream), "event");
+  dev.sync();
+  cudaFree(dbuf);
+  const double dsec = whole.ms() * 1e-3;
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  for (int i = 0; i < n_problems; ++i) {
+    const double* r = h.data() + (size_t)kF * i;
+    specmc_smc_result& o = out[i];
+    o.F = r[0];
+    o.diverged = (int32_t)r[1];
+    o.levels = (int32_t)r[2];
+    o.status = (int32_t)r[3];
+    o.proposals = (int64_t)r[4];
+    o.trials = (int64_t)r[5];
+    o.d = (int32_t)r[6];
+    o.device_seconds = dsec;
+    o.wall_seconds = wall;
     if (o.status != SPECMC_OK && first_bad == SPECMC_OK) first_bad = o.status;
   }
   return first_bad;
@@ -1715,6 +1949,12 @@ int specmc_comm_init_nccl(int32_t rank, int32_t world, const uint8_t* id, int32_
 void specmc_comm_destroy(specmc_comm* c) {
   auto* p = reinterpret_cast<CommImpl*>(c);
   if (!p) return;
+  for (auto& kv : p->subs) {
+    try {
+      NcclApi::get().CommDestroy(kv.second);
+    } catch (...) {
+    }
+  }
   if (p->comm) {
     try {
       NcclApi::get().CommDestroy(p->comm);
@@ -1722,6 +1962,33 @@ void specmc_comm_destroy(specmc_comm* c) {
     }
   }
   delete p;
+}
+
+int specmc_plan(int32_t n_runs, const double* costs, const int64_t* T, const int32_t* n_sweeps, int32_t world,
+                int32_t* rank0, int32_t* shards, double* rank_load, double* makespan) {
+  if (n_runs < 1 || !costs || !T || !n_sweeps || world < 1 || !rank0 || !shards) return SPECMC_EINVAL;
+  for (int i = 0; i < n_runs; ++i)
+    if (!(costs[i] >= 0.0) || T[i] < 2 || n_sweeps[i] < 1) return SPECMC_EINVAL;
+  const Plan p = make_plan(n_runs, costs, T, n_sweeps, world);
+  std::copy(p.rank0.begin(), p.rank0.end(), rank0);
+  std::copy(p.shards.begin(), p.shards.end(), shards);
+  if (rank_load) std::copy(p.load.begin(), p.load.end(), rank_load);
+  if (makespan) *makespan = p.makespan;
+  return SPECMC_OK;
+}
+
+int specmc_smc_run_distributed(int32_t n_problems, const specmc_problem* problems, int32_t n_spectra,
+                               const specmc_spectrum* spectra, specmc_comm* comm, int32_t* plan_rank0,
+                               int32_t* plan_shards, specmc_smc_result* out, char* err, size_t errlen) {
+  if (out && n_problems > 0) std::memset(out, 0, sizeof(specmc_smc_result) * (size_t)n_problems);
+  return guarded(err, errlen, [&]() -> int {
+    if (!out) throw Error(SPECMC_EINVAL, "null results");
+    const int r = run_distributed(n_problems, problems, n_spectra, spectra, reinterpret_cast<CommImpl*>(comm),
+                                  plan_rank0, plan_shards, out);
+    if (r != SPECMC_OK)
+      copy_err(err, errlen, "smc: max_levels exceeded before reaching beta = 1 (or total weight is zero)");
+    return r;
+  });
 }
 
 void specmc_free(void* p) { std::free(p); }

@@ -65,7 +65,7 @@ __global__ void k_init_draw(const GroupDesc* __restrict__ gds, const int* __rest
 }
 
 // ------------------------------------------------------- block reductions
-constexpr int kTemperThreads = 1024;
+constexpr int kTemperThreads = 512;
 
 template <typename T, typename Op>
 __device__ __forceinline__ T block_reduce(T v, T* sh, Op op, T ident) {
@@ -97,13 +97,12 @@ struct OpMaxI {
   __device__ long long operator()(long long a, long long b) const { return a > b ? a : b; }
 };
 
-// exp(a) for a <= 0 with fp64 range reduction and an fp32 MUFU mantissa
+// Tempering weight exp(a), a <= 0, at fp32 precision (one MUFU ex2 of
+// a log2(e) rounded to fp32): the weights are shifted so that the largest is
+// 1, where the fp32 argument is exact to ~6e-8; a weight below 2^-126 is 0
+// (it vanishes in every fp64 sum next to the largest weight 1).
 __device__ __forceinline__ double exp_neg_split(double a) {
-  if (!(a > -745.0)) return 0.0;
-  const double y = a * 1.4426950408889634074;
-  const double yi = floor(y);
-  const float yf = (float)(y - yi);
-  return scalbn((double)ex2f(yf), (int)yi);
+  return (double)ex2f((float)(a * 1.4426950408889634074));
 }
 
 struct TemperShared {
@@ -113,21 +112,6 @@ struct TemperShared {
   int ibc[4];
 };
 
-// (sum w)^2 / sum w^2 / T with w = exp(c (E - emin)) (smc.cpp:61-66, :76-79);
-// returns NaN when every weight vanishes
-__device__ double ess_ratio_at(const double* E, int64_t T, double emin, double c, TemperShared& sh) {
-  double a1 = 0.0, a2 = 0.0;
-  for (int64_t i = threadIdx.x; i < T; i += blockDim.x) {
-    const double w = exp_neg_split(c * (E[i] - emin));
-    a1 += w;
-    a2 += w * w;
-  }
-  const double s1 = block_reduce(a1, sh.red, OpAdd(), 0.0);
-  const double s2 = block_reduce(a2, sh.red, OpAdd(), 0.0);
-  if (!(s1 > 0.0)) return nan("");
-  return (s1 * s1 / s2) / (double)T;
-}
-
 __device__ double block_emin(const double* E, int64_t T, TemperShared& sh) {
   double m = dinf();
   for (int64_t i = threadIdx.x; i < T; i += blockDim.x) m = (E[i] < m) ? E[i] : m;
@@ -135,33 +119,121 @@ __device__ double block_emin(const double* E, int64_t T, TemperShared& sh) {
   return isfinite(m) ? m : 0.0;
 }
 
-// next_beta (smc.cpp:68-93); err = 1 when every weight vanishes
+// Sums NV = 16 doubles across a warp by recursive halving: each step a lane
+// keeps half of its values and adds its partner's copy of them, so the 16
+// values cost 16 double shuffles instead of 80; lane l ends with the warp
+// total of value (l >> 1).  Fixed order: deterministic.
+template <int NV>
+__device__ __forceinline__ double warp_multi_sum(double (&v)[NV], int lane) {
+#pragma unroll
+  for (int o = 16, h = NV / 2; h >= 1; o >>= 1, h >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double send = up ? v[i] : v[i + h];
+      const double keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+// next_beta (smc.cpp:68-93) in one CTA, D bisection steps per pass over E:
+// each pass evaluates the full step (first pass only) and the 2^D - 1
+// midpoints the next D steps can visit (the heap below the current (lo, hi),
+// as k_tp_ess_tree), then every warp replays the reference's control flow
+// through them (stop at |ESS/T - target| <= 1e-6 or 60 steps), so beta_next is
+// the reference bisection's.  One barrier per pass: the per-warp partial sums
+// are double-buffered and every warp reduces them and replays redundantly.
+// err = 1 when every weight vanishes.
+constexpr int kTemperDepth = 3;
+template <int D>
 __device__ double block_next_beta(const double* E, int64_t T, double n_data, double beta_prev, double target,
                                   TemperShared& sh, int& err) {
-  err = 0;
+  constexpr int S = 1 << D;
+  static_assert(S == 8, "warp_multi_sum layout: 2 S = 16 values");
+  __shared__ double shp[2][2 * S][kTemperThreads / 32];
   const double emin = block_emin(E, T, sh);
   const double full = 1.0 - beta_prev;
-  double r = ess_ratio_at(E, T, emin, -full * n_data, sh);
-  if (isnan(r)) {
-    err = 1;
-    return 0.0;
-  }
-  if (r >= target) return 1.0;
-  double lo = 0.0, hi = full, mid = 0.5 * full;
-  for (int it = 0; it < 60; ++it) {
-    mid = 0.5 * (lo + hi);
-    r = ess_ratio_at(E, T, emin, -mid * n_data, sh);
-    if (isnan(r)) {
-      err = 1;
-      return 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double blo = 0.0, bhi = full, beta = 1.0;
+  int it = -1, state = 0, par = 0;  // state: 0 running, 1 done, 2 error
+  while (state == 0) {
+    const bool first = it < 0;
+    double dl[S], lo[S], hi[S];
+    dl[0] = full;
+    lo[1] = blo;
+    hi[1] = bhi;
+#pragma unroll
+    for (int j = 1; j < S; ++j) {
+      dl[j] = 0.5 * (lo[j] + hi[j]);
+      if (2 * j + 1 < S) {
+        lo[2 * j] = lo[j];
+        hi[2 * j] = dl[j];
+        lo[2 * j + 1] = dl[j];
+        hi[2 * j + 1] = hi[j];
+      }
     }
-    if (fabs(r - target) <= 1e-6) break;
-    if (r > target)
-      lo = mid;
-    else
-      hi = mid;
+    double a[2 * S];  // (sum w, sum w^2) per slot
+#pragma unroll
+    for (int v = 0; v < 2 * S; ++v) a[v] = 0.0;
+    for (int64_t i = threadIdx.x; i < T; i += blockDim.x) {
+      const double x = E[i] - emin;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        if (s == 0 && !first) continue;
+        const double w = exp_neg_split(-dl[s] * n_data * x);
+        a[2 * s] += w;
+        a[2 * s + 1] += w * w;
+      }
+    }
+    const double ws = warp_multi_sum(a, lane);  // lane l: value l >> 1 of this warp
+    if ((lane & 1) == 0) shp[par][lane >> 1][warp] = ws;
+    __syncthreads();
+    double tot = 0.0;  // lane v < 2S: value v summed over the warps in warp order
+    if (lane < 2 * S)
+      for (int w = 0; w < nw; ++w) tot += shp[par][lane][w];
+    par ^= 1;
+    // replay (fin_ess semantics), warp-uniform: every lane fetches the slot sums it needs
+    auto step = [&](int s) {
+      const double s1 = __shfl_sync(0xffffffffu, tot, 2 * s), s2 = __shfl_sync(0xffffffffu, tot, 2 * s + 1);
+      const double delta = it < 0 ? full : 0.5 * (blo + bhi);
+      if (!(s1 > 0.0)) {  // ess: total weight is zero (smc.cpp:63)
+        state = 2;
+        return -1;
+      }
+      const double r = (s1 * s1 / s2) / (double)T;
+      if (it < 0) {
+        if (r >= target) {
+          beta = 1.0;
+          state = 1;
+          return -1;
+        }
+        it = 0;
+        return 0;
+      }
+      it += 1;
+      if (fabs(r - target) <= 1e-6 || it >= 60) {
+        beta = beta_prev + delta;
+        state = 1;
+        return -1;
+      }
+      if (r > target) {
+        blo = delta;
+        return 1;
+      }
+      bhi = delta;
+      return 0;
+    };
+    int go = it < 0 ? step(0) : 0;
+    for (int j = 1, k = 0; go >= 0 && k < D; ++k) {
+      go = step(j);
+      j = 2 * j + (go > 0 ? 1 : 0);
+    }
   }
-  return beta_prev + mid;
+  __syncthreads();  // (shp is reused by the next call)
+  err = state == 2 ? 1 : 0;
+  return err ? 0.0 : beta;
 }
 
 // incremental weights (smc.cpp:55-59) -> lse, ess ratio, log_mean_w; writes
@@ -328,6 +400,7 @@ __global__ void __launch_bounds__(kTemperThreads) k_temper(const GroupDesc* __re
   __shared__ TemperShared sh;
   const GroupDesc& g = gds[list[blockIdx.x]];
   GroupState* st = g.st;
+  if (!st->active) return;  // finished or failed (levels enqueued ahead of the host's check)
   const int level = st->level;
   if (level >= g.max_levels) {  // smc.cpp:195-196
     if (threadIdx.x == 0) {
@@ -340,7 +413,7 @@ __global__ void __launch_bounds__(kTemperThreads) k_temper(const GroupDesc* __re
   const int64_t T = g.T;
   const double beta_prev = st->beta;
   int err = 0;
-  const double beta_next = block_next_beta(E, T, g.n_data, beta_prev, g.ess_target, sh, err);
+  const double beta_next = block_next_beta<kTemperDepth>(E, T, g.n_data, beta_prev, g.ess_target, sh, err);
   double ess_ratio = 0.0, lmw = 0.0;
   bool ok = !err && block_weights(E, T, beta_next - beta_prev, g.n_data, g.wbuf, sh, ess_ratio, lmw);
   if (!ok) {
@@ -401,6 +474,7 @@ struct SliceCtx {
 __device__ __forceinline__ bool slice_ctx(const GroupDesc* gds, const int* list, SliceCtx& c) {
   c.g = &gds[list[blockIdx.y]];
   c.ts = c.g->ts;
+  if (!c.g->st->active) return false;  // finished or failed (levels enqueued ahead of the host's check)
   if ((int)blockIdx.x >= c.g->nslices) return false;
   const int64_t T = c.g->st->T_loc;
   c.i0 = (int64_t)blockIdx.x * c.g->slice_len;
@@ -822,7 +896,7 @@ __global__ void __launch_bounds__(256) k_stats_grid(const GroupDesc* __restrict_
   __shared__ TemperShared sh;
   const GroupDesc& g = gds[list[blockIdx.y]];
   const int i = blockIdx.x;
-  if (i >= g.d) return;
+  if (i >= g.d || !g.st->active) return;
   const int S = g.st->S_loc;
   double a = 0.0, l = 0.0;
   for (int c = threadIdx.x; c < S; c += blockDim.x) {
@@ -841,6 +915,7 @@ __global__ void k_stats_final(const GroupDesc* __restrict__ gds, const int* __re
   const GroupDesc& g = gds[list[blockIdx.x]];
   if (threadIdx.x != 0) return;
   GroupState* st = g.st;
+  if (!st->active) return;
   const int d = g.d, S = g.S, H = st->hist_count;  // S: all chains of the level (every shard)
   double* h = g.hist + (size_t)(H % kHist) * (1 + 2 * d);
   const double prop = (double)S * g.n;
@@ -921,7 +996,7 @@ __global__ void __launch_bounds__(kTemperThreads) k_unit_next_beta(const double*
                                                                    int* err) {
   __shared__ TemperShared sh;
   int e = 0;
-  const double b = block_next_beta(E, n, n_data, beta_prev, target, sh, e);
+  const double b = block_next_beta<kTemperDepth>(E, n, n_data, beta_prev, target, sh, e);
   if (threadIdx.x == 0) {
     *out = b;
     *err = e;

@@ -103,6 +103,8 @@ def _report(spec: ModelSpec, cfg: SmcConfig, n_data: int, r: _lib.SmcResultC) ->
                     trials=r.trials)
     rep.scalars = {"T": float(cfg.T), "n": float(cfg.n), "ess_target": cfg.ess_target, "seed": float(cfg.seed),
                    "workers": float(cfg.workers), "n_data": float(n_data), "levels": float(L)}
+    if not r.ladder:  # distributed entry: a run this rank did not hold (scalars only)
+        return rep
     rep.arrays = {
         "ladder": np.ctypeslib.as_array(r.ladder, (L + 1,)).copy(),
         "level_ess_ratio": np.ctypeslib.as_array(r.level_ess_ratio, (max(L, 1),))[:L].copy(),
@@ -319,6 +321,43 @@ def smc_run_sharded_batch(problems: Sequence[Tuple[ModelSpec, int, SmcConfig]], 
             lib.specmc_result_free(C.byref(res[i]))
         _raise(rc, err)
     return _collect(problems, spectra, res, raise_on_error)
+
+
+def plan(costs, T, n, world: int):
+    """specmc_plan: placement of runs on `world` ranks -> (rank0, shards, rank_load, makespan)."""
+    costs = _d(costs)
+    m = len(costs)
+    Ta = np.ascontiguousarray(T, dtype=np.int64) if np.ndim(T) else np.full(m, T, dtype=np.int64)
+    na = np.ascontiguousarray(n, dtype=np.int32) if np.ndim(n) else np.full(m, n, dtype=np.int32)
+    r0 = np.empty(m, dtype=np.int32)
+    sh = np.empty(m, dtype=np.int32)
+    load = np.empty(world)
+    mk = C.c_double()
+    rc = lib.specmc_plan(m, _p(costs), Ta.ctypes.data_as(_lib._lp), na.ctypes.data_as(_lib._ip), int(world),
+                         r0.ctypes.data_as(_lib._ip), sh.ctypes.data_as(_lib._ip), _p(load), C.byref(mk))
+    if rc:
+        raise ValueError("plan: invalid arguments")
+    return r0, sh, load, mk.value
+
+
+def smc_run_distributed(problems: Sequence[Tuple[ModelSpec, int, SmcConfig]], spectra: Sequence[Spectrum],
+                        comm: "Comm", raise_on_error: bool = True):
+    """Every problem of the batch placed on the ranks of ``comm`` (specmc_smc_run_distributed):
+    returns (reports, rank0, shards).  Every report carries F / levels / trials; posterior
+    and diagnostics only where this rank ran (part of) the run."""
+    probs, sps, keep = _pack(problems, spectra)
+    m = len(problems)
+    res = (_lib.SmcResultC * m)()
+    r0 = np.empty(m, dtype=np.int32)
+    sh = np.empty(m, dtype=np.int32)
+    err = C.create_string_buffer(1024)
+    rc = lib.specmc_smc_run_distributed(m, probs, len(spectra), sps, comm._h, r0.ctypes.data_as(_lib._ip),
+                                        sh.ctypes.data_as(_lib._ip), res, err, 1024)
+    if rc and rc != _lib.SPECMC_ERUNTIME:
+        for i in range(m):
+            lib.specmc_result_free(C.byref(res[i]))
+        _raise(rc, err)
+    return _collect(problems, spectra, res, raise_on_error), r0, sh
 
 
 def probe_mufu(device: int = 0) -> float:

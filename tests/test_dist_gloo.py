@@ -1,7 +1,16 @@
-"""Multi-rank host logic on CPU (gloo, world_size 2): trial-sharded model
-selection, max-over-ranks timing, the cross-rank ESS normalisers and the
-global systematic-resampling ranges."""
-import math
+"""Multi-rank host logic on CPU (gloo, world_size 2), SURVEY.md 8e.
+
+* The placement of a model selection on the ranks is the library's own
+  (specmc_plan, host.cu make_plan; host-only, no device needed): every rank
+  computes it from the same inputs and must get the same plan; the plan must
+  cover every run once, shard only runs larger than a rank's share, over
+  aligned power-of-two rank blocks whose shards keep whole chains.
+* The scalar exchange of specmc_smc_run_distributed (each run's owner
+  contributes its row, every shard its trial count, one sum all-reduce) is
+  replayed over gloo with the same plan: every rank must end with the full
+  table.
+* Trials mode: F per K gathered for model_select, max-over-ranks timing.
+"""
 import os
 import socket
 
@@ -18,41 +27,47 @@ def _port():
     return p
 
 
+def c2_costs():
+    # C2: N = 2000, T = 65536, K = 1..10 (d = 4K + 2), n = 8: cost = T d N
+    ks = np.arange(1, 11)
+    return ks, 65536.0 * (4 * ks + 2) * 2000.0
+
+
 def _worker(rank, ws, port, q):
+    import torch
     import torch.distributed as dist
+    import paper_2604_03271_b200 as S
     from paper_2604_03271_b200 import dist as D
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=ws)
     out = {}
-    # trial-sharded model selection: rank r's trial has its minimum at K = 3 (or 2 on rank 1)
-    ks = [1, 2, 3, 4]
+    ks, cost = c2_costs()
+    plans = {}
+    for world in (1, 2, 4, 8):
+        r0, sh, load, mk = S.plan(cost, 65536, 8, world)
+        t = torch.tensor(np.concatenate([r0, sh]).astype(np.int64))
+        g = [torch.empty_like(t) for _ in range(ws)]
+        dist.all_gather(g, t)
+        plans[world] = (r0.tolist(), sh.tolist(), load.tolist(), mk, [x.tolist() for x in g])
+    out["plans"] = plans
+    # the distributed entry's scalar exchange with the world-2 plan
+    r0, sh = np.array(plans[2][0]), np.array(plans[2][1])
+    F = 1000.0 - 3.0 * ks + 0.5 * (ks - 6) ** 2  # synthetic per-run results
+    local_trials = 100 * ks + rank  # a shard's own trial count
+    rows = torch.zeros((len(ks), 3), dtype=torch.float64)
+    for i in range(len(ks)):
+        held = rank in range(r0[i], r0[i] + sh[i])
+        if held:
+            rows[i, 1] = float(local_trials[i])
+        if rank == r0[i]:
+            rows[i, 0] = F[i]
+            rows[i, 2] = 1.0
+    dist.all_reduce(rows)
+    out["rows"] = rows.numpy()
+    # trials mode
     Fs = [10.0, 5.0 + rank * -0.2, 4.95, 6.0]
-    out["sel"] = D.gather_selection(ks, Fs)
+    out["sel"] = D.gather_selection([1, 2, 3, 4], Fs)
     out["timing"] = D.reduce_timing(1.0 + rank, 100.0)
-    # ESS normalisers over two particle shards == single-array values
-    rng = np.random.default_rng(7)
-    lw = rng.normal(size=1000) * 3
-    part = np.array_split(lw, ws)[rank]
-    m = part.max()
-    out["w"] = D.allreduce_weight_stats(m, float(np.exp(part - m).sum()), float(np.exp(2 * (part - m)).sum()))
-    # global systematic comb ranges from per-rank totals
-    gm = lw.max()
-    lse = gm + math.log(np.exp(lw - gm).sum())
-    w = np.exp(lw - lse)
-    shards = np.array_split(np.arange(1000), ws)
-    local = w[shards[rank]]
-    u, S = 0.37, 125
-    j0, j1, off = D.global_resample_range(float(local.sum()), u, S)
-    c = off + np.cumsum(local)
-    anc = []
-    lo = j0
-    for i, ci in enumerate(c):
-        last = rank == ws - 1 and i == len(c) - 1
-        k = S if last else D.count_le(float(ci), u, S)
-        k = min(max(k, lo), j1)
-        anc += [int(shards[rank][i])] * (k - lo)
-        lo = k
-    out["anc"] = (j0, j1, anc)
     q.put((rank, out))
     dist.barrier()
     dist.destroy_process_group()
@@ -66,10 +81,47 @@ def results():
     ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in ps:
         p.start()
-    res = dict(q.get(timeout=120) for _ in ps)
+    res = dict(q.get(timeout=180) for _ in ps)
     for p in ps:
         p.join(timeout=60)
     return res
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_plan_identical_on_every_rank_and_valid(results, world):
+    ks, cost = c2_costs()
+    r0, sh, load, mk, gathered = results[0]["plans"][world]
+    assert results[1]["plans"][world][:2] == (r0, sh)
+    for g in gathered:  # what each rank computed, as seen by rank 0
+        assert g == r0 + sh
+    share = cost.sum() / world
+    placed = np.zeros(world)
+    for i in range(len(ks)):
+        s = sh[i]
+        assert s >= 1 and (s & (s - 1)) == 0 and r0[i] % s == 0 and r0[i] + s <= world
+        assert 65536 % s == 0 and (65536 // s) % 8 == 0
+        if s > 1:
+            assert cost[i] > share  # only runs above a rank's share are split
+        placed[r0[i]:r0[i] + s] += cost[i] / s
+    assert np.allclose(placed, load) and mk == pytest.approx(max(load))
+    assert sum(load) == pytest.approx(cost.sum())
+    # LPT bound on the split instance
+    pieces = max(cost[i] / sh[i] for i in range(len(ks)))
+    assert mk <= 4.0 / 3.0 * max(share, pieces) + 1e-6 * cost.sum()
+    if world == 8:  # C2 at 8 GPUs: the three largest K (d = 34, 38, 42 > 240/8 = 30) span two ranks each
+        assert sh == [1] * 7 + [2, 2, 2]
+
+
+def test_distributed_scalar_exchange_complete_on_every_rank(results):
+    ks, _ = c2_costs()
+    r0, sh = np.array(results[0]["plans"][2][0]), np.array(results[0]["plans"][2][1])
+    F = 1000.0 - 3.0 * ks + 0.5 * (ks - 6) ** 2
+    for rank in (0, 1):
+        rows = results[rank]["rows"]
+        assert np.all(rows[:, 2] == 1.0)  # exactly one owner per run
+        assert np.allclose(rows[:, 0], F)
+        want = [sum(100 * k + r for r in range(r0[i], r0[i] + sh[i])) for i, k in enumerate(ks)]
+        assert np.allclose(rows[:, 1], want)
 
 
 def test_model_selection_over_trials(results):
@@ -82,26 +134,3 @@ def test_model_selection_over_trials(results):
 
 def test_max_over_ranks(results):
     assert results[0]["timing"] == (2.0, 200.0) == results[1]["timing"]
-
-
-def test_weight_stats_match_single_array(results):
-    rng = np.random.default_rng(7)
-    lw = rng.normal(size=1000) * 3
-    m = lw.max()
-    gm, s1, s2 = results[0]["w"]
-    assert gm == m
-    assert s1 == pytest.approx(np.exp(lw - m).sum(), rel=1e-12)
-    assert s2 == pytest.approx(np.exp(2 * (lw - m)).sum(), rel=1e-12)
-
-
-def test_global_resampling_matches_single_array(results, port):
-    rng = np.random.default_rng(7)
-    lw = rng.normal(size=1000) * 3
-    ref = port.systematic_resample(lw, 125, 0.37)
-    j0a, j1a, a0 = results[0]["anc"]
-    j0b, j1b, a1 = results[1]["anc"]
-    assert j0a == 0 and j1a == j0b and j1b == 125
-    got = np.array(a0 + a1)
-    assert len(got) == 125
-    mism = np.nonzero(got != ref)[0]
-    assert len(mism) <= 1  # only a target on a CDF boundary within rounding may differ

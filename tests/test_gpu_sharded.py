@@ -91,3 +91,23 @@ def test_sharded_batch_equals_single_sharded_runs(smc):
         one = smc.smc_run_sharded(w.spec(K), w.data, cfgs[K], n_virtual=4)
         assert b.F == one.F and np.array_equal(b.posterior, one.posterior)
     assert smc.model_select(list(zip((1, 2, 3), batch))).K_best == 3
+
+
+def test_distributed_one_rank_equals_batch(smc):
+    """specmc_smc_run_distributed on a one-rank NCCL communicator: the plan keeps
+    every run local, so the results equal specmc_smc_run_batch bitwise; the
+    per-run scalars come back through the NCCL all-reduce."""
+    w = syn.config("C1")
+    probs = [(w.spec(K), 0, smc.SmcConfig(T=2048, n=8, seed=9)) for K in (1, 2, 3)]
+    comm = smc.Comm(0, 1, smc.Comm.unique_id(), 0)
+    try:
+        reps, r0, sh = smc.smc_run_distributed(probs, [w.data], comm)
+        again, _, _ = smc.smc_run_distributed(probs, [w.data], comm)  # cached communicator state reused
+    finally:
+        comm.close()
+    ref = smc.smc_run_batch(probs, [w.data])
+    assert list(r0) == [0, 0, 0] and list(sh) == [1, 1, 1]
+    for a, b, c in zip(reps, ref, again):
+        assert a.F == b.F == c.F and a.trials == b.trials and a.proposals == b.proposals
+        assert np.array_equal(a.posterior, b.posterior)
+        assert a.scalars["levels"] == b.scalars["levels"]
