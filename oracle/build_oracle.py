@@ -22,10 +22,10 @@ REF_ROOT = Path("/root/reference/proj")
 PORT_SO = HERE / "liboracle.so"
 REF_SO = HERE / "_ref" / "libspecmc_ref.so"
 
-# reference translation units on the SMC path (+ the synthetic generators and
-# model selection used by the parity tests); remc/bench/config/CLI are out of
-# scope
-REF_SOURCES = ["priors", "model", "energy", "mcmc", "smc", "spectrum", "report", "synthetic", "posterior"]
+# reference translation units on the SMC path (+ the synthetic generators,
+# model selection, and the benchmark harness with the REMC comparator it
+# tabulates, used by the parity tests); config/CLI are out of scope
+REF_SOURCES = ["priors", "model", "energy", "mcmc", "smc", "spectrum", "report", "synthetic", "posterior", "remc", "bench"]
 
 COMMON = ["-O3", "-march=x86-64-v2", "-ffp-contract=off", "-fPIC", "-shared"]
 

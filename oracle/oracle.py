@@ -296,6 +296,9 @@ class Ref:
         L.ref_xrd_model_priors.argtypes = [C.c_int, C.c_int, _ip, _dp, _dp, _dp, _dp, C.c_int64, _ip, _dp, _dp]
         L.ref_gen_xrd.argtypes = [C.c_int64, C.c_uint64, _dp, _dp]
         L.ref_model_select.argtypes = [C.c_int, _ip, _dp, _ip, _ip]
+        L.ref_bench_table.argtypes = [C.POINTER(C.c_char_p), C.c_int, C.c_char_p, C.c_char_p, C.c_size_t]
+        L.ref_ci_table.argtypes = [C.POINTER(C.c_char_p), C.c_int, C.c_char_p, C.c_char_p, C.c_double, C.c_char_p,
+                                   C.c_size_t]
         L.ref_trial_seed.restype = C.c_uint64
         L.ref_trial_seed.argtypes = [C.c_uint64, C.c_int]
 
@@ -432,6 +435,24 @@ class Ref:
         if rc:
             raise OracleError(rc, "model_select")
         return kb.value
+
+    def bench_table(self, paths, reference_label="") -> str:
+        """bench_table_text(table_from_reports(read_report(p) for p in paths)) (bench.cpp:147-327)"""
+        arr = (C.c_char_p * len(paths))(*[str(p).encode() for p in paths])
+        buf = C.create_string_buffer(1 << 20)
+        n = self.lib.ref_bench_table(arr, len(paths), reference_label.encode(), buf, len(buf))
+        if n < 0:
+            raise OracleError(3, buf.value.decode())
+        return buf.value.decode()
+
+    def ci_table(self, paths, truth_path, param, level=0.95) -> str:
+        """ci_table_text(ci_error_curve(...)) (bench.cpp:251-338)"""
+        arr = (C.c_char_p * len(paths))(*[str(p).encode() for p in paths])
+        buf = C.create_string_buffer(1 << 20)
+        n = self.lib.ref_ci_table(arr, len(paths), str(truth_path).encode(), param.encode(), level, buf, len(buf))
+        if n < 0:
+            raise OracleError(3, buf.value.decode())
+        return buf.value.decode()
 
     def trial_seed(self, base, trial) -> int:
         return self.lib.ref_trial_seed(base, trial)

@@ -13,6 +13,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "specmc/bench.hpp"
 #include "specmc/energy.hpp"
 #include "specmc/mcmc.hpp"
 #include "specmc/posterior.hpp"
@@ -462,6 +463,40 @@ int ref_write_report(const char* path, const char* sampler, const char* label, d
     return 0;
   } catch (const std::exception&) {
     return 3;
+  }
+}
+
+// ---- benchmark tables (bench.cpp:147-338) over persisted reports
+namespace {
+int copy_out(const std::string& s, char* out, size_t outlen) {
+  if (s.size() + 1 > outlen) return -(int)(s.size() + 1);
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return (int)s.size();
+}
+}  // namespace
+
+// table_from_reports + bench_table_text; returns the text length (or -needed)
+int ref_bench_table(const char* const* paths, int n, const char* ref_label, char* out, size_t outlen) {
+  try {
+    std::vector<RunReport> runs;
+    for (int i = 0; i < n; ++i) runs.push_back(read_report(paths[i]));
+    return copy_out(bench_table_text(table_from_reports(runs, ref_label)), out, outlen);
+  } catch (const std::exception& e) {
+    copy_out(std::string("error: ") + e.what(), out, outlen);
+    return -1000000;
+  }
+}
+
+// ci_error_curve + ci_table_text
+int ref_ci_table(const char* const* paths, int n, const char* truth_path, const char* param, double level, char* out,
+                 size_t outlen) {
+  try {
+    std::vector<RunReport> runs;
+    for (int i = 0; i < n; ++i) runs.push_back(read_report(paths[i]));
+    return copy_out(ci_table_text(ci_error_curve(runs, read_report(truth_path), param, level)), out, outlen);
+  } catch (const std::exception& e) {
+    copy_out(std::string("error: ") + e.what(), out, outlen);
+    return -1000000;
   }
 }
 
