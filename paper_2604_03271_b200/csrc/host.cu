@@ -413,9 +413,15 @@ struct RunSpec;
 // MUFU lane-ops per point slot of one block shape evaluation (move kernel):
 // gm ex2, xps ex2 + rcp, Lorentzian rcp, xrd (ex2 + rcp) per reflection
 double mufu_per_shape(int kfam, const RunSpec& R);
-// ... and of one evaluation's noise terms: the paired hetero models share one
-// rcp and one lg2 per two points, poisson one lg2, gauss none
-double mufu_per_noise(int nz) { return nz == NZ_GAUSS ? 0.0 : 1.0; }
+// ... and of one evaluation's noise terms per point slot
+// (paired hetero models: four slots -- two points per half and pair -- share one
+// rcp and one lg2 per half, the leftover slots pair up: chain.cuh lane_noise_sum)
+double mufu_per_noise(int nz, int ppl) {
+  if (nz == NZ_GAUSS) return 0.0;
+  if (nz == NZ_POISSON) return 1.0;
+  const int ph = ppl / 2, k4 = ph / 4 * 4;
+  return (0.5 * k4 + 1.0 * (ph - k4)) / ph;
+}
 
 PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, const double* ys, int64_t N,
                                   const Shape& s, double x_shift) {
@@ -1148,7 +1154,7 @@ struct ClassRun {
     const double slots = (double)shape.PPL * 32.0 * shape.W;  // every lane evaluates its padded slots
     for (int gi = 0; gi < G; ++gi) {
       pe += (double)h_st[gi].trials * (double)gds[gi].N;
-      mo += slots * ((double)h_st[gi].shape_evals * mufu_shape[gi] + (double)h_st[gi].trials * mufu_per_noise(noise));
+      mo += slots * ((double)h_st[gi].shape_evals * mufu_shape[gi] + (double)h_st[gi].trials * mufu_per_noise(noise, shape.PPL));
     }
     g_stats.point_evals += pe;
     g_stats.move_mufu_ops += mo;
