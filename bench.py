@@ -22,12 +22,14 @@ CPU side), plus the time to log-evidence for K = 1..Kmax (time_to_evidence_s).
             clock per call (H2D of spectrum/priors, D2H of every posterior
             block, energies and diagnostics inside), max over ranks.
   roofline  the move kernel (k_chain<..., move, noise>, 97% of device time):
-            executed MUFU lane-ops/s (shape evaluations x MUFU per shape +
-            trials x MUFU per noise term, over the padded point slots, counted
-            by the library) from CUDA events around every move launch, against
-            the measured MUFU throughput of this GPU (specmc_probe_mufu).
-            algorithmic_frac credits SURVEY.md 8d's count instead (4 MUFU per
-            point-eval for pV + hetero noise, 3 for the Lorentzian basis).
+            ALGORITHMIC MUFU ops/s = point-evals/s (from CUDA events around
+            every move launch) x SURVEY.md 8d's MUFU per point-eval (4 for pV +
+            hetero noise, 3 for the Lorentzian basis, 1 for gm + Gaussian),
+            against the measured MUFU throughput of this GPU
+            (specmc_probe_mufu).  executed / executed_frac: the MUFU lane-ops
+            the kernel actually issues (counted by the library), fewer than
+            the algorithmic count (amplitude trials need no shape, four points
+            share one noise rcp and lg2).
   cpu_baseline  the reference itself (oracle/_ref: the unchanged reference
             sources, Release flags for this host's ISA), smc_run with
             workers = 0 (all host threads) on a bounded sample of the same
@@ -290,12 +292,15 @@ def roofline(S, b: Bench, st, peak_mufu):
             traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    return {"bound": "sfu", "achieved": ex / 1e9, "peak": peak_mufu / 1e9, "unit": "Gop/s (MUFU)",
-            "frac": ex / peak_mufu if peak_mufu else None, "traffic": traffic,
-            "algorithmic_frac": pe_rate * alg_pt / peak_mufu if peak_mufu else None,
-            "note": "move kernel: executed MUFU lane-ops/s (shape evaluations x MUFU per shape + trials x MUFU per "
-                    "noise term, padded slots) from CUDA events on the launch stream / measured MUFU peak of this "
-                    f"GPU (specmc_probe_mufu); algorithmic_frac = point-evals/s x {alg_pt:g} (SURVEY 8d) / peak"}, pe_rate
+    alg = pe_rate * alg_pt
+    return {"bound": "sfu", "achieved": alg / 1e9, "peak": peak_mufu / 1e9, "unit": "Gop/s (MUFU)",
+            "frac": alg / peak_mufu if peak_mufu else None, "traffic": traffic,
+            "executed": ex / 1e9, "executed_frac": ex / peak_mufu if peak_mufu else None,
+            "note": f"move kernel: algorithmic MUFU ops/s = point-evals/s (trials x N, CUDA events around every move "
+                    f"launch on its stream) x {alg_pt:g} MUFU per point-eval (SURVEY 8d: shape + noise term) / the "
+                    "measured MUFU peak of this GPU (specmc_probe_mufu); executed = the MUFU lane-ops the kernel "
+                    "issues (shape evaluations incl. block entries x MUFU per shape + trials x MUFU per noise "
+                    "term, padded slots; amplitude trials evaluate no shape, four points share a noise rcp/lg2)"}, pe_rate
 
 
 def problems_for(S, b: Bench, seed, device):
