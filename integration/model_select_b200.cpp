@@ -59,7 +59,7 @@ int main(int argc, char** argv) {
     }
     std::vector<std::pair<int, RunReport>> rows;
     for (size_t i = 0; i < reps.size(); ++i) {
-      std::printf("run K=%d trial=%d F=%.6f levels=%g diverged=%d draws=%ld\n", tag[i].first, tag[i].second,
+      std::printf("run K=%d trial=%d F=%.17g levels=%g diverged=%d draws=%ld\n", tag[i].first, tag[i].second,
                   reps[i].F, reps[i].scalars.at("levels"), (int)reps[i].diverged, (long)reps[i].posterior.cols());
       rows.emplace_back(tag[i].first, reps[i]);
     }

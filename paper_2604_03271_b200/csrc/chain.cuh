@@ -407,39 +407,15 @@ struct NoiseAcc {
   f2 quad, lg;
   float mn;
 };
-// numerator and variance product of slots a, b (component-wise, one point
-// pair per half): ra^2 vb + rb^2 va and va vb
-template <int NZ>
-__device__ __forceinline__ void noise_pairnum(const GroupDesc& g, f2 fa, f2 fb, f2 ya, f2 yb, f2& num, f2& vv,
-                                              float& mn) {
-  const f2 ra = add2(fa, ya), rb = add2(fb, yb);  // (f - y): the layout stores -y (only r^2 enters)
-  const f2 va = nz_var2<NZ>(g, fa), vb = nz_var2<NZ>(g, fb);
-  num = fma2(mul2(ra, ra), vb, mul2(mul2(rb, rb), va));
-  vv = mul2(va, vb);
-  mn = fminf(mn, fminf(fminf(va.x, va.y), fminf(vb.x, vb.y)));  // two FMNMX3
-}
 template <int NZ>
 __device__ __forceinline__ void noise_quad(const GroupDesc& g, f2 fa, f2 fb, f2 ya, f2 yb, NoiseAcc& a) {
-  f2 num, vv;
-  noise_pairnum<NZ>(g, fa, fb, ya, yb, num, vv, a.mn);
+  const f2 ra = add2(fa, ya), rb = add2(fb, yb);  // (f - y): the layout stores -y (only r^2 enters)
+  const f2 va = nz_var2<NZ>(g, fa), vb = nz_var2<NZ>(g, fb);
+  const f2 num = fma2(mul2(ra, ra), vb, mul2(mul2(rb, rb), va));
+  const f2 vv = mul2(va, vb);
   a.quad = fma2(num, rcpf2(vv), a.quad);
   a.lg = add2(a.lg, lg2f2(vv));
-}
-// four slots (two point pairs per half) share one rcp and one lg2 per half:
-// 1/2 MUFU per point.  The variance product of four points may leave the fp32
-// range (large counts with s1 > 0, or a model value near 0): the lane's sum is
-// then non-finite and lane_noise_sum reports a range fault, upon which the
-// caller redoes the lane with pairs (exact as before).
-template <int NZ>
-__device__ __forceinline__ void noise_oct(const GroupDesc& g, f2 fa, f2 fb, f2 fc, f2 fd, f2 ya, f2 yb, f2 yc, f2 yd,
-                                          NoiseAcc& a) {
-  f2 n1, v1, n2, v2;
-  noise_pairnum<NZ>(g, fa, fb, ya, yb, n1, v1, a.mn);
-  noise_pairnum<NZ>(g, fc, fd, yc, yd, n2, v2, a.mn);
-  const f2 num = fma2(n1, v2, mul2(n2, v1));
-  const f2 vv = mul2(v1, v2);
-  a.quad = fma2(num, rcpf2(vv), a.quad);
-  a.lg = add2(a.lg, lg2f2(vv));
+  a.mn = fminf(a.mn, fminf(fminf(va.x, va.y), fminf(vb.x, vb.y)));  // two FMNMX3
 }
 // the odd last slot of a lane with PH odd: its two points pair with each other
 template <int NZ>
@@ -457,23 +433,14 @@ __device__ __forceinline__ void noise_pair_h(const GroupDesc& g, f2 f, f2 y, Noi
 // (the lane's points >= nv) replicate the spectrum's last point, so npad copies
 // of the term at the lane's last point are removed at once.  Without CORR the
 // caller removes the padding terms (uniform xps layout, eval_shirley_uniform).
-// OCT (paired models): four slots per rcp / lg2; `range` is set when that
-// leaves the fp32 range (the caller then reruns the lane with OCT = false).
-template <int NZ, int PPL, int W, bool CORR = true, bool OCT = true, class F>
-__device__ __forceinline__ float lane_noise_sum(const GroupDesc& g, const Unit<PPL, W>& u, F&& fk, bool& range) {
+template <int NZ, int PPL, int W, bool CORR = true, class F>
+__device__ __forceinline__ float lane_noise_sum(const GroupDesc& g, const Unit<PPL, W>& u, F&& fk) {
   constexpr int PH = PPL / 2;
   NoiseAcc a{F2(0.f), F2(0.f), FLT_MAX};
   float flast = 0.f;
   if (nz_pairs<NZ>()) {
-    constexpr int k4 = OCT ? PH / 4 * 4 : 0;  // slots grouped by four
 #pragma unroll
-    for (int k = 0; k < k4; k += 4) {
-      const f2 fa = fk(k), fb = fk(k + 1), fc = fk(k + 2), fd = fk(k + 3);
-      noise_oct<NZ>(g, fa, fb, fc, fd, u.y2(k), u.y2(k + 1), u.y2(k + 2), u.y2(k + 3), a);
-      flast = fd.y;
-    }
-#pragma unroll
-    for (int k = k4; k + 1 < PH; k += 2) {
+    for (int k = 0; k + 1 < PH; k += 2) {
       const f2 fa = fk(k), fb = fk(k + 1);
       noise_quad<NZ>(g, fa, fb, u.y2(k), u.y2(k + 1), a);
       flast = fb.y;
@@ -502,27 +469,14 @@ __device__ __forceinline__ float lane_noise_sum(const GroupDesc& g, const Unit<P
     }
   }
   float acc;
-  range = false;
   if (nz_pairs<NZ>()) {
     const float t = fmaf(g.nz_q, a.quad.x + a.quad.y, a.lg.x + a.lg.y);
     acc = a.mn > 0.f ? t : __int_as_float(0x7fc00000);
-    range = OCT && a.mn > 0.f && !(fabsf(t) <= FLT_MAX);
   } else {
     acc = a.quad.x + a.quad.y;
   }
   if (!CORR) return acc;
   if (u.npad > 0.f) acc = fmaf(-u.npad, noise_term<NZ>(g, flast, make_float2(g.y_last, g.s_last)), acc);
-  return acc;
-}
-
-// lane_noise_sum with the four-slot grouping, redone with pairs on the
-// (rare) lanes whose grouped products left the fp32 range; gen() makes a
-// fresh slot generator (the generators carry running sums)
-template <int NZ, int PPL, int W, bool CORR = true, class G>
-__device__ __forceinline__ float lane_noise(const GroupDesc& g, const Unit<PPL, W>& u, G&& gen) {
-  bool range = false;
-  float acc = lane_noise_sum<NZ, PPL, W, CORR, true>(g, u, gen(), range);
-  if (nz_pairs<NZ>() && range) acc = lane_noise_sum<NZ, PPL, W, CORR, false>(g, u, gen(), range);
   return acc;
 }
 
@@ -534,7 +488,7 @@ __device__ __forceinline__ double finish_energy(const GroupDesc& g, double s) {
 
 template <int PPL, int W, int NZ>
 __device__ __forceinline__ double eval_plain_nz(const GroupDesc& g, Unit<PPL, W>& u, const f2 (&Pn)[PPL / 2]) {
-  const float acc = lane_noise<NZ>(g, u, [&]() { return [&](int k) { return Pn[k]; }; });
+  const float acc = lane_noise_sum<NZ>(g, u, [&](int k) { return Pn[k]; });
   return finish_energy<NZ>(g, unit_sum(u, acc));
 }
 
@@ -613,25 +567,19 @@ __device__ __forceinline__ double eval_shirley_uniform(const GroupDesc& g, Unit<
     const f2 m = F2(fmaf(-0.5f, scale, 1.f));
     // f_k = Pn_k + a + scale (R_k - P_0/2 - Pn_k/2) = B_k + m Pn_k with the
     // running background B_k = a + scale (R_k - P_0/2): two FFMA2 per slot
-    const f2 B0 = make_float2(fmaf(scale, prefix + init, bga), fmaf(scale, prefix + run.x, bga));
+    f2 B = make_float2(fmaf(scale, prefix + init, bga), fmaf(scale, prefix + run.x, bga));
     const f2 S = F2(scale);
-    f2 B;
-    acc = lane_noise<NZ, PPL, W, false>(g, u, [&]() {
-      B = B0;
-      return [&](int k) {
-        B = fma2(S, Pn[k], B);
-        return fma2(m, Pn[k], B);
-      };
+    acc = lane_noise_sum<NZ, PPL, W, false>(g, u, [&](int k) {
+      B = fma2(S, Pn[k], B);
+      return fma2(m, Pn[k], B);
     });
     fpad = u.tail ? fmaf(-scale, Pn[PH - 1].y, B.y) : B.y;
   } else {  // linear ramp a -> b (padding sits at x = 1e30: clamp to the last point)
     const float sl = ba * g.inv_range;
-    acc = lane_noise<NZ, PPL, W, false>(g, u, [&]() {
-      return [&](int k) {
-        const f2 x = u.x2(k);
-        const f2 xc = make_float2(fminf(x.x, g.x1s), fminf(x.y, g.x1s));
-        return add2(Pn[k], fma2(F2(sl), add2(xc, F2(-g.x0s)), F2(bga)));
-      };
+    acc = lane_noise_sum<NZ, PPL, W, false>(g, u, [&](int k) {
+      const f2 x = u.x2(k);
+      const f2 xc = make_float2(fminf(x.x, g.x1s), fminf(x.y, g.x1s));
+      return add2(Pn[k], fma2(F2(sl), add2(xc, F2(-g.x0s)), F2(bga)));
     });
     fpad = fmaf(sl, g.x1s - g.x0s, bga);
   }
@@ -668,26 +616,21 @@ __device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, 
     const float scale = ba * rcpf(total);
     const f2 base = make_float2(fmaf(scale, prefix, bga), fmaf(scale, prefix + run.x, bga));
     const f2 S = F2(scale);
-    f2 run2;
-    acc = lane_noise<NZ>(g, u, [&]() {
-      run2 = F2(0.f);
-      return [&](int k) {
-        f2 Ck;  // C_k = sum_{j<=k} c_j Pn_j - h_{k+1} Pn_k (lane-local part of each half)
-        if (kKeepC) {
-          Ck = Cn[kKeepC ? k : 0];
-        } else {
-          const float4 c = u.c4(k);
-          run2 = fma2(make_float2(c.x, c.y), Pn[k], run2);
-          Ck = fma2(make_float2(-c.z, -c.w), Pn[k], run2);
-        }
-        return add2(Pn[k], fma2(S, Ck, base));
-      };
+    f2 run2 = F2(0.f);
+    acc = lane_noise_sum<NZ>(g, u, [&](int k) {
+      f2 Ck;  // C_k = sum_{j<=k} c_j Pn_j - h_{k+1} Pn_k (lane-local part of each half)
+      if (kKeepC) {
+        Ck = Cn[kKeepC ? k : 0];
+      } else {
+        const float4 c = u.c4(k);
+        run2 = fma2(make_float2(c.x, c.y), Pn[k], run2);
+        Ck = fma2(make_float2(-c.z, -c.w), Pn[k], run2);
+      }
+      return add2(Pn[k], fma2(S, Ck, base));
     });
   } else {  // linear ramp a -> b
-    acc = lane_noise<NZ>(g, u, [&]() {
-      return [&](int k) {
-        return add2(Pn[k], fma2(F2(ba), mul2(add2(u.x2(k), F2(-g.x0s)), F2(g.inv_range)), F2(bga)));
-      };
+    acc = lane_noise_sum<NZ>(g, u, [&](int k) {
+      return add2(Pn[k], fma2(F2(ba), mul2(add2(u.x2(k), F2(-g.x0s)), F2(g.inv_range)), F2(bga)));
     });
   }
   // padding points (c = h = 0) replicate the spectrum's last point exactly

@@ -414,14 +414,8 @@ struct RunSpec;
 // gm ex2, xps ex2 + rcp, Lorentzian rcp, xrd (ex2 + rcp) per reflection
 double mufu_per_shape(int kfam, const RunSpec& R);
 // ... and of one evaluation's noise terms per point slot
-// (paired hetero models: four slots -- two points per half and pair -- share one
-// rcp and one lg2 per half, the leftover slots pair up: chain.cuh lane_noise_sum)
-double mufu_per_noise(int nz, int ppl) {
-  if (nz == NZ_GAUSS) return 0.0;
-  if (nz == NZ_POISSON) return 1.0;
-  const int ph = ppl / 2, k4 = ph / 4 * 4;
-  return (0.5 * k4 + 1.0 * (ph - k4)) / ph;
-}
+// (paired hetero models: two points share one rcp and one lg2)
+double mufu_per_noise(int nz, int /*ppl*/) { return nz == NZ_GAUSS ? 0.0 : 1.0; }
 
 PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, const double* ys, int64_t N,
                                   const Shape& s, double x_shift) {

@@ -50,9 +50,8 @@ def _cases():
         idx = np.linspace(0, len(sp.xs) - 1, n).round().astype(int)
         spn = M.Spectrum(np.linspace(sp.xs[0], sp.xs[-1], n), sp.ys[idx].copy())
         cases.append((f"xps2_n{n}", M.xps_model(2, spn), spn))
-    # counts ~1e8 with s1 > 0: variances ~1e12, so the four-point variance
-    # products of the noise sum leave the fp32 range and every lane takes the
-    # pairwise fallback (chain.cuh lane_noise)
+    # counts ~1e8 with s1 > 0 (variances ~1e12: the paired variance products
+    # ~1e24 stay inside the fp32 range)
     big = M.Spectrum(sp.xs.copy(), sp.ys * 3e4)
     cases.append(("xps3_hetero_1e8_counts", M.xps_model(3, big, M.XpsHeteroNoise(1.0, 0.01, 0.0)), big))
     xr, _ = syn.gen_xrd(600, 5)
