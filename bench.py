@@ -64,7 +64,7 @@ sys.path.insert(0, str(ROOT))
 MUFU_ALG = {("xps", False): 4.0, ("xps", True): 3.0, ("gm", False): 1.0}
 # reference-CPU sample per config: particles (and spectra for C4) per step
 CPU_SAMPLE = {"C1": dict(T=4096), "C2": dict(T=512), "C3": dict(T=512), "C4": dict(T=1024, spectra=4),
-              "C5": dict(T=128)}
+              "C5": dict(T=256)}
 WORKLOAD_TEXT = {
     "C1": "synthetic XPS-like spectrum, 3 Gaussian peaks (flat background as a known offset)",
     "C2": "synthetic XRD-like spectrum, 6 pseudo-Voigt peaks + Shirley",
