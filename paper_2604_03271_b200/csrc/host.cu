@@ -1542,42 +1542,55 @@ int run_sharded_batch(int n_problems, const specmc_problem* problems, int n_spec
 
 // ------------------------------------------------- multi-GPU model selection
 // Placement of a batch of runs (the K range of a model selection, SURVEY.md
-// 8e-1/8e-3) on `world` ranks.  Cost of a run = T d N (its proposals per level
-// times points; the level count grows only weakly with K).  A run costing more
-// than a rank's share L = sum / world is particle-sharded over s ranks (the
-// smallest power of two >= cost / L that divides T), placed on the aligned
-// block of s ranks with the least load; every other run goes to the least
-// loaded rank, longest first (LPT).  Deterministic: every rank computes the
-// same plan from the same inputs.
+// 8e-1/8e-3) on `world` ranks, by cost (run_cost: T d^1.5 N).  A run costing more
+// than alpha x a rank's share (sum / world) is particle-sharded over s ranks
+// (the smallest power of two >= cost / (alpha share) whose shards keep whole
+// chains), placed on the contiguous block of s ranks with the least load; every
+// other run goes to the least loaded rank, longest first (LPT).  The loads
+// charge a sharded run 3% per doubling for its exchanges; the plan with the
+// least makespan over alpha in {1, 0.85, 0.7, 0.55, 0.4} wins.  Deterministic:
+// every rank computes the same plan from the same inputs.
 struct Plan {
   std::vector<int> rank0, shards;
   std::vector<double> load;
   double makespan = 0.0;
 };
-Plan make_plan(int n, const double* cost, const int64_t* T, const int32_t* n_sweeps, int world) {
+// one placement with the sharding threshold alpha * share
+Plan place(int n, const double* cost, const int64_t* T, const int32_t* n_sweeps, int world, double alpha) {
   Plan p;
   p.rank0.assign(n, 0);
   p.shards.assign(n, 1);
   p.load.assign(world, 0.0);
   double total = 0.0;
   for (int i = 0; i < n; ++i) total += cost[i];
-  const double share = total / world;
-  std::vector<int> order(n);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  const double cut = alpha * total / world;
   int wpow = 1;
   while (wpow * 2 <= world) wpow *= 2;
-  for (int i : order) {
+  std::vector<int> sh(n, 1);
+  std::vector<double> piece(n);
+  for (int i = 0; i < n; ++i) {
     int s = 1;
-    if (world > 1 && cost[i] > share * (1.0 + 1e-9)) {
-      while (s < wpow && s * share < cost[i]) s *= 2;
+    if (world > 1 && cost[i] > cut * (1.0 + 1e-9)) {
+      while (s < wpow && s * cut < cost[i]) s *= 2;
       // every shard keeps whole chains: T / s divisible by n with >= 2 chains
       while (s > 1 && (T[i] % s != 0 || (T[i] / s) % n_sweeps[i] != 0 || T[i] / s / n_sweeps[i] < 2)) s /= 2;
     }
+    sh[i] = s;
+    // a sharded run pays its per-level exchanges: 3% per doubling of the shard count
+    piece[i] = cost[i] / s * (1.0 + 0.03 * std::log2((double)s));
+  }
+  // largest pieces first (LPT over the pieces; ties: more shards first)
+  std::vector<int> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return piece[a] != piece[b] ? piece[a] > piece[b] : sh[a] > sh[b];
+  });
+  for (int i : order) {
+    const int s = sh[i];
     int best = 0;
     if (s > 1) {
       double bl = 1e300;
-      for (int b = 0; b + s <= world; b += s) {
+      for (int b = 0; b + s <= world; ++b) {  // any contiguous block of s ranks
         double m = 0.0;
         for (int r = b; r < b + s; ++r) m = std::max(m, p.load[r]);
         if (m < bl) {
@@ -1585,11 +1598,11 @@ Plan make_plan(int n, const double* cost, const int64_t* T, const int32_t* n_swe
           best = b;
         }
       }
-      for (int r = best; r < best + s; ++r) p.load[r] += cost[i] / s;
+      for (int r = best; r < best + s; ++r) p.load[r] += piece[i];
     } else {
       for (int r = 1; r < world; ++r)
         if (p.load[r] < p.load[best]) best = r;
-      p.load[best] += cost[i];
+      p.load[best] += piece[i];
     }
     p.rank0[i] = best;
     p.shards[i] = s;
@@ -1598,8 +1611,27 @@ Plan make_plan(int n, const double* cost, const int64_t* T, const int32_t* n_swe
   return p;
 }
 
+// the placement with the least makespan over a few sharding thresholds (runs
+// above alpha x a rank's share are split; ties keep the larger alpha, i.e.
+// fewer shards)
+Plan make_plan(int n, const double* cost, const int64_t* T, const int32_t* n_sweeps, int world) {
+  Plan best;
+  bool have = false;
+  for (double alpha : {1.0, 0.85, 0.7, 0.55, 0.4}) {
+    Plan p = place(n, cost, T, n_sweeps, world, alpha);
+    if (!have || p.makespan < best.makespan * (1.0 - 1e-12)) {
+      best = std::move(p);
+      have = true;
+    }
+  }
+  return best;
+}
+
+// T d N per level times the level count, which grows about as sqrt(d) (the
+// reference's own C2 run, profiles/r02_cpu_c2_full.json: 20 levels at d = 6,
+// 57 at d = 42)
 double run_cost(const specmc_problem& pr, const specmc_spectrum* sps) {
-  return (double)pr.cfg.T * (double)pr.model.d * (double)sps[pr.spectrum].n;
+  return (double)pr.cfg.T * (double)pr.model.d * std::sqrt((double)pr.model.d) * (double)sps[pr.spectrum].n;
 }
 
 // The batch split over the ranks of `world` by make_plan: first the sharded
@@ -1639,22 +1671,32 @@ int run_distributed(int n_problems, const specmc_problem* problems, int n_spectr
   std::vector<specmc_problem> probs(problems, problems + n_problems);
   for (auto& p : probs) p.cfg.device = world->device;
   // 1) particle-sharded runs, one rank block at a time
+  // SPECMC_DIST_SHARD_ALL=1 (tests): every run takes the sharded path, even on
+  // a one-rank block -- the sub-communicator split and the NCCL exchanges then
+  // run on one GPU without any rank waiting on another
+  const bool shard_all = std::getenv("SPECMC_DIST_SHARD_ALL") && std::atoi(std::getenv("SPECMC_DIST_SHARD_ALL")) == 1;
+  auto sharded = [&](int i) { return plan.shards[i] > 1 || shard_all; };
   std::map<std::pair<int, int>, std::vector<int>> blocks;
   for (int i = 0; i < n_problems; ++i)
-    if (plan.shards[i] > 1) blocks[{plan.rank0[i], plan.shards[i]}].push_back(i);
+    if (sharded(i)) blocks[{plan.rank0[i], plan.shards[i]}].push_back(i);
   int first_bad = SPECMC_OK;
+  // every split first (collective over the world, in block order), so that
+  // disjoint blocks then run concurrently instead of waiting in the next split
+  for (auto& kv : blocks) {
+    const int b0 = kv.first.first, s = kv.first.second;
+    if (world->subs.count(kv.first)) continue;
+    if (!api.CommSplit) throw Error(SPECMC_ECOMM, "NCCL without ncclCommSplit (needs >= 2.18)");
+    const bool in = me >= b0 && me < b0 + s;
+    ncclComm_t sub = nullptr;
+    api.check(api.CommSplit(world->comm, in ? b0 * 4096 + s : NCCL_SPLIT_NOCOLOR, me, &sub, nullptr),
+              "ncclCommSplit");
+    world->subs.emplace(kv.first, sub);
+  }
   for (auto& kv : blocks) {
     const int b0 = kv.first.first, s = kv.first.second;
     const bool in = me >= b0 && me < b0 + s;
-    auto it = world->subs.find(kv.first);
-    if (it == world->subs.end()) {
-      if (!api.CommSplit) throw Error(SPECMC_ECOMM, "NCCL without ncclCommSplit (needs >= 2.18)");
-      ncclComm_t sub = nullptr;
-      api.check(api.CommSplit(world->comm, in ? b0 * 4096 + s : NCCL_SPLIT_NOCOLOR, me, &sub, nullptr),
-                "ncclCommSplit");
-      it = world->subs.emplace(kv.first, sub).first;
-    }
     if (!in) continue;
+    auto it = world->subs.find(kv.first);
     CommImpl sc;
     sc.comm = it->second;
     sc.rank = me - b0;
@@ -1671,7 +1713,7 @@ int run_distributed(int n_problems, const specmc_problem* problems, int n_spectr
   // 2) this rank's own runs
   std::vector<int> mine;
   for (int i = 0; i < n_problems; ++i)
-    if (plan.shards[i] == 1 && plan.rank0[i] == me) mine.push_back(i);
+    if (!sharded(i) && plan.rank0[i] == me) mine.push_back(i);
   if (!mine.empty()) {
     std::vector<specmc_problem> bp;
     for (int i : mine) bp.push_back(probs[i]);
@@ -1686,8 +1728,7 @@ int run_distributed(int n_problems, const specmc_problem* problems, int n_spectr
   constexpr int kF = 7;
   std::vector<double> h((size_t)kF * n_problems, 0.0);
   for (int i = 0; i < n_problems; ++i) {
-    const bool ran = plan.shards[i] > 1 ? (me >= plan.rank0[i] && me < plan.rank0[i] + plan.shards[i])
-                                        : me == plan.rank0[i];
+    const bool ran = sharded(i) ? (me >= plan.rank0[i] && me < plan.rank0[i] + plan.shards[i]) : me == plan.rank0[i];
     if (!ran) continue;
     double* r = h.data() + (size_t)kF * i;
     r[5] = (double)out[i].trials;  // local share of a sharded run
@@ -1951,7 +1992,7 @@ void specmc_comm_destroy(specmc_comm* c) {
   if (!p) return;
   for (auto& kv : p->subs) {
     try {
-      NcclApi::get().CommDestroy(kv.second);
+      if (kv.second) NcclApi::get().CommDestroy(kv.second);
     } catch (...) {
     }
   }

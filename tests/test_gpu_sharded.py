@@ -111,3 +111,23 @@ def test_distributed_one_rank_equals_batch(smc):
         assert a.F == b.F == c.F and a.trials == b.trials and a.proposals == b.proposals
         assert np.array_equal(a.posterior, b.posterior)
         assert a.scalars["levels"] == b.scalars["levels"]
+
+
+def test_distributed_sharded_path_one_rank_equals_unsharded(smc, monkeypatch):
+    """The distributed entry's sharded branch on one GPU: SPECMC_DIST_SHARD_ALL
+    sends every run through an ncclCommSplit sub-communicator and the NCCL
+    exchanges of the particle-sharded level loop (one-rank block); with one
+    shard that is the unsharded grid-tempering path, bitwise (T > 2^15)."""
+    w = syn.config("C1", 1 << 16)
+    probs = [(w.spec(K), 0, smc.SmcConfig(T=1 << 16, n=8, seed=21)) for K in (2, 3)]
+    ref = smc.smc_run_batch(probs, [w.data])
+    monkeypatch.setenv("SPECMC_DIST_SHARD_ALL", "1")
+    comm = smc.Comm(0, 1, smc.Comm.unique_id(), 0)
+    try:
+        reps, r0, sh = smc.smc_run_distributed(probs, [w.data], comm)
+    finally:
+        comm.close()
+    for a, b in zip(reps, ref):
+        assert a.F == b.F and a.trials == b.trials and a.scalars["levels"] == b.scalars["levels"]
+        assert np.array_equal(a.arrays["ladder"], b.arrays["ladder"])
+        assert np.array_equal(a.posterior, b.posterior)
