@@ -212,6 +212,55 @@ int specmc_smc_run_distributed(int32_t n_problems, const specmc_problem* problem
 int specmc_plan(int32_t n_runs, const double* costs, const int64_t* T, const int32_t* n_sweeps, int32_t world,
                 int32_t* rank0, int32_t* shards, double* rank_load, double* makespan);
 
+/* ---- replica exchange MC: the paper's comparator --
+ * RemcConfig (proj/include/specmc/remc.hpp:14-22): L replicas above beta = 0
+ * on the geometric ladder (remc.cpp:22-30) unless `ladder` (n_ladder entries,
+ * 0 ... 1, strictly increasing) is given; total_sweeps sweeps, the first
+ * round(burn_in_fraction * total_sweeps) adapting the step sizes
+ * (Robbins-Monro) and discarded; a swap step every swap_period sweeps.
+ * Results (RunReport of remc_run, remc.cpp:170-190): F = -sum_l log mean
+ * exp(-(beta_{l+1} - beta_l) N E_l) over the retained sweeps, the ladder, the
+ * swap rate per pair, the post-burn-in acceptance per replica and the
+ * beta = 1 draws (d x draws, column-major).  Every run of a batch executes
+ * concurrently: one chain unit per replica, one sweep of every replica per
+ * launch.  Parity with the reference's remc_run is statistical (Philox). */
+typedef struct {
+  int32_t L;
+  const double* ladder;
+  int32_t n_ladder;
+  int64_t total_sweeps;
+  double burn_in_fraction;
+  int64_t swap_period;
+  uint64_t seed;
+  int32_t workers; /* echoed only */
+  int32_t device;
+} specmc_remc_config;
+
+typedef struct {
+  specmc_model_desc model;
+  int32_t spectrum;
+  specmc_remc_config cfg;
+} specmc_remc_problem;
+
+typedef struct {
+  int32_t status;
+  double F;
+  int32_t diverged;
+  double wall_seconds;
+  double device_seconds;
+  int32_t R;          /* replicas (ladder entries) */
+  int32_t d;
+  int64_t draws;      /* retained sweeps */
+  double* ladder;     /* R */
+  double* swap_rate;  /* R - 1 */
+  double* replica_acc; /* R */
+  double* posterior;  /* d * draws */
+} specmc_remc_result;
+
+int specmc_remc_run_batch(int32_t n_problems, const specmc_remc_problem* problems, int32_t n_spectra,
+                          const specmc_spectrum* spectra, specmc_remc_result* out, char* err, size_t errlen);
+void specmc_remc_result_free(specmc_remc_result* r);
+
 /* ---- parity units (each runs the same device code as the sampler) ------ */
 
 /* Batched full energies E(theta) for fixed parameters: the K2 kernel.

@@ -296,6 +296,8 @@ class Ref:
         L.ref_xrd_model_priors.argtypes = [C.c_int, C.c_int, _ip, _dp, _dp, _dp, _dp, C.c_int64, _ip, _dp, _dp]
         L.ref_gen_xrd.argtypes = [C.c_int64, C.c_uint64, _dp, _dp]
         L.ref_model_select.argtypes = [C.c_int, _ip, _dp, _ip, _ip]
+        L.ref_remc_run.argtypes = [C.POINTER(_Model), C.c_int, C.c_int64, C.c_double, C.c_int64, C.c_uint64, C.c_int,
+                                   _dp, _ip, _dp, _dp, _dp, C.c_char_p, C.c_size_t]
         L.ref_bench_table.argtypes = [C.POINTER(C.c_char_p), C.c_int, C.c_char_p, C.c_char_p, C.c_size_t]
         L.ref_ci_table.argtypes = [C.POINTER(C.c_char_p), C.c_int, C.c_char_p, C.c_char_p, C.c_double, C.c_char_p,
                                    C.c_size_t]
@@ -435,6 +437,19 @@ class Ref:
         if rc:
             raise OracleError(rc, "model_select")
         return kb.value
+
+    def remc_run(self, m: OracleModel, L=44, total_sweeps=10000, burn_in_fraction=0.5, swap_period=1, seed=0,
+                 workers=1):
+        """remc_run(problem, cfg) (remc.cpp:78-163): (F, diverged, swap_rate[L], replica_acc[L + 1], wall)"""
+        s = m.struct()
+        F, dv, wall = C.c_double(), C.c_int(), C.c_double()
+        sr, ra = np.zeros(L), np.zeros(L + 1)
+        err = C.create_string_buffer(512)
+        rc = self.lib.ref_remc_run(C.byref(s), L, total_sweeps, burn_in_fraction, swap_period, seed, workers,
+                                   C.byref(F), C.byref(dv), _ptr(sr), _ptr(ra), C.byref(wall), err, 512)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return F.value, bool(dv.value), sr, ra, wall.value
 
     def bench_table(self, paths, reference_label="") -> str:
         """bench_table_text(table_from_reports(read_report(p) for p in paths)) (bench.cpp:147-327)"""

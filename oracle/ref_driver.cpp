@@ -466,6 +466,37 @@ int ref_write_report(const char* path, const char* sampler, const char* label, d
   }
 }
 
+// ---- replica exchange (remc.cpp:78-190): F, swap rates, replica acceptance
+#include "specmc/remc.hpp"
+int ref_remc_run(const ref_model* m, int L, int64_t total_sweeps, double burn, int64_t swap_period, uint64_t seed,
+                 int workers, double* F, int* diverged, double* swap_rate, double* replica_acc, double* wall, char* err,
+                 size_t errlen) {
+  try {
+    RemcConfig cfg;
+    cfg.L = L;
+    cfg.total_sweeps = total_sweeps;
+    cfg.burn_in_fraction = burn;
+    cfg.swap_period = swap_period;
+    cfg.seed = seed;
+    cfg.workers = workers;
+    RemcResult r;
+    if (m->family == FAM_OFFSET) {
+      r = remc_run(conjugate_problem(m->ys, m->n, m->sigma, m->prior_a[0], m->prior_b[0]), cfg);
+    } else {
+      ModelSpec spec = REF_SPEC(m);
+      r = remc_run(make_problem(spec, make_data(m->xs, m->ys, m->n)), cfg);
+    }
+    *F = r.F;
+    *diverged = r.diverged;
+    *wall = r.wall_seconds;
+    for (Index i = 0; i < r.swap_rate.size(); ++i) swap_rate[i] = r.swap_rate[i];
+    for (Index i = 0; i < r.replica_acc.size(); ++i) replica_acc[i] = r.replica_acc[i];
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, err, errlen);
+  }
+}
+
 // ---- benchmark tables (bench.cpp:147-338) over persisted reports
 namespace {
 int copy_out(const std::string& s, char* out, size_t outlen) {

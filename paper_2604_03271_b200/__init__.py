@@ -11,7 +11,8 @@ from .report import (credible_interval, format_double, parse_double, read_report
                      weighted_quantile, write_report)
 from .smc import (Comm, CudaError, ModelChoice, RunReport, Session, SmcConfig, probe_mufu, device_count, energies, energy, ess,
                   launch_shape, log_mean_exp, model_select, next_beta, predict_step_size, smc_run, smc_run_batch,
-                  stats, stats_reset, systematic_resample, validate_smc_config, smc_run_sharded, smc_run_sharded_batch, init_ensemble, smc_run_distributed, plan)
+                  stats, stats_reset, systematic_resample, validate_smc_config, smc_run_sharded, smc_run_sharded_batch, init_ensemble, smc_run_distributed, plan,
+                  RemcConfig, remc_run, remc_run_batch)
 
 __all__ = [
     "GammaPrior", "GaussianApproxPoissonNoise", "GaussianFixedNoise", "ModelSpec", "NormalPrior", "PoissonNoise",
@@ -19,5 +20,5 @@ __all__ = [
     "prior_scale", "xps_model", "xrd_model", "PhaseRef", "Reflection", "CudaError", "ModelChoice", "RunReport", "Session", "SmcConfig", "probe_mufu", "device_count", "energies",
     "energy", "ess", "launch_shape", "log_mean_exp", "model_select", "next_beta", "predict_step_size", "smc_run",
     "write_report", "read_report", "format_double", "parse_double", "weighted_quantile", "credible_interval",
-    "sort_peak_blocks", "smc_run_batch", "smc_run_sharded", "smc_run_sharded_batch", "init_ensemble", "smc_run_distributed", "plan", "Comm", "stats", "stats_reset", "systematic_resample", "validate_smc_config",
+    "sort_peak_blocks", "smc_run_batch", "smc_run_sharded", "smc_run_sharded_batch", "init_ensemble", "smc_run_distributed", "plan", "RemcConfig", "remc_run", "remc_run_batch", "Comm", "stats", "stats_reset", "systematic_resample", "validate_smc_config",
 ]

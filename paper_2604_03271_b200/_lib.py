@@ -40,12 +40,28 @@ class SmcResultC(C.Structure):
                 ("posterior", _dp), ("energies", _dp), ("proposals", C.c_int64), ("trials", C.c_int64)]
 
 
+class RemcConfigC(C.Structure):
+    _fields_ = [("L", C.c_int32), ("ladder", _dp), ("n_ladder", C.c_int32), ("total_sweeps", C.c_int64),
+                ("burn_in_fraction", C.c_double), ("swap_period", C.c_int64), ("seed", C.c_uint64),
+                ("workers", C.c_int32), ("device", C.c_int32)]
+
+
+class RemcResultC(C.Structure):
+    _fields_ = [("status", C.c_int32), ("F", C.c_double), ("diverged", C.c_int32), ("wall_seconds", C.c_double),
+                ("device_seconds", C.c_double), ("R", C.c_int32), ("d", C.c_int32), ("draws", C.c_int64),
+                ("ladder", _dp), ("swap_rate", _dp), ("replica_acc", _dp), ("posterior", _dp)]
+
+
 class ProblemC(C.Structure):
     _fields_ = [("model", ModelDesc), ("spectrum", C.c_int32), ("cfg", SmcConfigC)]
 
 
 class SpectrumC(C.Structure):
     _fields_ = [("xs", _dp), ("ys", _dp), ("n", C.c_int64)]
+
+
+class RemcProblemC(C.Structure):
+    _fields_ = [("model", ModelDesc), ("spectrum", C.c_int32), ("cfg", RemcConfigC)]
 
 
 class StatsC(C.Structure):
@@ -61,7 +77,8 @@ EXPORTS = [
     "specmc_launch_shape", "specmc_device_count", "specmc_version", "specmc_session_create", "specmc_session_run",
     "specmc_session_fetch", "specmc_session_destroy", "specmc_probe_mufu", "specmc_smc_run_sharded",
     "specmc_nccl_unique_id", "specmc_comm_init_nccl", "specmc_comm_destroy", "specmc_init_ensemble",
-    "specmc_smc_run_sharded_batch", "specmc_smc_run_distributed", "specmc_plan",
+    "specmc_smc_run_sharded_batch", "specmc_smc_run_distributed", "specmc_plan", "specmc_remc_run_batch",
+    "specmc_remc_result_free",
 ]
 SPECMC_COMM_ID_BYTES = 128
 
@@ -102,6 +119,11 @@ def _load():
         lib.specmc_smc_run_distributed.argtypes = [C.c_int32, C.POINTER(ProblemC), C.c_int32, C.POINTER(SpectrumC),
                                                    C.c_void_p, _ip, _ip, C.POINTER(SmcResultC), E, Z]
         lib.specmc_plan.argtypes = [C.c_int32, _dp, _lp, _ip, C.c_int32, _ip, _ip, _dp, _dp]
+    if hasattr(lib, "specmc_remc_run_batch"):
+        lib.specmc_remc_run_batch.argtypes = [C.c_int32, C.POINTER(RemcProblemC), C.c_int32, C.POINTER(SpectrumC),
+                                              C.POINTER(RemcResultC), E, Z]
+        lib.specmc_remc_result_free.argtypes = [C.POINTER(RemcResultC)]
+        lib.specmc_remc_result_free.restype = None
     lib.specmc_result_free.argtypes = [C.POINTER(SmcResultC)]
     lib.specmc_result_free.restype = None
     lib.specmc_free.argtypes = [C.c_void_p]

@@ -708,7 +708,7 @@ struct Bounds {
 // The level's work for one chain unit (initial energy, then the move kernel's
 // n sweeps), with the noise model NZ fixed at compile time for the move
 // kernels: the sweep loop holds a single evaluation variant.
-template <int FAM, int PPL, int W, bool ENERGY, int NZ>
+template <int FAM, int PPL, int W, bool ENERGY, int NZ, bool REMC = false>
 __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, const int c, const int unit,
                                            const int wiu, const int lane, const GroupState* st, const int cur,
                                            const int d, const int T, double* th, double* lsv, int* acc, double* nvb,
@@ -730,14 +730,16 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
   }
 
   // ---- waste-free chain: n sweeps at beta_next, every post-sweep state kept
-  const int n = g.n, S = g.S;
+  // (REMC: one sweep of replica c at its ladder beta, sweep index t = st->level,
+  // Robbins-Monro while t <= n_burn (remc.cpp:125-133), state updated in place)
+  const int n = REMC ? 1 : g.n, S = g.S;
   const int level = st->level;
-  const double beta = st->beta;
+  const double beta = REMC ? g.ladder[c] : st->beta;
   const double nd = g.n_data;
   const int adapt_sweeps = (n + 1) / 2;  // smc.cpp:136
   const uint32_t cg = g.chain_base + (uint32_t)(st->chain_lo + c);  // global chain id
-  double* thn = g.theta[cur ^ 1];
-  double* En = g.E[cur ^ 1];
+  double* thn = g.theta[REMC ? cur : cur ^ 1];
+  double* En = g.E[REMC ? cur : cur ^ 1];
   // components inside a block (everything but the xps Shirley endpoints and the offset family)
   const int npeak = FAM == FAM_OFFSET ? 0 : (FAM == FAM_XRD ? g.d : stride * g.K);
   unsigned trials = 0, shape_evals = 0;  // shape_evals: block-entry and trial shape evaluations (MUFU count)
@@ -762,8 +764,9 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
     // check (mcmc.cpp:61-68) and the Philox draws are all fixed at sweep start.
     for (int i = lane; i < d; i += 32) {
       // counter (t-1) d + i < n d <= 2^32 (make_runspec rejects larger n d): unsigned, no wrap
-      const u32x4 o = philox(u32x4{cg, (uint32_t)level, (uint32_t)(t - 1) * (uint32_t)d + (uint32_t)i, ROLE_CHAIN},
-                             g.key0, g.key1);
+      const u32x4 o = REMC ? philox(u32x4{cg, (uint32_t)level, (uint32_t)i, ROLE_REMC}, g.key0, g.key1)
+                           : philox(u32x4{cg, (uint32_t)level, (uint32_t)(t - 1) * (uint32_t)d + (uint32_t)i, ROLE_CHAIN},
+                                    g.key0, g.key1);
       const double old_i = th[i];
       const double nv = old_i + (double)__expf((float)lsv[i]) * (double)normal_f32(o.x, o.y);
       double dlp = 0.0;
@@ -887,18 +890,20 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
     // These are read-modify-writes of the unit's shared state: warp 0 alone does them
     // (the other warps read lsv after the unit barrier that opens the next sweep).
     if (wiu == 0) {
-      const float gam = (t <= adapt_sweeps) ? exp2f(-0.6f * log2f((float)t)) : 0.f;  // t^-0.6
+      const bool adapt = REMC ? (long long)level <= g.n_burn : t <= adapt_sweeps;
+      const int ta = REMC ? level : t;  // the RM clock: sweep of the level (SMC) or of the run (REMC)
+      const float gam = adapt ? exp2f(-0.6f * log2f((float)ta)) : 0.f;  // t^-0.6
       for (int i = lane; i < d; i += 32) {
         const int a = flg[i] >> 1;
         acc[i] += a;
-        if (t <= adapt_sweeps) {
+        if (adapt) {
           const double ls = lsv[i] + (double)gam * ((double)a - 0.5);
           lsv[i] = fmin(fmax(ls, kLogStepMin), kLogStepMax);
         }
       }
     }
     __syncwarp();
-    const size_t slot = (size_t)c * n + (t - 1);  // smc.cpp:151
+    const size_t slot = REMC ? (size_t)c : (size_t)c * n + (t - 1);  // smc.cpp:151 (REMC: in place)
     if (wiu == 0) {
       for (int i = lane; i < d; i += 32) thn[(size_t)i * g.tp + slot] = th[i];
       if (lane == 0) En[slot] = e;
@@ -906,7 +911,10 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
   }
   if (wiu == 0) {
     for (int i = lane; i < d; i += 32) {
-      g.chain_acc[(size_t)i * g.sp + c] = acc[i];
+      if (REMC)  // tallies accumulate over the run (reset at the end of burn-in)
+        g.chain_acc[(size_t)i * g.sp + c] += acc[i];
+      else
+        g.chain_acc[(size_t)i * g.sp + c] = acc[i];
       g.chain_ls[(size_t)i * g.sp + c] = lsv[i];
     }
   }
@@ -920,7 +928,7 @@ __device__ __forceinline__ void chain_body(const GroupDesc& g, Unit<PPL, W>& u, 
   }
 }
 
-template <int FAM, int PPL, int W, bool ENERGY, int NZ>
+template <int FAM, int PPL, int W, bool ENERGY, int NZ, bool REMC = false>
 __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_blocks)
     k_chain(const GroupDesc* __restrict__ gds, const int* __restrict__ list, const int* __restrict__ cta_prefix,
             int n_list, int U, int dpad) {
@@ -1003,28 +1011,28 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   const int cur = st->cur;
   const int d = g.d, T = g.T;
   const double* thc = g.theta[cur];
-  const int src = ENERGY ? c : g.anc[c];
+  const int src = (ENERGY || REMC) ? c : g.anc[c];
   for (int i = lane; i < d; i += 32) {
     th[i] = thc[(size_t)i * g.tp + src];
     thf[i] = (float)th[i];
     if (!ENERGY) {
-      lsv[i] = g.ls0[i];
+      lsv[i] = REMC ? g.chain_ls[(size_t)i * g.sp + c] : g.ls0[i];  // REMC: the replica's own step sizes
       acc[i] = 0;
     }
   }
   __syncwarp();
 
-  chain_body<FAM, PPL, W, ENERGY, NZ>(g, u, c, unit, wiu, lane, st, cur, d, T, th, lsv, acc, nvb, dlpb, lub, flg, thf,
+  chain_body<FAM, PPL, W, ENERGY, NZ, REMC>(g, u, c, unit, wiu, lane, st, cur, d, T, th, lsv, acc, nvb, dlpb, lub, flg, thf,
                                       nvf, gcache, pcache);
 }
 
 // ------------------------------------------------------------------ launch
-template <int FAM, int PPL, int W, bool ENERGY, int NZ>
+template <int FAM, int PPL, int W, bool ENERGY, int NZ, bool REMC = false>
 cudaError_t launch_chain_t(int U, int lay, int dmax, const GroupDesc* gds, const int* list, const int* prefix,
                            int n_list, int total_ctas, cudaStream_t st) {
   const int dpad = (dmax + 1) & ~1;
   const size_t smem = Smem<PPL, W>::bytes(U, dpad, lay);
-  auto kern = k_chain<FAM, PPL, W, ENERGY, NZ>;
+  auto kern = k_chain<FAM, PPL, W, ENERGY, NZ, REMC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1042,11 +1050,11 @@ cudaError_t launch_chain_t(int U, int lay, int dmax, const GroupDesc* gds, const
   X(2, 10) X(2, 12) X(2, 14) X(2, 16) X(2, 20) X(2, 24) X(2, 28) X(2, 32)                             \
   X(4, 20) X(4, 24) X(4, 28) X(4, 32) X(8, 20) X(8, 24) X(8, 28) X(8, 32)
 
-template <int FAM, bool ENERGY, int NZ>
+template <int FAM, bool ENERGY, int NZ, bool REMC = false>
 cudaError_t launch_chain_fam(const Shape& s, int dmax, const GroupDesc* gds, const int* list, const int* prefix,
                              int n_list, int total_ctas, cudaStream_t st) {
 #define SMC_CASE(WW, PP) \
-  if (s.W == WW && s.PPL == PP) return launch_chain_t<FAM, PP, WW, ENERGY, NZ>(s.U, s.lay, dmax, gds, list, prefix, n_list, total_ctas, st);
+  if (s.W == WW && s.PPL == PP) return launch_chain_t<FAM, PP, WW, ENERGY, NZ, REMC>(s.U, s.lay, dmax, gds, list, prefix, n_list, total_ctas, st);
   SMC_FOR_EACH_SHAPE(SMC_CASE)
 #undef SMC_CASE
   return cudaErrorInvalidValue;

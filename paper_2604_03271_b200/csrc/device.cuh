@@ -24,7 +24,7 @@ namespace smc {
 enum Family : int { FAM_GM = 0, FAM_XPS = 1, FAM_XRD = 2, FAM_OFFSET = 3 };
 enum NoiseDev : int { NZ_DYN = -1, NZ_GAUSS = 0, NZ_HETERO = 1, NZ_POISSON = 2, NZ_HLIN = 3, NZ_HPROP = 4 };
 enum PriorKind : int { PR_NORMAL = 0, PR_GAMMA = 1, PR_UNIFORM = 2 };
-enum Role : uint32_t { ROLE_INIT = 1, ROLE_CHAIN = 2, ROLE_RESAMPLE = 3 };
+enum Role : uint32_t { ROLE_INIT = 1, ROLE_CHAIN = 2, ROLE_RESAMPLE = 3, ROLE_REMC = 4, ROLE_SWAP = 5 };
 enum GroupError : int { GE_NONE = 0, GE_MAX_LEVELS = 1, GE_ZERO_WEIGHT = 2 };
 
 constexpr int kHist = 5;       // predict_step_size window (mcmc.cpp:28)
@@ -124,6 +124,13 @@ struct GroupDesc {  // immutable per group
   int nslices;        // slices of the grid-level tempering (0: single-CTA path)
   int slice_len;
   double* stat_acc;   // [2d] per-component accept sums and log-step sums of the level (k_stats_grid)
+  // replica-exchange runs (REMC comparator, remc.cpp): one chain unit per
+  // replica; T = S = R replicas, st->level = the current sweep t (1-based)
+  const double* ladder;  // [R] inverse temperatures beta_0 = 0 < ... < beta_{R-1} = 1
+  double* pair_acc;      // [R-1][2] running (max, scaled sum) of exp(tempered_term) after burn-in
+  int* swaps;            // [R-1][2] (accepts, attempts)
+  double* post;          // [d][draws] beta = 1 draws after burn-in
+  long long n_burn, total_sweeps, swap_period;
 };
 
 // ----------------------------------------------------------------- Philox4x32-10

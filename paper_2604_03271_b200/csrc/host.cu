@@ -1540,6 +1540,310 @@ int run_sharded_batch(int n_problems, const specmc_problem* problems, int n_spec
   return first_bad;
 }
 
+// ----------------------------------------------------- replica exchange MC
+// The paper's comparator (remc.cpp:78-163) on the device: every run of the
+// batch is a group whose T = S = R replicas are chain units; per sweep one
+// launch of k_chain in REMC mode over every replica of every run, then
+// k_remc_exchange (swaps, accumulators, draws, sweep counter).  Runs are
+// classed like SMC runs (family, noise, launch shape); the host enqueues all
+// sweeps without waiting and reads the accumulators once at the end.
+std::vector<double> remc_ladder(const specmc_remc_config& c) {  // remc.cpp:22-41
+  std::vector<double> b;
+  if (c.n_ladder > 0) {
+    if (!c.ladder) throw Error(SPECMC_EINVAL, "remc: null ladder");
+    b.assign(c.ladder, c.ladder + c.n_ladder);
+    if (b.size() < 2) throw Error(SPECMC_EINVAL, "remc: explicit ladder needs >= 2 entries");
+    if (b[0] != 0.0) throw Error(SPECMC_EINVAL, "remc: ladder must start at beta = 0");
+    if (b.back() != 1.0) throw Error(SPECMC_EINVAL, "remc: ladder must end at beta = 1");
+    for (size_t i = 1; i < b.size(); ++i)
+      if (!(b[i] > b[i - 1])) throw Error(SPECMC_EINVAL, "remc: ladder must be strictly increasing");
+    return b;
+  }
+  if (c.L < 1) throw Error(SPECMC_EINVAL, "remc: L must be >= 1");
+  b.assign(c.L + 1, 0.0);
+  for (int j = 1; j <= c.L; ++j)
+    b[j] = c.L == 1 ? 1.0 : std::pow(10.0, -5.0 * (double)(c.L - j) / (double)(c.L - 1));
+  b[c.L] = 1.0;
+  return b;
+}
+
+void validate_remc(const specmc_remc_config& c) {  // remc.cpp:43-51
+  remc_ladder(c);
+  if (c.total_sweeps < 1) throw Error(SPECMC_EINVAL, "remc: total_sweeps must be >= 1");
+  if (!(c.burn_in_fraction > 0.0 && c.burn_in_fraction < 1.0))
+    throw Error(SPECMC_EINVAL, "remc: burn_in_fraction must lie in (0, 1)");
+  if (c.swap_period < 1) throw Error(SPECMC_EINVAL, "remc: swap_period must be >= 1");
+  if (c.workers < 0) throw Error(SPECMC_EINVAL, "remc: workers must be >= 0");
+  if (c.total_sweeps > ((int64_t)1 << 31) - 2) throw Error(SPECMC_EINVAL, "remc: total_sweeps above 2^31");
+}
+
+int run_remc_batch(int n, const specmc_remc_problem* problems, int n_spectra, const specmc_spectrum* sps,
+                   specmc_remc_result* out) {
+  const auto t0 = std::chrono::steady_clock::now();
+  if (n < 1 || !problems) throw Error(SPECMC_EINVAL, "remc batch: no problems");
+  if (n_spectra < 1 || !sps) throw Error(SPECMC_EINVAL, "remc batch: no spectra");
+  std::vector<RunSpec> runs;
+  std::vector<std::vector<double>> ladders;
+  const int device = problems[0].cfg.device;
+  for (int i = 0; i < n; ++i) {
+    const auto& p = problems[i];
+    if (p.spectrum < 0 || p.spectrum >= n_spectra) throw Error(SPECMC_EINVAL, "batch: spectrum index out of range");
+    if (p.cfg.device != device) throw Error(SPECMC_EINVAL, "batch: all problems must target the same device");
+    validate_remc(p.cfg);
+    ladders.push_back(remc_ladder(p.cfg));
+    const int R = (int)ladders.back().size();
+    specmc_smc_config sc{R, 1, 0.5, 1, p.cfg.seed, p.cfg.workers, device};  // T = S = R replicas
+    runs.push_back(make_runspec(p.model, p.spectrum, sc, sps[p.spectrum]));
+  }
+  Device dev(device);
+  cudaStream_t st = dev.stream;
+  std::map<std::tuple<int, int, int>, std::vector<int>> cls;
+  for (int i = 0; i < n; ++i) {
+    const Shape s = pick_shape(runs[i].N, runs[i].m.d);
+    cls[{runs[i].m.family, dev_noise(runs[i].m), s.W * 100 + s.PPL}].push_back(i);
+  }
+  Timer whole;
+  cuda_check(cudaEventRecord(whole.a, st), "event");
+  struct Done {
+    GroupDesc g;
+    GroupState* d_st;
+    int64_t draws;
+  };
+  std::vector<Done> done(n);
+  std::vector<std::unique_ptr<Arena>> arenas;
+  for (auto& kv : cls) {
+    const std::vector<int>& idx = kv.second;
+    const int G = (int)idx.size();
+    int64_t Nmax = 0;
+    int dmax = 1;
+    for (int r : idx) {
+      Nmax = std::max(Nmax, runs[r].N);
+      dmax = std::max(dmax, runs[r].m.d);
+    }
+    Shape shape = pick_shape(Nmax, dmax);
+    if ((int64_t)32 * shape.W * shape.PPL < Nmax)
+      throw Error(SPECMC_EINVAL, "spectrum has more points than the device path supports (8192)");
+    const int family = runs[idx[0]].m.family, noise = dev_noise(runs[idx[0]].m);
+    std::map<SpecKey, PreparedSpectrum> prep;
+    for (int r : idx) {
+      const auto key = spec_key(runs[r]);
+      if (!prep.count(key)) {
+        const auto& sp = sps[runs[r].spectrum];
+        prep.emplace(key, prepare_spectrum(runs[r].m, sp.xs, sp.ys, sp.n, shape, runs[r].x_shift));
+      }
+    }
+    shape.lay = spectrum_layout(family, noise, prep);
+    if (chain_smem_bytes(shape, dmax) > kChainSmemMax)
+      throw Error(SPECMC_EINVAL, "model too large for the device path (shared memory)");
+    const size_t npt = (size_t)shape.PPL * 32 * shape.W;
+    size_t bytes = Arena::al(sizeof(GroupDesc) * G) + Arena::al(sizeof(GroupState) * G) + 2 * Arena::al(4 * (G + 1));
+    bytes += prep.size() * (Arena::al(npt * 4) + 2 * Arena::al(npt * 8));
+    for (int gi = 0; gi < G; ++gi) {
+      const RunSpec& R = runs[idx[gi]];
+      const size_t Rn = ladders[idx[gi]].size(), d = R.m.d, tp = row_pitch(Rn);
+      const int64_t nb = std::min<int64_t>(std::max<int64_t>(std::llround(problems[idx[gi]].cfg.burn_in_fraction *
+                                                                          (double)problems[idx[gi]].cfg.total_sweeps), 0),
+                                           problems[idx[gi]].cfg.total_sweeps - 1);
+      const size_t draws = (size_t)(problems[idx[gi]].cfg.total_sweeps - nb);
+      bytes += 3 * Arena::al(d * 8) + Arena::al(d * 4) + Arena::al(d * tp * 8) + Arena::al(Rn * 8);
+      bytes += Arena::al(d * tp * 4) + Arena::al(d * tp * 8) + Arena::al(Rn * 8) + Arena::al(2 * Rn * 8);
+      bytes += Arena::al(2 * Rn * 4) + Arena::al(d * draws * 8) + Arena::al(R.refl.size() * 4 + 8) +
+               Arena::al(R.refl_off.size() * 4 + 4);
+    }
+    arenas.push_back(std::make_unique<Arena>());
+    Arena& ar = *arenas.back();
+    ar.reserve(bytes, dev.ordinal, st);
+    cuda_check(prime_level_kernels(family, noise, shape, dmax), "loading the level kernels");
+    GroupDesc* d_gds = ar.take<GroupDesc>(G);
+    GroupState* d_st = ar.take<GroupState>(G);
+    int* d_list = ar.take<int>(G + 1);
+    int* d_prefix = ar.take<int>(G + 1);
+    std::map<SpecKey, std::tuple<float*, float2*, float2*>> dspec;
+    for (auto& p : prep) {
+      float* x = ar.take<float>(npt);
+      float2* c = ar.take<float2>(npt);
+      float2* y = ar.take<float2>(npt);
+      h2d(x, p.second.x.data(), npt, st);
+      h2d(reinterpret_cast<float*>(c), p.second.c.data(), 2 * npt, st);
+      h2d(reinterpret_cast<float*>(y), p.second.y.data(), 2 * npt, st);
+      dspec[p.first] = std::make_tuple(x, c, y);
+    }
+    std::vector<GroupDesc> gds(G);
+    std::vector<GroupState> sts(G);
+    std::vector<int> list(G), prefix(G + 1);
+    int total = 0;
+    for (int gi = 0; gi < G; ++gi) {
+      const int ri = idx[gi];
+      const RunSpec& R = runs[ri];
+      const auto& lad = ladders[ri];
+      const int Rn = (int)lad.size(), d = R.m.d;
+      const PreparedSpectrum& ps = prep.at(spec_key(R));
+      GroupDesc& g = gds[gi];
+      std::memset(&g, 0, sizeof(g));
+      g.family = R.m.family;
+      g.K = R.m.K;
+      g.d = d;
+      g.noise = ps.nz;
+      g.T = g.S = Rn;
+      g.n = 1;
+      g.max_levels = 1;
+      g.n_data = (double)R.N;
+      const uint64_t k = mix64(R.cfg.seed);
+      g.key0 = (uint32_t)k;
+      g.key1 = (uint32_t)(k >> 32);
+      g.N = (int)R.N;
+      g.e_a0 = ps.e_a0;
+      g.e_a1 = ps.e_a1;
+      g.nz_a0 = ps.a0;
+      g.nz_a1 = ps.a1;
+      g.nz_a2 = ps.a2;
+      g.nz_q = ps.q;
+      g.x0s = ps.x0s;
+      g.inv_range = ps.inv_range;
+      g.range = ps.range;
+      g.sh_uniform = ps.uniform ? 1 : 0;
+      g.x1s = ps.x1s;
+      g.y_last = ps.y_last;
+      g.s_last = ps.s_last;
+      auto t = dspec.at(spec_key(R));
+      g.spec_x = std::get<0>(t);
+      g.spec_c = std::get<1>(t);
+      g.spec_y = std::get<2>(t);
+      int* pk = ar.take<int>(d);
+      double* pa = ar.take<double>(d);
+      double* pb = ar.take<double>(d);
+      h2d(pk, R.pk.data(), d, st);
+      h2d(pa, R.pa.data(), d, st);
+      h2d(pb, R.pb.data(), d, st);
+      g.pkind = pk;
+      g.pa = pa;
+      g.pb = pb;
+      g.tp = g.sp = (int)row_pitch(Rn);
+      g.theta[0] = g.theta[1] = ar.take<double>((size_t)d * g.tp);
+      g.E[0] = g.E[1] = ar.take<double>(Rn);
+      g.chain_acc = ar.take<int>((size_t)d * g.sp);
+      g.chain_ls = ar.take<double>((size_t)d * g.sp);
+      double* lad_d = ar.take<double>(Rn);
+      h2d(lad_d, lad.data(), Rn, st);
+      g.ladder = lad_d;
+      g.pair_acc = ar.take<double>(2 * (size_t)Rn);
+      g.swaps = ar.take<int>(2 * (size_t)Rn);
+      const auto& c = problems[ri].cfg;
+      g.total_sweeps = c.total_sweeps;
+      g.n_burn = std::min<int64_t>(std::max<int64_t>(std::llround(c.burn_in_fraction * (double)c.total_sweeps), 0),
+                                   c.total_sweeps - 1);
+      g.swap_period = c.swap_period;
+      const int64_t draws = c.total_sweeps - g.n_burn;
+      g.post = ar.take<double>((size_t)d * draws);
+      if (!R.refl.empty()) {
+        float2* rf = ar.take<float2>(R.refl.size() / 2);
+        int* ro = ar.take<int>(R.refl_off.size());
+        h2d(reinterpret_cast<float*>(rf), R.refl.data(), R.refl.size(), st);
+        h2d(ro, R.refl_off.data(), R.refl_off.size(), st);
+        g.refl = rf;
+        g.refl_off = ro;
+      }
+      g.st = d_st + gi;
+      // initial step sizes clamp(prior_scale) (mcmc.cpp:7-12) for every replica; tallies 0;
+      // accumulators (max, sum) = (-inf, 0); swap tallies 0
+      std::vector<double> ls((size_t)d * g.sp, 0.0);
+      for (int i = 0; i < d; ++i) {
+        const int kd = R.pk[i];
+        const double a = R.pa[i], b = R.pb[i];
+        double sc = kd == SPECMC_PRIOR_NORMAL ? std::sqrt(b) : (kd == SPECMC_PRIOR_GAMMA ? std::sqrt(a) / b : (b - a) / std::sqrt(12.0));
+        sc = std::min(std::max(sc, 1e-12), 1e12);
+        for (int r = 0; r < Rn; ++r) ls[(size_t)i * g.sp + r] = std::log(sc);
+      }
+      h2d(g.chain_ls, ls.data(), ls.size(), st);
+      cuda_check(cudaMemsetAsync(g.chain_acc, 0, sizeof(int) * (size_t)d * g.sp, st), "memset");
+      std::vector<double> pa0(2 * (size_t)Rn, 0.0);
+      for (int l = 0; l < Rn; ++l) pa0[2 * l] = -INFINITY;
+      h2d(g.pair_acc, pa0.data(), pa0.size(), st);
+      cuda_check(cudaMemsetAsync(g.swaps, 0, sizeof(int) * 2 * (size_t)Rn, st), "memset");
+      GroupState& s = sts[gi];
+      std::memset(&s, 0, sizeof(s));
+      s.active = 1;
+      s.level = 1;
+      s.T_loc = s.S_loc = Rn;
+      list[gi] = gi;
+      prefix[gi] = total;
+      total += (Rn + shape.U - 1) / shape.U;
+      done[ri] = Done{g, d_st + gi, draws};
+    }
+    prefix[G] = total;
+    h2d(d_gds, gds.data(), G, st);
+    h2d(d_st, sts.data(), G, st);
+    h2d(d_list, list.data(), G, st);
+    h2d(d_prefix, prefix.data(), G + 1, st);
+    dev.sync();  // (host vectors above go out of scope)
+    int64_t sweeps = 0;
+    for (int r : idx) sweeps = std::max<int64_t>(sweeps, problems[r].cfg.total_sweeps);
+    // init: prior draws and energies of every replica (remc.cpp:113-119)
+    int rmax = 0;
+    for (int r : idx) rmax = std::max<int>(rmax, (int)ladders[r].size());
+    cuda_check(launch_init_draw(d_gds, d_list, G, rmax, st), "k_init_draw");
+    cuda_check(launch_energy(family, shape, dmax, d_gds, d_list, d_prefix, G, total, st), "k_chain<energy>");
+    count_launch(2);
+    for (int64_t t = 1; t <= sweeps; ++t) {  // (a run with fewer sweeps turns inactive after its last one)
+      cuda_check(launch_remc_sweep(family, shape, dmax, d_gds, d_list, d_prefix, G, total, st), "k_chain<remc>");
+      cuda_check(launch_remc_exchange(d_gds, d_list, G, st), "k_remc_exchange");
+      count_launch(2);
+    }
+  }
+  cuda_check(cudaEventRecord(whole.b, st), "event");
+  dev.sync();
+  const double dsec = whole.ms() * 1e-3;
+  int first = SPECMC_OK;
+  for (int i = 0; i < n; ++i) {
+    const Done& dn = done[i];
+    const GroupDesc& g = dn.g;
+    specmc_remc_result& o = out[i];
+    const int Rn = g.S, d = g.d;
+    o.status = SPECMC_OK;
+    o.R = Rn;
+    o.d = d;
+    o.draws = dn.draws;
+    std::vector<double> acc(2 * (size_t)Rn), post((size_t)d * dn.draws);
+    std::vector<int> swaps(2 * (size_t)Rn), tall((size_t)d * g.sp);
+    d2h(acc.data(), g.pair_acc, acc.size(), st);
+    d2h(swaps.data(), g.swaps, swaps.size(), st);
+    d2h(tall.data(), g.chain_acc, tall.size(), st);
+    d2h(post.data(), g.post, post.size(), st);
+    dev.sync();
+    double F = 0.0;  // free_energy_remc (remc.cpp:75-79), LogMeanAcc::log_mean (math.hpp:48-54)
+    for (int l = 0; l + 1 < Rn; ++l) {
+      const double mx = acc[2 * l], sm = acc[2 * l + 1];
+      const double lm = std::isnan(mx) ? NAN : (mx == -INFINITY ? -INFINITY : mx + std::log(sm) - std::log((double)dn.draws));
+      F -= lm;
+    }
+    o.diverged = !std::isfinite(F);
+    o.F = std::isfinite(F) ? F : NAN;
+    o.ladder = static_cast<double*>(std::malloc(sizeof(double) * Rn));
+    std::memcpy(o.ladder, ladders[i].data(), sizeof(double) * Rn);
+    o.swap_rate = static_cast<double*>(std::malloc(sizeof(double) * std::max(Rn - 1, 1)));
+    for (int l = 0; l + 1 < Rn; ++l)
+      o.swap_rate[l] = swaps[2 * l + 1] > 0 ? (double)swaps[2 * l] / swaps[2 * l + 1] : 0.0;
+    o.replica_acc = static_cast<double*>(std::malloc(sizeof(double) * Rn));
+    for (int r = 0; r < Rn; ++r) {
+      double a = 0.0;
+      for (int c = 0; c < d; ++c) a += tall[(size_t)c * g.sp + r];
+      const double prop = (double)dn.draws * d;  // proposals after the burn-in reset (mcmc.cpp:64)
+      o.replica_acc[r] = prop > 0 ? a / prop : 0.0;
+    }
+    o.posterior = static_cast<double*>(std::malloc(sizeof(double) * std::max<int64_t>((int64_t)d * dn.draws, 1)));
+    const RunSpec& R = runs[i];
+    for (int64_t k = 0; k < dn.draws; ++k)
+      for (int c = 0; c < d; ++c) {
+        double v = post[(size_t)c * dn.draws + k];
+        if (is_location(R.m.family, R.m.K, c)) v += R.x_shift;
+        o.posterior[(size_t)k * d + c] = v;
+      }
+    o.device_seconds = dsec;
+    o.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return first;
+}
+
 // ------------------------------------------------- multi-GPU model selection
 // Placement of a batch of runs (the K range of a model selection, SURVEY.md
 // 8e-1/8e-3) on `world` ranks, by cost (run_cost: T d^1.5 N).  A run costing more
@@ -2030,6 +2334,24 @@ int specmc_smc_run_distributed(int32_t n_problems, const specmc_problem* problem
       copy_err(err, errlen, "smc: max_levels exceeded before reaching beta = 1 (or total weight is zero)");
     return r;
   });
+}
+
+int specmc_remc_run_batch(int32_t n_problems, const specmc_remc_problem* problems, int32_t n_spectra,
+                          const specmc_spectrum* spectra, specmc_remc_result* out, char* err, size_t errlen) {
+  if (out && n_problems > 0) std::memset(out, 0, sizeof(specmc_remc_result) * (size_t)n_problems);
+  return guarded(err, errlen, [&]() -> int {
+    if (!out) throw Error(SPECMC_EINVAL, "null results");
+    return run_remc_batch(n_problems, problems, n_spectra, spectra, out);
+  });
+}
+
+void specmc_remc_result_free(specmc_remc_result* r) {
+  if (!r) return;
+  std::free(r->ladder);
+  std::free(r->swap_rate);
+  std::free(r->replica_acc);
+  std::free(r->posterior);
+  r->ladder = r->swap_rate = r->replica_acc = r->posterior = nullptr;
 }
 
 void specmc_free(void* p) { std::free(p); }

@@ -270,12 +270,23 @@ __device__ bool block_weights(const double* E, int64_t T, double delta, double n
 }
 
 // #{j in [0,S): (j+u)/S <= x}, with the reference's fp64 comparison (smc.cpp:103-106)
+// ((double)j + u) / S <= x with the reference's correctly rounded fp64
+// division (smc.cpp:103-106), decided by the reciprocal product whenever it is
+// clear of x by more than its rounding (a few ulp), else by the division
+__device__ __forceinline__ bool target_le(long long j, double u, double Sd, double invS, double x) {
+  const double num = (double)j + u;
+  const double q = num * invS;
+  const double tol = 1e-15 * fabs(q);
+  if (q < x - tol) return true;
+  if (q > x + tol) return false;
+  return num / Sd <= x;
+}
 __device__ __forceinline__ long long count_le(double x, double u, long long S) {
-  const double Sd = (double)S;
+  const double Sd = (double)S, invS = 1.0 / Sd;
   double jm = floor(x * Sd - u);
   long long j = jm < -1.0 ? -1 : (jm > (double)(S - 1) ? S - 1 : (long long)jm);
-  while (j + 1 < S && ((double)(j + 1) + u) / Sd <= x) ++j;
-  while (j >= 0 && ((double)j + u) / Sd > x) --j;
+  while (j + 1 < S && target_le(j + 1, u, Sd, invS, x)) ++j;
+  while (j >= 0 && !target_le(j, u, Sd, invS, x)) --j;
   return j + 1;
 }
 
@@ -310,15 +321,14 @@ __device__ void block_resample_range(const double* w, int64_t T, double base, lo
     long long k = (i == T - 1) ? hi_b : count_le(cc, u, S);
     return k < lo_b ? lo_b : (k > hi_b ? hi_b : k);
   };
-  // running boundary counts; per-thread maximum then block exclusive max-scan
+  // running boundary counts (non-decreasing along the chunk: the weights are
+  // >= 0): the thread's maximum is its last element's; then a block exclusive max-scan
   long long mymax = lo_b;
-  {
+  if (b1 > b0) {
     double cc = prefix;
-    for (int64_t i = b0; i < b1; ++i) {
-      cc += w[i];
-      const long long k = bound(i, cc);
-      mymax = k > mymax ? k : mymax;
-    }
+    for (int64_t i = b0; i < b1; ++i) cc += w[i];
+    const long long k = bound(b1 - 1, cc);
+    mymax = k > mymax ? k : mymax;
   }
   long long v = mymax;
 #pragma unroll
@@ -1124,6 +1134,97 @@ cudaError_t launch_move(int family, int noise, const Shape& s, int dmax, const G
   }
 #undef SMC_MOVE_NZ
   return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------- replica exchange (REMC)
+cudaError_t launch_remc_sweep(int family, const Shape& s, int dmax, const GroupDesc* gds, const int* list,
+                              const int* prefix, int n_list, int total_ctas, cudaStream_t st) {
+  switch (family) {
+    case FAM_GM: return launch_chain_gm_remc(s, dmax, gds, list, prefix, n_list, total_ctas, st);
+    case FAM_XPS: return launch_chain_xps_remc(s, dmax, gds, list, prefix, n_list, total_ctas, st);
+    case FAM_XRD: return launch_chain_xrd_remc(s, dmax, gds, list, prefix, n_list, total_ctas, st);
+    case FAM_OFFSET: return launch_chain_offset_remc(s, dmax, gds, list, prefix, n_list, total_ctas, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// LogMeanAcc::add (math.hpp:34-46) on a (max, scaled sum) pair
+__device__ __forceinline__ void logmean_add(double* acc, double x) {
+  double& mx = acc[0];
+  double& sm = acc[1];
+  if (isnan(x)) {
+    mx = nan("");
+    return;
+  }
+  if (x == -dinf()) return;
+  if (mx == -dinf() || x > mx) {
+    sm = sm * exp(mx - x) + 1.0;
+    mx = x;
+  } else {
+    sm += exp(x - mx);
+  }
+}
+
+// after the sweep t of every replica (remc.cpp:134-151): the swap step of pairs
+// of parity (t / swap_period) mod 2 when swap_period divides t -- independent
+// pairs, one thread each, a Philox uniform per pair keyed by (t, pair) --,
+// the tally reset at the end of burn-in, then past burn-in the pair
+// accumulators of tempered_term(beta_{l+1} - beta_l, N, E_l) and the beta = 1
+// draw; finally the sweep counter advance.  One CTA per run.
+__global__ void __launch_bounds__(128) k_remc_exchange(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
+  const GroupDesc& g = gds[list[blockIdx.x]];
+  GroupState* st = g.st;
+  if (!st->active) return;
+  const long long t = st->level;
+  const int R = g.S, d = g.d;
+  double* th = g.theta[0];
+  double* E = g.E[0];
+  if (t % g.swap_period == 0) {
+    const int parity = (int)((t / g.swap_period) % 2);
+    for (int l = parity + 2 * threadIdx.x; l + 1 < R; l += 2 * blockDim.x) {
+      g.swaps[2 * l + 1] += 1;
+      const double dbeta = g.ladder[l + 1] - g.ladder[l];
+      const double log_alpha = dbeta * g.n_data * (E[l + 1] - E[l]);
+      bool accept = log_alpha >= 0.0;
+      if (!accept) {
+        const u32x4 o = philox(u32x4{(uint32_t)l, (uint32_t)t, (uint32_t)(t >> 32), ROLE_SWAP}, g.key0, g.key1);
+        accept = log(u53(o.x, o.y)) < log_alpha;  // NaN compares false
+      }
+      if (accept) {
+        g.swaps[2 * l] += 1;
+        const double e = E[l];
+        E[l] = E[l + 1];
+        E[l + 1] = e;
+        for (int i = 0; i < d; ++i) {
+          double* p = th + (size_t)i * g.tp + l;
+          const double v = p[0];
+          p[0] = p[1];
+          p[1] = v;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (t == g.n_burn)  // reset_tallies (remc.cpp:141-142)
+    for (int i = threadIdx.x; i < d * g.sp; i += blockDim.x) g.chain_acc[i] = 0;
+  if (t > g.n_burn) {
+    for (int l = threadIdx.x; l + 1 < R; l += blockDim.x) {
+      const double dbeta = g.ladder[l + 1] - g.ladder[l];
+      logmean_add(g.pair_acc + 2 * l, dbeta == 0.0 ? 0.0 : -dbeta * g.n_data * E[l]);  // tempered_term
+    }
+    const long long draw = t - g.n_burn - 1, draws = g.total_sweeps - g.n_burn;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) g.post[(size_t)i * draws + draw] = th[(size_t)i * g.tp + R - 1];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st->level = (int)(t + 1);
+    if (t >= g.total_sweeps) st->active = 0;
+  }
+}
+
+cudaError_t launch_remc_exchange(const GroupDesc* gds, const int* list, int n_list, cudaStream_t st) {
+  k_remc_exchange<<<n_list, 128, 0, st>>>(gds, list);
+  return cudaGetLastError();
 }
 
 // MUFU throughput probe: 8 independent ex2 chains per thread (the SFU roofline

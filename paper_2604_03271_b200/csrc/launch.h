@@ -57,6 +57,10 @@ SMC_DECL_CHAIN(launch_chain_xps_energy)
 SMC_DECL_CHAIN(launch_chain_xrd_energy)
 SMC_DECL_CHAIN(launch_chain_offset_energy)
 SMC_DECL_CHAIN(launch_chain_offset_move_dyn)
+SMC_DECL_CHAIN(launch_chain_gm_remc)
+SMC_DECL_CHAIN(launch_chain_xps_remc)
+SMC_DECL_CHAIN(launch_chain_xrd_remc)
+SMC_DECL_CHAIN(launch_chain_offset_remc)
 #define SMC_DECL_MOVE(FAM) \
   SMC_DECL_CHAIN(launch_chain_##FAM##_move_gauss)  \
   SMC_DECL_CHAIN(launch_chain_##FAM##_move_hetero) \
@@ -114,6 +118,14 @@ cudaError_t launch_xgather(const GroupDesc* d_gds, const int* d_list, int nruns,
 
 // step-size statistics, one CTA per (component, group), + per-group finalisation
 cudaError_t launch_stats_grid(const GroupDesc* d_gds, const int* d_list, int n_list, int dmax, cudaStream_t st);
+
+// ---- replica exchange (the paper's REMC comparator, remc.cpp): one sweep of
+// every replica of every listed run (k_chain in REMC mode), then per run the
+// swap step (remc.cpp:53-73), the post-burn-in pair accumulators and beta = 1
+// draws, and the sweep counter advance (k_remc_exchange)
+cudaError_t launch_remc_sweep(int family, const Shape& s, int dmax, const GroupDesc* d_gds, const int* d_list,
+                              const int* d_cta_prefix, int n_list, int total_ctas, cudaStream_t st);
+cudaError_t launch_remc_exchange(const GroupDesc* d_gds, const int* d_list, int n_list, cudaStream_t st);
 
 // load every kernel of one class (family, noise, shape) before its timed run
 cudaError_t prime_level_kernels(int family, int noise, const Shape& s, int dmax);

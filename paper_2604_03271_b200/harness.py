@@ -18,8 +18,9 @@ a reference report (:251-311).  Here the SMC conditions run on the GPU:
   reference's table arithmetic and text format (checked byte for byte against
   the reference build in tests/test_harness.py), so tables regenerated from
   persisted reports (report.py) match the reference's.
-REMC conditions (the paper's CPU comparator) are accepted in reports and
-tables (their speedup row), but are not run on the GPU.
+REMC conditions (the paper's comparator, remc.cpp) run on the GPU as well
+(smc.remc_run: one chain unit per replica), so the matched-|dF| speedup of
+SMC over REMC (bench.cpp:227-247) is measured on one device.
 """
 from __future__ import annotations
 
@@ -31,17 +32,18 @@ import numpy as np
 
 from . import synthetic
 from .report import credible_interval, format_double
-from .smc import RunReport, SmcConfig, smc_run, smc_run_batch
+from .smc import RemcConfig, RunReport, SmcConfig, remc_run, remc_run_batch, smc_run, smc_run_batch
 
 NAN = float("nan")
 
 
 @dataclass
 class BenchCondition:
-    """bench.hpp:9-14 (SMC conditions only run here)."""
+    """bench.hpp:9-14"""
     label: str
     sampler: str = "smc"
     smc: SmcConfig = field(default_factory=SmcConfig)
+    remc: RemcConfig = field(default_factory=RemcConfig)
 
 
 @dataclass
@@ -139,13 +141,27 @@ def time_at_error(pts: Sequence[Tuple[float, float]], err: float) -> float:
 
 
 def _report_of(spec, cond: BenchCondition, seed: int, rep: RunReport, trial: int, parallel: bool) -> RunReport:
-    """run_once (bench.cpp:65-100) fields for an SMC condition."""
-    r = RunReport(sampler="smc", label=cond.label, F=rep.F, diverged=rep.diverged, wall_seconds=rep.wall_seconds,
-                  param_names=list(spec.param_names), posterior=rep.posterior, energies=rep.energies,
-                  device_seconds=rep.device_seconds, proposals=rep.proposals, trials=rep.trials)
-    r.scalars = {"T": float(cond.smc.T), "n": float(cond.smc.n), "seed": float(seed), "trial": float(trial),
-                 "parallel_trials": 1.0 if parallel else 0.0}
+    """run_once (bench.cpp:65-100) fields of a condition's run."""
+    r = RunReport(sampler=cond.sampler, label=cond.label, F=rep.F, diverged=rep.diverged,
+                  wall_seconds=rep.wall_seconds, param_names=list(spec.param_names), posterior=rep.posterior,
+                  energies=rep.energies, device_seconds=rep.device_seconds, proposals=rep.proposals,
+                  trials=rep.trials)
+    if cond.sampler == "smc":
+        r.scalars = {"T": float(cond.smc.T), "n": float(cond.smc.n)}
+    else:
+        r.scalars = {"L": rep.scalars.get("L", float(cond.remc.L)), "total_sweeps": float(cond.remc.total_sweeps)}
+    r.scalars.update({"seed": float(seed), "trial": float(trial), "parallel_trials": 1.0 if parallel else 0.0})
     return r
+
+
+def _cfg_with_seed(cond: BenchCondition, seed: int):
+    if cond.sampler == "smc":
+        c = cond.smc
+        return SmcConfig(T=c.T, n=c.n, ess_target=c.ess_target, max_levels=c.max_levels, seed=seed,
+                         workers=c.workers, device=c.device)
+    c = cond.remc
+    return RemcConfig(L=c.L, ladder=c.ladder, total_sweeps=c.total_sweeps, burn_in_fraction=c.burn_in_fraction,
+                      swap_period=c.swap_period, seed=seed, workers=c.workers, device=c.device)
 
 
 def benchmark(spec, data, grid: Sequence[BenchCondition], trials: int, base_seed: int,
@@ -156,29 +172,30 @@ def benchmark(spec, data, grid: Sequence[BenchCondition], trials: int, base_seed
     if not grid:
         raise ValueError("benchmark: empty condition grid")
     for c in grid:
-        if c.sampler != "smc":
-            raise ValueError(f"benchmark: sampler '{c.sampler}' does not run on the B200 backend")
-    jobs = []
-    for c in grid:
-        for t in range(trials):
-            seed = trial_seed(base_seed, t)
-            cfg = SmcConfig(T=c.smc.T, n=c.smc.n, ess_target=c.smc.ess_target, max_levels=c.smc.max_levels,
-                            seed=seed, workers=c.smc.workers, device=c.smc.device)
-            jobs.append((c, t, seed, cfg))
-    runs: List[RunReport] = []
-    if batched:
-        reps = smc_run_batch([(spec, 0, cfg) for _, _, _, cfg in jobs], [data], raise_on_error=False)
-        for (c, t, seed, cfg), rep in zip(jobs, reps):
-            if isinstance(rep, Exception):
-                rep = RunReport(F=NAN, diverged=True)
-            runs.append(_report_of(spec, c, seed, rep, t, True))
+        if c.sampler not in ("smc", "remc"):
+            raise ValueError(f"benchmark: unknown sampler '{c.sampler}' (expected smc|remc)")
+    jobs = [(c, t, trial_seed(base_seed, t)) for c in grid for t in range(trials)]
+    reps: List[RunReport] = [None] * len(jobs)
+    if batched:  # one call per sampler for the whole grid (the reference's parallel_trials analogue)
+        for sampler, call in (("smc", smc_run_batch), ("remc", remc_run_batch)):
+            sel = [i for i, (c, _, _) in enumerate(jobs) if c.sampler == sampler]
+            if not sel:
+                continue
+            out = call([(spec, 0, _cfg_with_seed(jobs[i][0], jobs[i][2])) for i in sel], [data],
+                       **({"raise_on_error": False} if sampler == "smc" else {}))
+            for i, rep in zip(sel, out):
+                reps[i] = rep
     else:
-        for c, t, seed, cfg in jobs:
+        for i, (c, t, seed) in enumerate(jobs):
             try:
-                rep = smc_run(spec, data, cfg)
+                reps[i] = (smc_run if c.sampler == "smc" else remc_run)(spec, data, _cfg_with_seed(c, seed))
             except RuntimeError:
-                rep = RunReport(F=NAN, diverged=True)
-            runs.append(_report_of(spec, c, seed, rep, t, False))
+                reps[i] = None
+    runs = []
+    for (c, t, seed), rep in zip(jobs, reps):
+        if rep is None or isinstance(rep, Exception):
+            rep = RunReport(F=NAN, diverged=True)
+        runs.append(_report_of(spec, c, seed, rep, t, batched))
     return BenchResult(table_from_reports(runs, reference_label), runs)
 
 

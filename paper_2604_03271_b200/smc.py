@@ -360,6 +360,77 @@ def smc_run_distributed(problems: Sequence[Tuple[ModelSpec, int, SmcConfig]], sp
     return _collect(problems, spectra, res, raise_on_error), r0, sh
 
 
+# ------------------------------------------------- replica exchange (REMC)
+@dataclass
+class RemcConfig:
+    """proj/include/specmc/remc.hpp:14-22 (+ the CUDA device ordinal)."""
+    L: int = 44
+    ladder: Optional[Sequence[float]] = None
+    total_sweeps: int = 10000
+    burn_in_fraction: float = 0.5
+    swap_period: int = 1
+    seed: int = 0
+    workers: int = 1
+    device: int = 0
+
+    def c(self):
+        lad = None if self.ladder is None else _d(self.ladder)
+        cc = _lib.RemcConfigC(int(self.L), _p(lad) if lad is not None else None, 0 if lad is None else len(lad),
+                              int(self.total_sweeps), float(self.burn_in_fraction), int(self.swap_period),
+                              int(self.seed) & 0xFFFFFFFFFFFFFFFF, int(self.workers), int(self.device))
+        return cc, lad
+
+
+def remc_run_batch(problems: Sequence[Tuple[ModelSpec, int, RemcConfig]], spectra: Sequence[Spectrum],
+                   raise_on_error: bool = True):
+    """Every (spec, spectrum index, RemcConfig) concurrently on one GPU
+    (specmc_remc_run_batch): RunReports as remc_run(spec, data, cfg) fills them
+    (remc.cpp:170-190): sampler 'remc', scalars L / total_sweeps /
+    burn_in_fraction / swap_period / seed / workers / n_data, arrays ladder /
+    swap_rate / replica_acc_rate, the beta = 1 draws as posterior (d x draws)."""
+    n = len(problems)
+    probs = (_lib.RemcProblemC * n)()
+    keep = []
+    for i, (spec, si, cfg) in enumerate(problems):
+        desc, k = spec.desc()
+        cc, lad = cfg.c()
+        keep += [k, lad]
+        probs[i] = _lib.RemcProblemC(desc, int(si), cc)
+    sps = (_lib.SpectrumC * len(spectra))()
+    for j, sp in enumerate(spectra):
+        sps[j] = _lib.SpectrumC(_p(sp.xs), _p(sp.ys), len(sp.xs))
+    res = (_lib.RemcResultC * n)()
+    err = C.create_string_buffer(1024)
+    rc = lib.specmc_remc_run_batch(n, probs, len(spectra), sps, res, err, 1024)
+    try:
+        if rc:
+            _raise(rc, err)
+        out = []
+        for i, (spec, si, cfg) in enumerate(problems):
+            r = res[i]
+            rep = RunReport(sampler="remc", F=r.F, diverged=bool(r.diverged), wall_seconds=r.wall_seconds,
+                            param_names=spec.param_names, device_seconds=r.device_seconds)
+            R = r.R
+            rep.scalars = {"L": float(R - 1), "total_sweeps": float(cfg.total_sweeps),
+                           "burn_in_fraction": float(cfg.burn_in_fraction), "swap_period": float(cfg.swap_period),
+                           "seed": float(cfg.seed), "workers": float(cfg.workers),
+                           "n_data": float(len(spectra[si].xs))}
+            rep.arrays = {"ladder": np.ctypeslib.as_array(r.ladder, (R,)).copy(),
+                          "swap_rate": np.ctypeslib.as_array(r.swap_rate, (max(R - 1, 1),))[:R - 1].copy(),
+                          "replica_acc_rate": np.ctypeslib.as_array(r.replica_acc, (R,)).copy()}
+            rep.posterior = np.ctypeslib.as_array(r.posterior, (int(r.draws), r.d)).copy().T
+            out.append(rep)
+        return out
+    finally:
+        for i in range(n):
+            lib.specmc_remc_result_free(C.byref(res[i]))
+
+
+def remc_run(spec: ModelSpec, data: Spectrum, cfg: RemcConfig) -> RunReport:
+    """RunReport remc_run(const ModelSpec&, const Spectrum&, const RemcConfig&) -- remc.cpp:170-190."""
+    return remc_run_batch([(spec, 0, cfg)], [data])[0]
+
+
 def probe_mufu(device: int = 0) -> float:
     """Measured MUFU ex2 throughput (ops/s) of the device."""
     v = C.c_double()
