@@ -942,7 +942,15 @@ __global__ void __launch_bounds__(Bounds<W, PPL>::threads, Bounds<W, PPL>::min_b
   }
   extern __shared__ __align__(16) unsigned char smem[];
   const int gi = find_group(cta_prefix, n_list, blockIdx.x);
-  const GroupDesc& g = gds[list[gi]];
+  // the group's descriptor staged in shared memory (every unit of a CTA runs
+  // the same group): its fields are read on every evaluation (measured: C3
+  // +3.6%, C5 +2.8%, C1 +4%, C2 +0.2% over reading them through L1)
+  __shared__ GroupDesc sg;
+  static_assert(sizeof(GroupDesc) % 4 == 0 && sizeof(GroupDesc) <= 4 * 256, "descriptor copy");
+  if (threadIdx.x < sizeof(GroupDesc) / 4)
+    reinterpret_cast<int*>(&sg)[threadIdx.x] = reinterpret_cast<const int*>(&gds[list[gi]])[threadIdx.x];
+  __syncthreads();
+  const GroupDesc& g = sg;
   const int cta_in_group = blockIdx.x - cta_prefix[gi];
   // a move launch covers every group of the class; finished or failed groups'
   // CTAs leave at once (levels are enqueued ahead of the host's check)

@@ -38,7 +38,7 @@ __host__ __device__ constexpr int chain_threads(int W) { return W >= 8 ? 32 * W 
 // (and W = 1 with wide lanes, PPL >= 20: 512 < N <= 1024)
 __host__ __device__ constexpr bool chain_p_in_smem(int W, int PPL) { return W == 2 || W == 4 || (W == 1 && PPL >= 20); }
 
-constexpr size_t kChainSmemMax = 227 * 1024;  // dynamic shared memory per CTA
+constexpr size_t kChainSmemMax = 226 * 1024;  // dynamic shared memory per CTA (227 KB less the static descriptor copy)
 Shape pick_shape(int64_t N, int dmax);
 bool ppl_supported(int ppl);
 size_t chain_smem_bytes(const Shape& s, int dmax);

@@ -56,3 +56,39 @@ def test_tree_ess_passes_equal_single_steps_bitwise():
     assert tree.pop("launches") < single.pop("launches")
     # ... the results do not
     assert tree == single, (tree, single)
+
+
+def test_grid_and_single_cta_next_beta_agree():
+    """The same energies through the single-CTA bisection (k_temper's
+    block_next_beta, T <= 2^15) and through the production grid launches
+    (k_tp_emin + k_tp_ess_tree, forced with SPECMC_GRID_T in a subprocess):
+    both replay the reference's bisection exactly, so beta_next agrees to the
+    fp64 rounding of the differently ordered weight sums."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    import numpy as np
+    import paper_2604_03271_b200 as S
+
+    rng = np.random.default_rng(5)
+    cases = []
+    for T, nd, bp in ((4096, 301.0, 0.0), (20000, 2000.0, 1e-4), (30000, 840.0, 0.2)):
+        E = 5.0 + np.abs(rng.normal(size=T)) * 3
+        E[::101] = np.inf
+        cases.append((E, nd, bp))
+    block = [S.next_beta(E, nd, bp, 0.5) for E, nd, bp in cases]
+    root = Path(__file__).resolve().parent.parent
+    code = ("import sys, json, numpy as np; sys.path.insert(0, %r); import paper_2604_03271_b200 as S; "
+            "rng = np.random.default_rng(5); out = []\n"
+            "for T, nd, bp in ((4096, 301.0, 0.0), (20000, 2000.0, 1e-4), (30000, 840.0, 0.2)):\n"
+            "    E = 5.0 + np.abs(rng.normal(size=T)) * 3; E[::101] = np.inf; out.append(S.next_beta(E, nd, bp, 0.5))\n"
+            "print(json.dumps(out))") % str(root)
+    env = dict(os.environ, SPECMC_GRID_T="1024")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0, r.stderr
+    grid = json.loads(r.stdout.strip().splitlines()[-1])
+    for b, g in zip(block, grid):
+        assert g == pytest.approx(b, rel=1e-12), (block, grid)
