@@ -974,14 +974,17 @@ struct ClassRun {
     dev.sync();
   }
 
-  int build_list(const std::vector<int>& groups, bool energy, std::vector<int>& list, std::vector<int>& prefix) {
+  // all_chains: size for every chain of the run (a shard may resolve up to S
+  // of them; the kernels stop at the shard's own count)
+  int build_list(const std::vector<int>& groups, bool energy, std::vector<int>& list, std::vector<int>& prefix,
+                 bool all_chains = false) {
     list.clear();
     prefix.clear();
     int total = 0;
     for (int gi : groups) {
       list.push_back(gi);
       prefix.push_back(total);
-      const int units = energy ? (int)runs_T0[gi] : h_st[gi].S_loc;
+      const int units = energy ? (int)runs_T0[gi] : (all_chains ? gds[gi].S : h_st[gi].S_loc);
       total += (units + shape.U - 1) / shape.U;
     }
     prefix.push_back(total);
@@ -1018,57 +1021,25 @@ struct ClassRun {
     if (init_only) d2h(h_st, d_st, G, st);
     double move_ms = 0.0;
     int64_t move_launches = 0;
-    while (!active.empty() && xch) {
-      // particle-sharded level: every shard of the run takes part in every exchange.
-      // The chains a shard resolves are known only after its tempering, so the
-      // move grid is sized from a read-back of the shard states.
-      dev.sync();
-      std::copy(active.begin(), active.end(), h_list + 3 * (G + 1));
-      h2d(d_list_big, h_list + 3 * (G + 1), active.size(), st);
-      cuda_check(launch_temper_sharded(d_gds, d_list_big, (int)active.size(), max_slices, *xch, st),
-                 "k_tp_* (sharded)");
-      count_launch(temper_sharded_launches());
-      d2h(h_st, d_st, G, st);
-      dev.sync();
-      bool alive = true;
-      for (int gi : active) alive = alive && h_st[gi].active;
-      if (!alive) break;  // an error ends the run on every shard (identical global state)
-      total = build_list(active, false, list, prefix);
-      const int na = (int)list.size();
-      std::memcpy(h_list, list.data(), sizeof(int) * na);
-      std::memcpy(h_list + (G + 1), prefix.data(), sizeof(int) * (na + 1));
-      h2d(d_list, h_list, na, st);
-      h2d(d_prefix, h_list + (G + 1), na + 1, st);
-      cuda_check(cudaEventRecord(mv.a, st), "event");
-      if (total > 0)
-        cuda_check(launch_move(kfam, noise, shape, dmax, d_gds, d_list, d_prefix, na, total, st), "k_chain<move>");
-      cuda_check(cudaEventRecord(mv.b, st), "event");
-      cuda_check(launch_stats_sharded(d_gds, d_list, na, dmax, *xch, st), "k_stats (sharded)");
-      count_launch(4);
-      d2h(h_st, d_st, G, st);
-      dev.sync();
-      move_ms += mv.ms();
-      ++move_launches;
-      std::vector<int> next;
-      for (int gi : active)
-        if (h_st[gi].active) next.push_back(gi);
-      active.swap(next);
-    }
-    if (!active.empty() && !xch) {
-      // Unsharded class: every level is the same launch sequence over every
-      // group of the class (the kernels skip finished or failed groups), so
-      // the host enqueues levels ahead without waiting for them: after each
-      // level the small GroupState array is copied into a pinned ring slot and
-      // an event recorded; the host keeps up to kAhead levels in flight and
-      // retires / stages runs as their levels' copies land.  Once every run is
-      // seen inactive no further level is enqueued (at most kAhead levels of
-      // empty launches run past the end).
+    if (!active.empty()) {
+      // Every level is the same launch sequence over every group of the class
+      // (the kernels skip finished or failed groups), so the host enqueues
+      // levels ahead without waiting for them: after each level the small
+      // GroupState array is copied into a pinned ring slot and an event
+      // recorded; the host keeps up to kAhead levels in flight and retires /
+      // stages runs as their levels' copies land.  Once every run is seen
+      // inactive no further level is enqueued (at most kAhead levels of empty
+      // launches run past the end).  Particle-sharded classes (xch) run the
+      // sharded tempering and statistics with their exchanges (stream-ordered
+      // NCCL collectives or device kernels) and size the move grid for all S
+      // chains of each run (a shard resolves its own share after the
+      // tempering; the other CTAs leave at once): no host round trip per level.
       constexpr int kAhead = 3, kRing = kAhead + 1;
-      total = build_list(order, false, list, prefix);  // every group, its S chains (static)
+      total = build_list(order, false, list, prefix, /*all_chains=*/xch != nullptr);  // static
       const int na = (int)list.size();
       dev.sync();  // h_list's pinned bytes of the init launches may still be in flight
       std::vector<int> small, big;
-      for (int gi : order) (gds[gi].nslices > 0 ? big : small).push_back(gi);
+      for (int gi : order) (gds[gi].nslices > 0 || xch ? big : small).push_back(gi);
       std::memcpy(h_list, list.data(), sizeof(int) * na);
       std::memcpy(h_list + (G + 1), prefix.data(), sizeof(int) * (na + 1));
       std::copy(small.begin(), small.end(), h_list + 2 * (G + 1));
@@ -1096,14 +1067,21 @@ struct ClassRun {
             cuda_check(launch_temper(d_gds, d_list_small, (int)small.size(), st), "k_temper");
             count_launch(1);
           }
-          if (!big.empty()) {
+          if (!big.empty() && xch) {
+            cuda_check(launch_temper_sharded(d_gds, d_list_big, (int)big.size(), max_slices, *xch, st),
+                       "k_tp_* (sharded)");
+            count_launch(temper_sharded_launches());
+          } else if (!big.empty()) {
             cuda_check(launch_temper_grid(d_gds, d_list_big, (int)big.size(), max_slices, st), "k_tp_*");
             count_launch(temper_grid_launches());
           }
           cuda_check(cudaEventRecord(ma[k], st), "event");
           cuda_check(launch_move(kfam, noise, shape, dmax, d_gds, d_list, d_prefix, na, total, st), "k_chain<move>");
           cuda_check(cudaEventRecord(mb[k], st), "event");
-          cuda_check(launch_stats_grid(d_gds, d_list, na, dmax, st), "k_stats_grid");
+          if (xch)
+            cuda_check(launch_stats_sharded(d_gds, d_list, na, dmax, *xch, st), "k_stats (sharded)");
+          else
+            cuda_check(launch_stats_grid(d_gds, d_list, na, dmax, st), "k_stats_grid");
           count_launch(3);
           d2h(ring + (size_t)k * G, d_st, G, st);
           cuda_check(cudaEventRecord(lev[k], st), "event");

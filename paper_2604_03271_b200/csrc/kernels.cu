@@ -876,26 +876,28 @@ __global__ void __launch_bounds__(kGridThreads) k_tp_resample(const GroupDesc* _
 }
 
 // cross-shard finalisers (one thread per listed group), after the exchange
+// (a finished or failed run's shards skip every finaliser: levels are enqueued
+// ahead of the host's check and the exchanges still cover them)
 __global__ void k_tpf_emin(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
   const GroupDesc& g = gds[list[blockIdx.x]];
-  if (threadIdx.x == 0 && !g.ts->err) fin_emin(g, g.ts, g.xbuf[0]);
+  if (threadIdx.x == 0 && g.st->active && !g.ts->err) fin_emin(g, g.ts, g.xbuf[0]);
 }
 template <int D>
 __global__ void k_tpf_ess_tree(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
   const GroupDesc& g = gds[list[blockIdx.x]];
-  if (threadIdx.x == 0 && !g.ts->done && !g.ts->err) ess_replay<D>(g, g.ts, g.xbuf);
+  if (threadIdx.x == 0 && g.st->active && !g.ts->done && !g.ts->err) ess_replay<D>(g, g.ts, g.xbuf);
 }
 __global__ void k_tpf_wmax(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
   const GroupDesc& g = gds[list[blockIdx.x]];
-  if (threadIdx.x == 0 && !g.ts->err) fin_wmax(g, g.ts, g.xbuf[0]);
+  if (threadIdx.x == 0 && g.st->active && !g.ts->err) fin_wmax(g, g.ts, g.xbuf[0]);
 }
 __global__ void k_tpf_wsum(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
   const GroupDesc& g = gds[list[blockIdx.x]];
-  if (threadIdx.x == 0 && !g.ts->err) fin_wsum(g, g.ts, g.xbuf[0], g.xbuf[1]);
+  if (threadIdx.x == 0 && g.st->active && !g.ts->err) fin_wsum(g, g.ts, g.xbuf[0], g.xbuf[1]);
 }
 __global__ void k_tpf_offsets(const GroupDesc* __restrict__ gds, const int* __restrict__ list) {
   const GroupDesc& g = gds[list[blockIdx.x]];
-  if (threadIdx.x == 0 && !g.ts->err) fin_offsets(g, g.ts, g.xgat, g.nshards, g.shard);
+  if (threadIdx.x == 0 && g.st->active && !g.ts->err) fin_offsets(g, g.ts, g.xgat, g.nshards, g.shard);
 }
 
 // step-size statistics, one CTA per (component, group) (smc.cpp:162-179): sums
