@@ -800,10 +800,6 @@ struct ClassRun {
     shape = pick_shape(Nmax, dmax);
     if ((int64_t)32 * shape.W * shape.PPL < Nmax)
       throw Error(SPECMC_EINVAL, "spectrum has more points than the device path supports (8192)");
-    if (chain_smem_bytes(shape, dmax) > kChainSmemMax)
-      throw Error(SPECMC_EINVAL, "model too large for the device path (shared memory)");
-    // module load of this class's kernels happens here, outside the timed level loop
-    cuda_check(prime_level_kernels(kfam, noise, shape, dmax), "loading the level kernels");
 
     // one prepared copy per (spectrum, shift, noise parameters): the inverse
     // noise scales and the centring constants depend on the noise model
@@ -816,6 +812,10 @@ struct ClassRun {
       }
     }
     shape.lay = spectrum_layout(family, noise, prep);
+    if (chain_smem_bytes(shape, dmax) > kChainSmemMax)  // (with the launch's spectrum layout)
+      throw Error(SPECMC_EINVAL, "model too large for the device path (shared memory)");
+    // module load of this class's kernels happens here, outside the timed level loop
+    cuda_check(prime_level_kernels(kfam, noise, shape, dmax), "loading the level kernels");
     const size_t npt = (size_t)shape.PPL * 32 * shape.W;
     size_t bytes = Arena::al(sizeof(GroupDesc) * G) + Arena::al(sizeof(GroupState) * G) + 7 * Arena::al(4 * (G + 1));
     bytes += prep.size() * (Arena::al(npt * 4) + 2 * Arena::al(npt * 8));
