@@ -1047,7 +1047,7 @@ cudaError_t launch_chain_t(int U, int lay, int dmax, const GroupDesc* gds, const
   if (e != cudaSuccess) return e;
   if (total_ctas <= 0) return cudaSuccess;  // prime only (module load + attributes, see prime_level_kernels)
   const int dpad_lay = chain_dyn_layout(W) ? (dpad | (lay << 16)) : dpad;
-  kern<<<total_ctas, Bounds<W, PPL>::threads, smem, st>>>(gds, list, prefix, n_list, U, dpad_lay);
+  kern<<<total_ctas, 32 * W * U, smem, st>>>(gds, list, prefix, n_list, U, dpad_lay);  // U <= threads / 32 W
   return cudaGetLastError();
 }
 

@@ -552,6 +552,12 @@ double pick_shift(const specmc_model_desc& m, const double* xs, int64_t N) {
   return 0.5 * (xs[0] + xs[N - 1]);
 }
 
+// fewer chains per CTA when the launch's spectrum layout leaves no room for
+// the default count's caches (W = 8 on a non-uniform grid: launch.h)
+void fit_units(Shape& s, int dmax) {
+  while (s.U > 1 && chain_smem_bytes(s, dmax) > kChainSmemMax) --s.U;
+}
+
 // ------------------------------------------------------------------ batch
 struct RunSpec {
   specmc_model_desc m;
@@ -812,6 +818,7 @@ struct ClassRun {
       }
     }
     shape.lay = spectrum_layout(family, noise, prep);
+    fit_units(shape, dmax);
     if (chain_smem_bytes(shape, dmax) > kChainSmemMax)  // (with the launch's spectrum layout)
       throw Error(SPECMC_EINVAL, "model too large for the device path (shared memory)");
     // module load of this class's kernels happens here, outside the timed level loop
@@ -1611,6 +1618,7 @@ int run_remc_batch(int n, const specmc_remc_problem* problems, int n_spectra, co
       }
     }
     shape.lay = spectrum_layout(family, noise, prep);
+    fit_units(shape, dmax);
     if (chain_smem_bytes(shape, dmax) > kChainSmemMax)
       throw Error(SPECMC_EINVAL, "model too large for the device path (shared memory)");
     const size_t npt = (size_t)shape.PPL * 32 * shape.W;
@@ -2378,6 +2386,7 @@ int specmc_energy_batch(const specmc_model_desc* model, const double* xs, const 
       throw Error(SPECMC_EINVAL, "spectrum has more points than the device path supports (8192)");
     const PreparedSpectrum ps = prepare_spectrum(*model, xs, ys, n_points, shape, R.x_shift);
     shape.lay = spectrum_layout(model->family, ps.nz, std::map<int, PreparedSpectrum>{{0, ps}});
+    fit_units(shape, model->d);
     const int d = model->d;
     const int64_t T = n_thetas;
     Scratch sc;

@@ -34,15 +34,16 @@ struct Shape {
 // chain-kernel CTA size per unit width W (units per CTA = threads / 32 W):
 // W = 2 runs 8 units per 512-thread CTA, one CTA per SM, so the spectrum is
 // staged once per SM and the 8 units' P and Q caches fit in shared memory
-#ifndef SPECMC_W8_UNITS
-#define SPECMC_W8_UNITS 1
-#endif
+// W = 8 (N <= 8192): two chains per 512-thread CTA with P in shared memory
+// (one spectrum copy per SM); a launch whose spectrum layout leaves no room
+// for two chains' P and Q caches (a non-uniform grid's trapezoid weights)
+// runs one chain per 256-thread CTA instead (fit_units, host.cu)
 __host__ __device__ constexpr int chain_threads(int W) {
-  return W >= 8 ? 32 * W * SPECMC_W8_UNITS : (W == 2 ? 64 * SPECMC_W2_UNITS : 256);
+  return W >= 8 ? 64 * W : (W == 2 ? 64 * SPECMC_W2_UNITS : 256);
 }
 // (and W = 1 with wide lanes, PPL >= 20: 512 < N <= 1024)
 __host__ __device__ constexpr bool chain_p_in_smem(int W, int PPL) {
-  return W == 2 || W == 4 || (W == 1 && PPL >= 20) || (W == 8 && SPECMC_W8_UNITS > 1);
+  return W == 2 || W == 4 || W == 8 || (W == 1 && PPL >= 20);
 }
 
 constexpr size_t kChainSmemMax = 226 * 1024;  // dynamic shared memory per CTA (227 KB less the static descriptor copy)
