@@ -86,6 +86,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--shard", default="model", choices=["model", "trials", "particles"])
+    ap.add_argument("--dist-always", action="store_true",
+                    help="(check) take the multi-GPU path even on one rank: NCCL process group + communicator")
     return ap.parse_args()
 
 
@@ -328,8 +330,12 @@ def run_ours(args, ws, rank, local):
 
     torch.cuda.set_device(local)
     dist = comm = None
-    if ws > 1:
+    multi = ws > 1 or args.dist_always
+    if multi:
         import torch.distributed as dist
+        if args.dist_always and "MASTER_ADDR" not in os.environ:
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=os.environ.get("MASTER_PORT", "29571"),
+                              RANK=str(rank), WORLD_SIZE=str(ws))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         if args.shard != "trials":
             comm = S.Comm.from_torch(local)
@@ -338,7 +344,7 @@ def run_ours(args, ws, rank, local):
     problems = problems_for(S, b, seed, local)
     peak_mufu = S.probe_mufu(local)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    mode = args.shard if ws > 1 else "local"
+    mode = args.shard if multi else "local"
 
     def step_device():
         """one model selection; returns (device seconds, reports)"""
