@@ -30,6 +30,7 @@
 #include <vector>
 
 #include <dlfcn.h>
+#include <unistd.h>
 #include <nccl.h>  // types only: the library is resolved at run time (dlopen), see NcclApi
 
 #include "../../include/specmc_b200.h"
@@ -275,7 +276,14 @@ ArenaCache& arena_cache() {
 // copied D2H into pinned memory while the remaining runs still step; pinning
 // 100+ MB costs tens of ms, so buffers are kept for later calls).
 struct PinnedCache {
-  static constexpr size_t kMaxCached = size_t(4) << 30;
+  // keep up to a quarter of the host's memory pinned between calls (at most
+  // 32 GB): re-pinning a large result staging buffer per call costs seconds
+  // (C4: 12.9 GB, cudaHostAlloc + cudaFreeHost ~3-4 s per call)
+  const size_t kMaxCached = [] {
+    const long pages = sysconf(_SC_PHYS_PAGES), psz = sysconf(_SC_PAGE_SIZE);
+    const size_t quarter = pages > 0 && psz > 0 ? (size_t)pages * (size_t)psz / 4 : (size_t(4) << 30);
+    return std::min(quarter, size_t(32) << 30);
+  }();
   std::mutex mu;
   std::multimap<size_t, void*> free_;
   size_t cached = 0;
