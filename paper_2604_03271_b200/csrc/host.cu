@@ -827,6 +827,15 @@ struct ClassRun {
     }
     shape.lay = spectrum_layout(family, noise, prep);
     fit_units(shape, dmax);
+    {  // few chains per level (a shard of a particle-sharded run, small populations):
+       // fewer chains per CTA, so that the chains spread over every SM
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev.ordinal);
+      double chains = 0.0;
+      for (int r : idx) chains += (double)(runs[r].cfg.T / runs[r].cfg.n) / (double)runs[r].nshards;
+      while (shape.U > 1 && shape.U % 2 == 0 && chains / (shape.U / 2) <= 2.0 * sms && chains / shape.U < sms)
+        shape.U /= 2;
+    }
     if (chain_smem_bytes(shape, dmax) > kChainSmemMax)  // (with the launch's spectrum layout)
       throw Error(SPECMC_EINVAL, "model too large for the device path (shared memory)");
     // module load of this class's kernels happens here, outside the timed level loop
