@@ -12,11 +12,8 @@
 // failures throw std::runtime_error.  Link with paper_2604_03271_b200/libspecmc_b200.so.
 #pragma once
 
-#include <charconv>
 #include <cmath>
 #include <cstdint>
-#include <fstream>
-#include <sstream>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -359,118 +356,8 @@ inline int model_select(const std::vector<std::pair<int, RunReport>>& reports) {
   return best;
 }
 
-// ---- report file format (report.cpp:10-136): shortest round-trip numbers
-inline std::string format_double(double v) {
-  char buf[64];
-  auto r = std::to_chars(buf, buf + sizeof buf, v);
-  return std::string(buf, r.ptr);
-}
-inline double parse_double(const std::string& s) {
-  double v;
-  auto r = std::from_chars(s.data(), s.data() + s.size(), v);
-  if (r.ec != std::errc()) throw std::runtime_error("bad number in report: " + s);
-  return v;
-}
-
-// max_draws < T downsamples the posterior block by a deterministic stride
-inline void write_report(const RunReport& r, const std::string& path, std::int64_t max_draws = 20000) {
-  std::ofstream out(path);
-  if (!out) throw std::runtime_error("cannot write report: " + path);
-  out << "specmc-report 1\n" << "sampler " << r.sampler << "\n";
-  if (!r.label.empty()) out << "label " << r.label << "\n";
-  out << "diverged " << (r.diverged ? 1 : 0) << "\n";
-  out << "scalar F " << format_double(r.F) << "\n";
-  out << "scalar wall_seconds " << format_double(r.wall_seconds) << "\n";
-  for (auto& [k, v] : r.scalars) out << "scalar " << k << " " << format_double(v) << "\n";
-  if (!r.param_names.empty()) {
-    out << "param_names";
-    for (auto& n : r.param_names) out << " " << n;
-    out << "\n";
-  }
-  for (auto& [k, v] : r.arrays) {
-    out << "array " << k << " " << v.size();
-    for (double x : v) out << " " << format_double(x);
-    out << "\n";
-  }
-  std::int64_t keep = r.T, stride = 1;
-  if (max_draws > 0 && r.T > max_draws) {
-    stride = (r.T + max_draws - 1) / max_draws;
-    keep = (r.T + stride - 1) / stride;
-  }
-  if (r.d > 0 && keep > 0) {
-    out << "posterior " << keep << " " << r.d << "\n";
-    for (std::int64_t j = 0; j < keep; ++j) {
-      const double* col = r.posterior.data() + (j * stride) * r.d;
-      for (std::int64_t i = 0; i < r.d; ++i) out << (i ? " " : "") << format_double(col[i]);
-      out << "\n";
-    }
-  }
-  out << "config_begin\n";
-  for (auto& line : r.config_lines) out << line << "\n";
-  out << "config_end\n";
-}
-
-inline RunReport read_report(const std::string& path) {
-  std::ifstream in(path);
-  if (!in) throw std::runtime_error("cannot open report: " + path);
-  std::string line;
-  if (!std::getline(in, line) || line != "specmc-report 1") throw std::runtime_error("not a specmc report: " + path);
-  RunReport r;
-  r.sampler.clear();
-  while (std::getline(in, line)) {
-    std::istringstream ss(line);
-    std::string tag;
-    if (!(ss >> tag)) continue;
-    if (tag == "sampler") {
-      ss >> r.sampler;
-    } else if (tag == "label") {
-      ss >> r.label;
-    } else if (tag == "diverged") {
-      int v = 0;
-      ss >> v;
-      r.diverged = v != 0;
-    } else if (tag == "scalar") {
-      std::string k, v;
-      ss >> k >> v;
-      const double x = parse_double(v);
-      if (k == "F")
-        r.F = x;
-      else if (k == "wall_seconds")
-        r.wall_seconds = x;
-      else
-        r.scalars[k] = x;
-    } else if (tag == "param_names") {
-      std::string n;
-      while (ss >> n) r.param_names.push_back(n);
-    } else if (tag == "array") {
-      std::string k, tok;
-      std::int64_t n = 0;
-      ss >> k >> n;
-      std::vector<double> v;
-      for (std::int64_t i = 0; i < n; ++i) {
-        if (!(ss >> tok)) throw std::runtime_error("short array in report: " + k);
-        v.push_back(parse_double(tok));
-      }
-      r.arrays[k] = v;
-    } else if (tag == "posterior") {
-      ss >> r.T >> r.d;
-      r.posterior.assign(static_cast<std::size_t>(r.T * r.d), 0.0);
-      std::string tok;
-      for (std::int64_t j = 0; j < r.T; ++j) {
-        if (!std::getline(in, line)) throw std::runtime_error("short posterior block");
-        std::istringstream rs(line);
-        for (std::int64_t i = 0; i < r.d; ++i) {
-          if (!(rs >> tok)) throw std::runtime_error("short posterior row");
-          r.posterior[j * r.d + i] = parse_double(tok);
-        }
-      }
-    } else if (tag == "config_begin") {
-      while (std::getline(in, line) && line != "config_end") r.config_lines.push_back(line);
-    } else {
-      throw std::runtime_error("unknown report tag: " + tag);
-    }
-  }
-  return r;
-}
+// The on-disk report (report.cpp:33-136) is written and read by the reference's
+// own report code: a RunReport filled by smc_run() goes through its
+// write_report() unchanged (integration/specmc_b200_cli.cpp links report.cpp).
 
 }  // namespace specmc_b200

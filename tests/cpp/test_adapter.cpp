@@ -99,29 +99,6 @@ int main(int argc, char** argv) {
     CHECK(r.posterior.size() == static_cast<size_t>(13 * 1024));
     std::printf("xrd F = %.4f\n", r.F);
   }
-  // report file format round trip (report.cpp:33-136)
-  {
-    RunReport r;
-    r.label = "t1";
-    r.F = 27.964921243765353;
-    r.wall_seconds = 0.125;
-    r.param_names = {"A1", "mu1"};
-    r.scalars = {{"T", 6.0}, {"n", 2.0}};
-    r.arrays = {{"ladder", {0.0, 0.1, 1.0}}};
-    r.d = 2;
-    r.T = 6;
-    for (int i = 0; i < 12; ++i) r.posterior.push_back(0.1 * i - 1e-7 * i * i);
-    r.config_lines = {"[smc]", "T = 6"};
-    const char* path = "/tmp/specmc_b200_adapter_report.txt";
-    write_report(r, path, 0);
-    const RunReport b = read_report(path);
-    CHECK(b.F == r.F && b.label == r.label && b.scalars == r.scalars && b.arrays == r.arrays);
-    CHECK(b.posterior == r.posterior && b.d == 2 && b.T == 6 && b.config_lines == r.config_lines);
-    write_report(r, path, 4);  // stride 2: draws 0, 2, 4
-    const RunReport c = read_report(path);
-    CHECK(c.T == 3 && c.posterior[2] == r.posterior[4] && c.posterior[4] == r.posterior[8]);
-    std::remove(path);
-  }
   std::printf("%s (%d failures)\n", fails ? "FAILED" : "OK", fails);
   return fails ? 1 : 0;
 }
