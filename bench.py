@@ -28,7 +28,7 @@ CPU side), plus the time to log-evidence for K = 1..Kmax (time_to_evidence_s).
             against the measured MUFU throughput of this GPU
             (specmc_probe_mufu).  executed / executed_frac: the MUFU lane-ops
             the kernel actually issues (counted by the library), fewer than
-            the algorithmic count (amplitude trials need no shape, four points
+            the algorithmic count (amplitude trials need no shape, two points
             share one noise rcp and lg2).
   cpu_baseline  the reference itself (oracle/_ref: the unchanged reference
             sources, Release flags for this host's ISA), smc_run with
@@ -302,7 +302,7 @@ def roofline(S, b: Bench, st, peak_mufu):
                     f"launch on its stream) x {alg_pt:g} MUFU per point-eval (SURVEY 8d: shape + noise term) / the "
                     "measured MUFU peak of this GPU (specmc_probe_mufu); executed = the MUFU lane-ops the kernel "
                     "issues (shape evaluations incl. block entries x MUFU per shape + trials x MUFU per noise "
-                    "term, padded slots; amplitude trials evaluate no shape, four points share a noise rcp/lg2)"}, pe_rate
+                    "term, padded slots; amplitude trials evaluate no shape, two points share a noise rcp and lg2)"}, pe_rate
 
 
 def problems_for(S, b: Bench, seed, device):
