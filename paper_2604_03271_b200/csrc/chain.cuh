@@ -117,9 +117,12 @@ __device__ __forceinline__ f2 shape_add2(const BlockC& b, f2 x, f2 acc) {
     return fma2(F2(b.c1), ex2f2(mul2(F2(b.c2), mul2(dx, dx))), acc);
   } else if (is_xps<FAM>()) {
     const f2 t = fma2(x, F2(b.c3), F2(b.mu));
-    const f2 nu = mul2(t, neg2(t));  // -u: the negation rides on the FMUL2 (MUFU.EX2 takes no negate)
+    if (FAM == FAM_XPSL) return add2(acc, rcpf2(fma2(mul2(t, t), F2(b.c2), F2(b.c2))));
+    // -u = t (-t), -t from its own FFMA2 over negated broadcast constants (free
+    // operand modifiers; ptxas negates a packed register with two scalar FADDs)
+    // -- bit-identical to -(t t): round-to-nearest is symmetric
+    const f2 nu = mul2(t, fma2(x, F2(-b.c3), F2(-b.mu)));
     const f2 r = rcpf2(fma2(nu, F2(-b.c2), F2(b.c2)));
-    if (FAM == FAM_XPSL) return add2(acc, r);
     return add2(fma2(F2(b.c1), ex2f2(nu), acc), r);
   } else {
     return add2(acc, F2(b.c1));
