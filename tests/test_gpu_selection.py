@@ -1,11 +1,13 @@
 """Model selection and posterior moments against the reference itself.
 
-Golden files tests/golden/selection_{C1,C2}.json hold, for 10 seeds
+Golden files tests/golden/selection_{C1,C2,C3}.json hold, for 10 seeds
 trial_seed(4242, t), the reference's F per K, its per-seed selected K and
 modal K, and the posterior mean/std at the true K (peak blocks sorted by
 centre per particle); tests/golden/make_selection_golden.py made them by
 running the unchanged reference sources (oracle/_ref) through smc_run as
-cmd_model_select does (proj/tools/specmc_main.cpp:147-170).
+cmd_model_select does (proj/tools/specmc_main.cpp:147-170).  C3 (T = 512)
+runs with SURVEY Appendix A's eta override, so on the GPU it takes the
+Lorentzian-basis kernel family.
 
 The B200 sampler runs the same K range, T, n and seeds (its own Philox
 streams: parity is statistical) and must
@@ -49,7 +51,7 @@ def _load(cfg):
     return json.loads(p.read_text())
 
 
-@pytest.fixture(scope="module", params=["C1", "C2"])
+@pytest.fixture(scope="module", params=["C1", "C2", "C3"])
 def runs(request, smc):
     g = _load(request.param)
     w = syn.config(g["config"], g["T"])
