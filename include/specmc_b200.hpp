@@ -6,6 +6,7 @@
 //   gm_model, xps_model             proj/src/model.cpp:121-136, :169-189
 //   SmcConfig, smc_run -> RunReport proj/include/specmc/smc.hpp:12-21, :78; proj/src/smc.cpp:218-249
 //   model_select                    proj/src/posterior.cpp:68-104
+//   RemcConfig, remc_run            proj/include/specmc/remc.hpp:14-22; proj/src/remc.cpp:170-190
 // Vectors replace Eigen types; the posterior is d x T column-major as the
 // reference's MatrixXd.  Config/model/spectrum violations throw
 // std::invalid_argument, numeric failures (max_levels, zero weight) and CUDA
@@ -327,6 +328,84 @@ inline std::vector<RunReport> smc_run_batch(const std::vector<Problem>& problems
 // RunReport smc_run(const ModelSpec&, const Spectrum&, const SmcConfig&) -- smc.cpp:218
 inline RunReport smc_run(const ModelSpec& spec, const Spectrum& data, const SmcConfig& cfg) {
   return smc_run_batch({Problem{spec, 0, cfg}}, {data}).front();
+}
+
+// ---- replica exchange (remc.hpp:14-22, remc.cpp:78-190): the paper's comparator
+struct RemcConfig {
+  int L = 44;                   // replicas above beta = 0
+  std::vector<double> ladder;   // explicit beta_0 .. beta_L; empty = geometric default
+  std::int64_t total_sweeps = 10000;
+  double burn_in_fraction = 0.5;
+  std::int64_t swap_period = 1;  // > total_sweeps disables swaps
+  std::uint64_t seed = 0;
+  int workers = 1;  // echoed in the report only
+  int device = 0;
+};
+
+struct RemcProblem {
+  ModelSpec spec;
+  int spectrum = 0;
+  RemcConfig cfg;
+};
+
+// every run of the batch concurrently on one GPU (one chain unit per replica)
+inline std::vector<RunReport> remc_run_batch(const std::vector<RemcProblem>& problems,
+                                             const std::vector<Spectrum>& spectra) {
+  std::vector<detail::Desc> descs;
+  descs.reserve(problems.size());
+  std::vector<specmc_remc_problem> ps;
+  for (const auto& p : problems) {
+    descs.push_back(detail::to_desc(p.spec));
+    const auto& c = p.cfg;
+    specmc_remc_config rc{c.L, c.ladder.empty() ? nullptr : c.ladder.data(), static_cast<std::int32_t>(c.ladder.size()),
+                          c.total_sweeps, c.burn_in_fraction, c.swap_period, c.seed, c.workers, c.device};
+    ps.push_back({descs.back().d, p.spectrum, rc});
+  }
+  std::vector<specmc_spectrum> ss;
+  for (const auto& s : spectra) {
+    if (s.xs.size() != s.ys.size()) throw std::invalid_argument("spectrum: xs/ys length mismatch");
+    ss.push_back({s.xs.data(), s.ys.data(), static_cast<std::int64_t>(s.xs.size())});
+  }
+  std::vector<specmc_remc_result> res(problems.size());
+  char err[1024] = {0};
+  const int rc = specmc_remc_run_batch(static_cast<std::int32_t>(ps.size()), ps.data(),
+                                       static_cast<std::int32_t>(ss.size()), ss.data(), res.data(), err, sizeof err);
+  std::vector<RunReport> out;
+  if (rc == SPECMC_OK) {
+    for (std::size_t i = 0; i < problems.size(); ++i) {
+      const auto& r = res[i];
+      const auto& c = problems[i].cfg;
+      RunReport rep;
+      rep.sampler = "remc";
+      rep.F = r.F;
+      rep.diverged = r.diverged != 0;
+      rep.wall_seconds = r.wall_seconds;
+      rep.device_seconds = r.device_seconds;
+      for (const auto& p : problems[i].spec.layout) rep.param_names.push_back(p.name);
+      rep.scalars = {{"L", static_cast<double>(r.R - 1)},
+                     {"total_sweeps", static_cast<double>(c.total_sweeps)},
+                     {"burn_in_fraction", c.burn_in_fraction},
+                     {"swap_period", static_cast<double>(c.swap_period)},
+                     {"seed", static_cast<double>(c.seed)},
+                     {"workers", static_cast<double>(c.workers)},
+                     {"n_data", static_cast<double>(spectra[problems[i].spectrum].xs.size())}};
+      rep.arrays["ladder"].assign(r.ladder, r.ladder + r.R);
+      rep.arrays["swap_rate"].assign(r.swap_rate, r.swap_rate + (r.R > 0 ? r.R - 1 : 0));
+      rep.arrays["replica_acc_rate"].assign(r.replica_acc, r.replica_acc + r.R);
+      rep.d = r.d;
+      rep.T = r.draws;
+      rep.posterior.assign(r.posterior, r.posterior + r.d * r.draws);
+      out.push_back(std::move(rep));
+    }
+  }
+  for (auto& r : res) specmc_remc_result_free(&r);
+  if (rc != SPECMC_OK) detail::raise(rc, err);
+  return out;
+}
+
+// RunReport remc_run(const ModelSpec&, const Spectrum&, const RemcConfig&) -- remc.cpp:170-190
+inline RunReport remc_run(const ModelSpec& spec, const Spectrum& data, const RemcConfig& cfg) {
+  return remc_run_batch({RemcProblem{spec, 0, cfg}}, {data}).front();
 }
 
 // posterior.cpp:68-104: argmin over K of the mean F; non-finite/diverged K excluded; ties keep the smaller K

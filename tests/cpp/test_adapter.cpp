@@ -99,6 +99,29 @@ int main(int argc, char** argv) {
     CHECK(r.posterior.size() == static_cast<size_t>(13 * 1024));
     std::printf("xrd F = %.4f\n", r.F);
   }
+  // replica exchange (remc.cpp:170-190): validation errors are invalid_argument,
+  // compute without a GPU is runtime_error; on the GPU a gm run reports the
+  // reference's RunReport fields
+  {
+    RemcConfig rc;
+    rc.L = 12;
+    rc.total_sweeps = 400;
+    rc.seed = 9;
+    RemcConfig rbad = rc;
+    rbad.burn_in_fraction = 1.5;
+    const ModelSpec g3 = gm_model(3, 0, 3, 0.1, GmMuPrior::UniformRange);
+    CHECK(throws<std::invalid_argument>([&] { remc_run(g3, data, rbad); }));
+    if (!gpu) {
+      CHECK(throws<std::runtime_error>([&] { remc_run(g3, data, rc); }));
+    } else {
+      const RunReport r = remc_run(g3, data, rc);
+      CHECK(r.sampler == "remc" && std::isfinite(r.F) && !r.diverged);
+      CHECK(r.arrays.at("ladder").size() == 13 && r.arrays.at("swap_rate").size() == 12);
+      CHECK(r.arrays.at("replica_acc_rate").size() == 13 && r.scalars.at("L") == 12.0);
+      CHECK(r.d == 9 && r.T == 200 && r.posterior.size() == static_cast<size_t>(9 * 200));
+      std::printf("remc F = %.4f\n", r.F);
+    }
+  }
   std::printf("%s (%d failures)\n", fails ? "FAILED" : "OK", fails);
   return fails ? 1 : 0;
 }
