@@ -605,9 +605,9 @@ __device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, 
   f2 run = F2(0.f);
 #pragma unroll
   for (int k = 0; k < PH; ++k) {
-    const float4 c = u.c4(k);  // (c_a, c_b, h_a, h_b)
+    const float4 c = u.c4(k);  // (c_a, c_b, -h_a, -h_b)
     run = fma2(make_float2(c.x, c.y), Pn[k], run);
-    if (kKeepC) Cn[k] = fma2(make_float2(-c.z, -c.w), Pn[k], run);
+    if (kKeepC) Cn[k] = fma2(make_float2(c.z, c.w), Pn[k], run);
   }
   float prefix, total;
   unit_scan(u, run.x + run.y, prefix, total);
@@ -627,7 +627,7 @@ __device__ __forceinline__ double eval_shirley_nz(const GroupDesc& g, Unit<PPL, 
       } else {
         const float4 c = u.c4(k);
         run2 = fma2(make_float2(c.x, c.y), Pn[k], run2);
-        Ck = fma2(make_float2(-c.z, -c.w), Pn[k], run2);
+        Ck = fma2(make_float2(c.z, c.w), Pn[k], run2);
       }
       return add2(Pn[k], fma2(S, Ck, base));
     });

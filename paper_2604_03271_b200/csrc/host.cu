@@ -516,7 +516,7 @@ PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, 
     return p < (size_t)N ? (int64_t)p : N - 1;
   };
   // pair-slot layout (chain.cuh): lane point k of lane l sits in slot
-  // k mod PH, component k / PH; x float2, weights float4 (c_a, c_b, h_a, h_b),
+  // k mod PH, component k / PH; x float2, weights float4 (c_a, c_b, -h_a, -h_b),
   // y float2 (-y_a, -y_b) or, for poisson, float4 (y_a, y_b, 1/s_a, 1/s_b)
   const int PH = s.PPL / 2;
   const bool y4 = ps.nz != NZ_POISSON;
@@ -530,7 +530,7 @@ PreparedSpectrum prepare_spectrum(const specmc_model_desc& m, const double* xs, 
     const double hk1 = q + 1 < N ? 0.5 * (xs[q + 1] - xs[q]) : 0.0;
     ps.x[2 * sidx + h] = (ps.uniform && !real) ? 1e30f : (float)(xs[q] - x_shift);
     ps.c[4 * sidx + h] = real ? (float)(hk + hk1) : 0.f;
-    ps.c[4 * sidx + 2 + h] = real ? (float)hk1 : 0.f;
+    ps.c[4 * sidx + 2 + h] = real ? (float)-hk1 : 0.f;  // negated: folded into the kernel's FFMA2
     if (y4) {  // negated: the kernel forms f - y with one FADD2 (only (f - y)^2 enters)
       ps.y[2 * sidx + h] = (float)-ys[q];
     } else {
